@@ -1,0 +1,194 @@
+"""CPU ORACLE protocol driver -- test infrastructure only.
+
+Runs a schedule of conv / activation layers for one image through the C
+restatement (oracle/ensei_oracle.c), mirroring AliceSession/BobSession
+(REF protocol.cpp:276-640) on one thread: Alice Enc -> Bob HomRec/ElementMult/
+HomShare -> Alice Dec, activations via trusted_activation semantics
+(REF protocol.cpp:237-268).
+
+Randomness comes from one of two providers that hand out per-polynomial arrays:
+
+* ``RefRandomness``    -- the reference's own mt19937_64 streams in the exact
+  consumption order of a reference session (Alice = Rng(seed).fork(0xA11CE):
+  keygen n Gaussians, then per conv layer per [channel][block] n Gaussians + n
+  uniform mod q, then per activation layer per element 1 uniform mod p;
+  Bob = Rng(seed).fork(0xB0B): per conv layer per [out][block] n uniform mod p).
+  Ciphertexts produced with it are bit-identical to the reference's wire frames.
+* ``PhiloxRandomness`` -- the counter-based streams the GPU kernels generate
+  (keyed by party seed; counter = (index, 0, stream id)); ternary secret,
+  CBD(k=20) noise (builder extension: no reference counterpart).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import (MTRng, PURPOSE_AHAT, PURPOSE_NOISE, PURPOSE_RESHARE, PURPOSE_SECRET,
+               PURPOSE_SHARE, SALT_ALICE, SALT_BOB, layer, lib, rand_cbd, rand_ternary,
+               rand_uniform_p, rand_uniform_q, stream_id)
+
+
+@dataclass
+class Conv:
+    fh: int
+    fw: int
+    same: bool
+    cin: int
+    cout: int
+
+
+@dataclass
+class Act:
+    fn: int  # 0 ReLU, 1 Square, 2 Identity
+
+
+def desc_rows(schedule):
+    """ref_harness layer descriptors: {kind, fh, fw, same, cin, cout, fn}."""
+    rows = []
+    for s in schedule:
+        if isinstance(s, Conv):
+            rows.append([0, s.fh, s.fw, int(s.same), s.cin, s.cout, 0])
+        else:
+            rows.append([1, 0, 0, 0, 0, 0, s.fn])
+    return rows
+
+
+class RefRandomness:
+    """Reference Rng streams (one session per image, seed = base + image)."""
+
+    def __init__(self, seed: int, n: int, q: int, p: int, sigma: float = 4.0):
+        self.alice = MTRng(seed, SALT_ALICE)
+        self.bob = MTRng(seed, SALT_BOB)
+        self.n, self.q, self.p, self.sigma = n, q, p, sigma
+
+    def secret(self):
+        return np.array([self.alice.gaussian(self.sigma) for _ in range(self.n)], np.int64)
+
+    def enc(self, layer_idx, cin, blocks):
+        e = np.empty((cin, blocks, self.n), np.int64)
+        a = np.empty((cin, blocks, self.n), np.uint64)
+        for c in range(cin):
+            for b in range(blocks):
+                e[c, b] = [self.alice.gaussian(self.sigma) for _ in range(self.n)]
+                a[c, b] = [self.alice.uniform_below(self.q) for _ in range(self.n)]
+        return e, a
+
+    def share(self, layer_idx, cout, blocks):
+        s = np.empty((cout, blocks, self.n), np.uint64)
+        for o in range(cout):
+            for b in range(blocks):
+                s[o, b] = [self.bob.uniform_below(self.p) for _ in range(self.n)]
+        return s
+
+    def reshare(self, layer_idx, ch, count):
+        return np.array([[self.alice.uniform_below(self.p) for _ in range(count)]
+                         for _ in range(ch)], np.uint64)
+
+
+class PhiloxRandomness:
+    """Counter-based streams (what the device kernels draw in throughput mode)."""
+
+    def __init__(self, seed: int, image: int, n: int, q: int, p: int, cbd_k: int = 20):
+        self.ka = lib().eo_fork_seed(seed, SALT_ALICE)
+        self.kb = lib().eo_fork_seed(seed, SALT_BOB)
+        self.image, self.n, self.q, self.p, self.k = image, n, q, p, cbd_k
+
+    def secret(self):
+        return rand_ternary(self.ka, stream_id(PURPOSE_SECRET, 0, 0, 0, 0), self.n)
+
+    def enc(self, layer_idx, cin, blocks):
+        e = np.empty((cin, blocks, self.n), np.int64)
+        a = np.empty((cin, blocks, self.n), np.uint64)
+        for c in range(cin):
+            for b in range(blocks):
+                e[c, b] = rand_cbd(self.ka, stream_id(PURPOSE_NOISE, layer_idx, self.image, c, b), self.n, self.k)
+                a[c, b] = rand_uniform_q(self.ka, stream_id(PURPOSE_AHAT, layer_idx, self.image, c, b), self.n, self.q)
+        return e, a
+
+    def share(self, layer_idx, cout, blocks):
+        s = np.empty((cout, blocks, self.n), np.uint64)
+        for o in range(cout):
+            for b in range(blocks):
+                s[o, b] = rand_uniform_p(self.kb, stream_id(PURPOSE_SHARE, layer_idx, self.image, o, b), self.n, self.p)
+        return s
+
+    def reshare(self, layer_idx, ch, count):
+        return np.stack([rand_uniform_p(self.ka, stream_id(PURPOSE_RESHARE, layer_idx, self.image, c, 0), count, self.p)
+                         for c in range(ch)])
+
+
+def secret_eval(L, t):
+    te = np.zeros(L.n, np.uint64)
+    lib().eo_secret_eval(C.byref(L), np.ascontiguousarray(t, np.int64), te)
+    return te
+
+
+def prepare_weights(L, w):
+    out = np.zeros(L.cout * L.cin * L.blocks * L.n, np.uint64)
+    lib().eo_prepare_weights(C.byref(L), np.ascontiguousarray(w, np.int64).reshape(-1), out)
+    return out.reshape(L.cout, L.cin, L.blocks, L.n)
+
+
+def run_layer(L, t_eval, alice_in, bob_prev, w_eval, e, a, s_b, want=()):
+    """One conv layer for one image. Returns dict with alice/bob shares (+ cts)."""
+    lb = lib()
+    n, B = L.n, L.blocks
+    ct = np.zeros(L.cin * B * 2 * n, np.uint64)
+    lb.eo_alice_encrypt(C.byref(L), t_eval, np.ascontiguousarray(alice_in, np.uint64).reshape(-1),
+                        np.ascontiguousarray(e, np.int64).reshape(-1),
+                        np.ascontiguousarray(a, np.uint64).reshape(-1), ct)
+    ct_out = np.zeros(L.cout * B * 2 * n, np.uint64)
+    bob_sh = np.zeros(L.cout * L.oh * L.ow, np.uint64)
+    prev = None if bob_prev is None else np.ascontiguousarray(bob_prev, np.uint64).reshape(-1)
+    lb.eo_bob_eval(C.byref(L), ct, np.ascontiguousarray(w_eval, np.uint64).reshape(-1),
+                   None if prev is None else prev.ctypes.data_as(C.c_void_p),
+                   np.ascontiguousarray(s_b, np.uint64).reshape(-1), ct_out, bob_sh)
+    al_sh = np.zeros(L.cout * L.oh * L.ow, np.uint64)
+    lb.eo_alice_decrypt(C.byref(L), t_eval, ct_out, al_sh)
+    r = {"alice": al_sh.reshape(L.cout, L.oh, L.ow), "bob": bob_sh.reshape(L.cout, L.oh, L.ow)}
+    if "ct" in want:
+        r["ct_in"] = ct.reshape(L.cin, B, 2, n)
+        r["ct_out"] = ct_out.reshape(L.cout, B, 2, n)
+    return r
+
+
+def run_protocol(schedule, image, weights, rand, q, p, n, want=()):
+    """Full schedule for one image. image: [cin][H][W] signed ints; weights: list of
+    [cout][cin][fh][fw] arrays (one per conv). Returns (output, trace)."""
+    t = rand.secret()
+    H, W = image.shape[1:]
+    alice = np.array([[[int(v) % p for v in row] for row in ch] for ch in image], np.uint64)
+    bob = None
+    t_eval = None
+    conv_i = 0
+    trace = []
+    out = None
+    for li, s in enumerate(schedule):
+        if isinstance(s, Conv):
+            L = layer(q, p, n, H, W, s.fh, s.fw, int(s.same), s.cin, s.cout)
+            if t_eval is None:
+                t_eval = secret_eval(L, t)
+            w_eval = prepare_weights(L, weights[conv_i])
+            e, a = rand.enc(li, s.cin, L.blocks)
+            s_b = rand.share(li, s.cout, L.blocks)
+            r = run_layer(L, t_eval, alice, bob, w_eval, e, a, s_b, want)
+            trace.append(r)
+            alice, bob = r["alice"], r["bob"]
+            H, W = L.oh, L.ow
+            conv_i += 1
+        else:
+            rec = (alice + bob) % np.uint64(p)
+            flat = np.ascontiguousarray(rec.reshape(-1))
+            if lib().eo_activation(flat, flat.size, p, s.fn) != 0:
+                raise OverflowError("square activation exceeds p_a/2")
+            val = flat.reshape(rec.shape)
+            fresh = rand.reshare(li, rec.shape[0], H * W).reshape(rec.shape)
+            if li + 1 == len(schedule):
+                out = val
+            alice = (val + np.uint64(p) - fresh) % np.uint64(p)
+            bob = fresh
+    if out is None:
+        out = (alice + bob) % np.uint64(p)
+    return out, trace

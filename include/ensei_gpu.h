@@ -1,0 +1,225 @@
+/*
+ * ensei_gpu.h -- C ABI of the B200-native ENSEI hot path (libensei_gpu.so).
+ *
+ * The reference (/root/reference/proj/core, "REF") exposes a C++ operator API in
+ * namespace ensei; it has no C ABI and no GPU code.  This header is the thin
+ * extern "C" layer the C++ host mirror (paper_2003_05328_b200/csrc/host/
+ * ensei_b200.hpp) and the Python ctypes binding call.  Every entry point names
+ * the REF interface it replaces.  Conventions:
+ *
+ *  - Plain pointers and sizes only.  Pointers named d_* are DEVICE pointers
+ *    (caller-allocated, caller-owned; no hidden allocations on hot calls);
+ *    h_* are host pointers.  `stream` is a cudaStream_t (NULL = legacy stream).
+ *  - Return value: 0 on success, else an ensei_status code that maps 1:1 onto
+ *    the REF exception hierarchy (REF errors.hpp:7-37); ensei_gpu_last_error()
+ *    gives the message (thread-local).
+ *  - Residues mod p travel as uint32 (p < 2^30); residues mod q as uint64.
+ *  - Evaluation-domain polynomials mod q live on the device in BIT-REVERSED slot
+ *    order ("device layout", like SEAL's NTT form).  ensei_gpu_permute() converts
+ *    to/from REF's natural slot order (slot k = x(psi^(2k+1))), which is what the
+ *    wire format and REF's ciphertexts use.
+ *  - Ciphertext array layout: [... ][2 (c0,c1)][R primes][n].  With R = 1 this is
+ *    REF's (c0 || c1) wire payload (REF wire.cpp:112-117) minus the tag and n.
+ */
+#ifndef ENSEI_GPU_H
+#define ENSEI_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ENSEI_GPU_ABI_VERSION 1
+
+typedef enum {
+  ENSEI_OK = 0,
+  ENSEI_ERR_GENERIC = 1,            /* ensei::Error */
+  ENSEI_ERR_ORDER_NOT_DIVIDING = 2, /* ensei::OrderNotDividing */
+  ENSEI_ERR_SEARCH_EXHAUSTED = 3,   /* ensei::SearchExhausted */
+  ENSEI_ERR_BAD_ROOT = 4,           /* ensei::BadRoot */
+  ENSEI_ERR_BAD_GEOMETRY = 5,       /* ensei::BadGeometry */
+  ENSEI_ERR_GEOMETRY_MISMATCH = 6,  /* ensei::GeometryMismatch */
+  ENSEI_ERR_DOMAIN_MISMATCH = 7,    /* ensei::DomainMismatch */
+  ENSEI_ERR_NOISE_EXHAUSTED = 8,    /* ensei::NoiseExhausted */
+  ENSEI_ERR_CHAIN_VIOLATION = 9,    /* ensei::ChainViolation */
+  ENSEI_ERR_LENGTH_MISMATCH = 10,   /* ensei::LengthMismatch */
+  ENSEI_ERR_RANGE_VIOLATION = 11,   /* ensei::RangeViolation */
+  ENSEI_ERR_PROTOCOL_ORDER = 12,    /* ensei::ProtocolOrderViolation */
+  ENSEI_ERR_RANGE_OVERFLOW = 13,    /* ensei::RangeOverflow */
+  ENSEI_ERR_MALFORMED_PAYLOAD = 14, /* ensei::MalformedPayload */
+  ENSEI_ERR_TRANSPORT = 15,         /* ensei::TransportError */
+  ENSEI_ERR_CUDA = 100,             /* CUDA runtime / launch failure */
+  ENSEI_ERR_UNSUPPORTED = 101,      /* valid for REF, not (yet) on this path */
+  ENSEI_ERR_INVALID_ARGUMENT = 102  /* null pointer, bad enum */
+} ensei_status;
+
+const char* ensei_gpu_last_error(void);
+int ensei_gpu_abi_version(void);
+
+/* ------------------------------------------------------------- context */
+typedef struct ensei_gpu_ctx ensei_gpu_ctx;
+
+#define ENSEI_MAX_PRIMES 4
+#define ENSEI_MOD_P 0xFFFFFFFFu /* selects the plaintext/image modulus p */
+
+/* RlweParams + ModulusChain::unified (REF ringbfv.cpp:65-87, hss.cpp:7-20):
+ * q = product of num_q NTT-friendly primes (num_q = 1 is REF's single-prime q;
+ * num_q > 1 is the RNS extension for large runs), p = p_N = p_A = p_E.
+ * Checks REF's invariants: every prime q_i and p are prime, == 1 mod 2n,
+ * q_i == 1 mod p, q > p; throws (returns) ENSEI_ERR_GENERIC otherwise.
+ * Builds canonical-root twiddle tables on `device`. */
+int ensei_gpu_ctx_create(int device, uint32_t n, const uint64_t* q_primes, uint32_t num_q,
+                         uint64_t p, ensei_gpu_ctx** out);
+void ensei_gpu_ctx_destroy(ensei_gpu_ctx* ctx);
+
+typedef struct {
+  uint32_t n, num_q;
+  uint64_t q[ENSEI_MAX_PRIMES];
+  uint64_t p;
+  uint64_t delta[ENSEI_MAX_PRIMES]; /* floor(Q/p) mod q_i  (REF ringbfv.cpp:80, Q = prod q_i) */
+  uint64_t psi_q[ENSEI_MAX_PRIMES]; /* canonical 2n-th roots (REF NegacyclicPlan::psi) */
+  uint64_t psi_p;
+  int device, sm_count;
+} ensei_ctx_info;
+int ensei_gpu_ctx_query(const ensei_gpu_ctx* ctx, ensei_ctx_info* info);
+
+/* ---------------------------------------------------- single transforms */
+#define ENSEI_LAYOUT_NATURAL 0 /* REF slot order */
+#define ENSEI_LAYOUT_BITREV 1  /* device evaluation layout */
+
+/* NegacyclicPlan::forward / ::inverse (REF ringbfv.cpp:49-59) over `count`
+ * contiguous length-n polynomials, in place.  modulus = prime index i < num_q
+ * (uint64 residues mod q_i) or ENSEI_MOD_P (uint64 residues mod p; this is
+ * encode_slots/decode_slots, REF ringbfv.cpp:109-125).  eval_layout selects the
+ * order of the evaluation side (output of forward, input of inverse).
+ * Inputs must be canonical residues; outputs are canonical. */
+int ensei_gpu_negacyclic(ensei_gpu_ctx* ctx, uint32_t modulus, int inverse, int eval_layout,
+                         uint64_t* d_data, size_t count, void* stream);
+
+/* ntt_2d / intt_2d (REF ntt.cpp:139-153): separable 2D cyclic transform over p
+ * with canonical roots, natural order on both sides, `count` rows x cols tiles
+ * (uint64 residues), in place.  rows, cols: powers of two in [1, 64]. */
+int ensei_gpu_ntt2d(ensei_gpu_ctx* ctx, int inverse, uint32_t rows, uint32_t cols,
+                    uint64_t* d_data, size_t count, void* stream);
+
+/* natural <-> bit-reversed order of `count` length-n uint64 polynomials */
+int ensei_gpu_permute(ensei_gpu_ctx* ctx, int to_natural, uint64_t* d_data, size_t count,
+                      void* stream);
+
+/* ------------------------------------------------------- conv layers */
+typedef struct {
+  uint32_t H, W;   /* input tile (REF ConvGeometry image_h/w) */
+  uint32_t fh, fw; /* filter */
+  uint32_t same;   /* 1 = ConvType::Same, 0 = Valid */
+  uint32_t cin, cout;
+} ensei_conv_desc;
+
+typedef struct {
+  uint32_t Lh, Lw;   /* padded grid (REF make_geometry, ntt.cpp:65-81) */
+  uint32_t blocks;   /* ciphertext blocks per channel, ceil(Lh*Lw/n) (REF protocol.cpp:180) */
+  uint32_t oh, ow;   /* output tile */
+  uint32_t r0, c0;   /* crop origin (REF ntt.hpp:44-49) */
+} ensei_layer_geom;
+
+/* make_geometry + plan_layers' block count. ENSEI_ERR_BAD_GEOMETRY as REF. */
+int ensei_gpu_layer_geometry(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
+                             ensei_layer_geom* geom);
+
+#define ENSEI_RAND_PHILOX 0   /* device counter-based streams (throughput mode) */
+#define ENSEI_RAND_INJECTED 1 /* caller-supplied draws (parity mode: REF's Rng stream) */
+
+typedef struct {
+  uint32_t mode;
+  uint32_t layer;      /* layer field of the stream ids */
+  uint32_t image_base; /* global index of the batch's first image (sharding-invariant) */
+  uint32_t cbd_k;      /* centered-binomial parameter for Enc noise (Philox mode) */
+  uint64_t alice_key;  /* Philox key of Alice's streams (Rng(seed).fork(0xA11CE) seed) */
+  uint64_t bob_key;    /* Philox key of Bob's streams   (Rng(seed).fork(0xB0B) seed) */
+  /* injected mode (natural slot order, per image / channel / block):           */
+  const int32_t* d_noise;  /* e0   [img][cin][B][n]   signed                    */
+  const uint64_t* d_a_hat; /* a^   [img][cin][B][R][n] canonical mod q_i        */
+  const uint32_t* d_share; /* s_B  [img][cout][B][n]  canonical mod p           */
+} ensei_randomness;
+
+/* keygen's evaluation form t_eval = NTT_q(t) (REF ringbfv.cpp:95-107) from
+ * signed coefficients d_t[n]; d_t_eval[R][n] in device layout. */
+int ensei_gpu_secret_from_coeffs(ensei_gpu_ctx* ctx, const int64_t* d_t, uint64_t* d_t_eval,
+                                 void* stream);
+/* ternary secret sampled from Philox (key = Alice key) -> t (optional) and t_eval */
+int ensei_gpu_secret_sample(ensei_gpu_ctx* ctx, uint64_t alice_key, int64_t* d_t,
+                            uint64_t* d_t_eval, void* stream);
+
+/* BobSession::prepare_weights + prepare_plain (REF protocol.cpp:462-502,
+ * ringbfv.cpp:265-280) for one layer: d_w[cout][cin][fh][fw] signed int32
+ * filter taps -> d_w_eval[cout][cin][B][R][n] (device layout).  t_setup. */
+int ensei_gpu_prepare_weights(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const int32_t* d_w,
+                              uint64_t* d_w_eval, void* stream);
+
+#define ENSEI_IN_U32 0 /* residues mod p */
+#define ENSEI_IN_U8 1  /* raw pixels (encode_signed of a non-negative value) */
+
+/* AliceSession::send_encrypted for `num_images` images (REF protocol.cpp:310-329):
+ * pad -> DFT2D -> flatten/split -> encrypt_freq_direct (REF ringbfv.cpp:180-201),
+ * fused in one kernel.  d_in[img][cin][H][W]; key_stride = 0 (one key) or R*n
+ * (per-image keys); d_ct[img][cin][B][2][R][n] in device layout. */
+int ensei_gpu_alice_encrypt(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
+                            const uint64_t* d_t_eval, uint32_t key_stride, const void* d_in,
+                            int in_dtype, uint32_t num_images, const ensei_randomness* rand,
+                            uint64_t* d_ct, void* stream);
+
+/* BobSession conv branch (REF protocol.cpp:537-607): optional HomRec with Bob's
+ * previous share d_bob_prev[img][cin][H][W] (NULL for the first layer), then
+ * ElementMult + channel accumulation (mul_plain/add_ct, REF ringbfv.cpp:233-306)
+ * with lazy 128-bit accumulation, then HomShare (REF hss.cpp:22-49) and Bob's
+ * share IDFT2D + crop.  d_ct_out[img][cout][B][2][R][n] (device layout),
+ * d_bob_share[img][cout][oh][ow]. */
+int ensei_gpu_bob_eval(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uint64_t* d_ct,
+                       const uint64_t* d_w_eval, const uint32_t* d_bob_prev, uint32_t num_images,
+                       const ensei_randomness* rand, uint64_t* d_ct_out, uint32_t* d_bob_share,
+                       void* stream);
+
+/* AliceSession::receive_shares (REF protocol.cpp:332-355): decrypt (REF
+ * ringbfv.cpp:203-231) -> merge -> IDFT2D -> crop, fused.  d_alice_share
+ * [img][cout][oh][ow]. */
+int ensei_gpu_alice_decrypt(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
+                            const uint64_t* d_t_eval, uint32_t key_stride, const uint64_t* d_ct_out,
+                            uint32_t num_images, uint32_t* d_alice_share, void* stream);
+
+/* recombine_clear (REF hss.cpp:64-73): out = (a + b) mod p */
+int ensei_gpu_recombine(ensei_gpu_ctx* ctx, const uint32_t* d_a, const uint32_t* d_b, size_t count,
+                        uint32_t* d_out, void* stream);
+
+/* Whole oblivious conv layer for a batch (Alice Enc -> Bob -> Alice Dec ->
+ * recombine), the batched equivalent of one conv step of run_inproc
+ * (REF protocol.cpp:670-692).  Workspace: ensei_gpu_conv_workspace_bytes(). */
+size_t ensei_gpu_conv_workspace_bytes(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
+                                      uint32_t num_images);
+int ensei_gpu_conv_layer(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uint64_t* d_t_eval,
+                         uint32_t key_stride, const uint64_t* d_w_eval, const void* d_in,
+                         int in_dtype, const uint32_t* d_bob_prev, uint32_t num_images,
+                         const ensei_randomness* rand, void* d_workspace, uint32_t* d_alice_share,
+                         uint32_t* d_bob_share, uint32_t* d_out, void* stream);
+
+/* Same with HOST buffers (pinned recommended): copies h_in to the device,
+ * runs the layer, copies the reconstructed output (and, if non-NULL, both
+ * shares) back, synchronously on `stream`.  d_workspace must also hold the
+ * staging input/output (ensei_gpu_conv_host_workspace_bytes()). */
+size_t ensei_gpu_conv_host_workspace_bytes(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
+                                           uint32_t num_images, int in_dtype);
+int ensei_gpu_conv_layer_host(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
+                              const uint64_t* d_t_eval, const uint64_t* d_w_eval, const void* h_in,
+                              int in_dtype, uint32_t num_images, const ensei_randomness* rand,
+                              void* d_workspace, uint32_t* h_out, void* stream);
+
+/* ------------------------------------------------------------ utilities */
+/* number of this library's kernels launched so far in the process */
+uint64_t ensei_gpu_launch_count(void);
+/* IMAD-pipe peak probe: returns mad.wide.u32 ops/s measured on `device` */
+double ensei_gpu_imad_peak(int device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ENSEI_GPU_H */

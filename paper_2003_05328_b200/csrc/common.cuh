@@ -1,0 +1,84 @@
+// common.cuh -- context layout, error plumbing and launch bookkeeping shared by the
+// kernels and the C ABI (include/ensei_gpu.h).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/ensei_gpu.h"
+#include "ntt_core.cuh"
+
+namespace ensei_gpu {
+
+// A C++ exception carrying an ensei_status; the ABI layer converts it to a code.
+struct Status : std::runtime_error {
+  int code;
+  Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& m) { throw Status(code, m); }
+inline void require(bool ok, int code, const char* m) {
+  if (!ok) fail(code, m);
+}
+#define EG_CUDA(x)                                                                      \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      ::ensei_gpu::fail(ENSEI_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+inline void check_launch(const char* what) {
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) fail(ENSEI_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  count_launch();
+}
+
+// Per-prime constants for Field64 kernels.
+struct PrimeConst {
+  Field64 f;
+  uint32_t cred;  // floor(2^64 / q) (fits 32 bits for q > 2^32), for reduce_lazy
+  uint64_t mu_hi, mu_lo;  // floor(2^128 / q)
+  uint64_t delta;         // floor(Q / p) mod q_i
+  uint64_t delta_shoup;   // Shoup companion of delta
+};
+
+struct PConst {
+  Field32 f;
+  uint32_t cred;  // floor(2^32 / p)
+  uint64_t m64;   // floor(2^64 / p)
+};
+
+// Device twiddle tables (TwPair = value + Shoup companion), see ntt_core.cuh for
+// the conventions.  Cyclic tables for L = 2^1 .. 2^6 live at offset L in tw_c_*.
+struct DeviceTables {
+  TwPair<uint64_t>* tw_q_fwd[ENSEI_MAX_PRIMES] = {};
+  TwPair<uint64_t>* tw_q_inv[ENSEI_MAX_PRIMES] = {};
+  TwPair<uint32_t>* tw_p_fwd = nullptr;  // negacyclic n-point over p
+  TwPair<uint32_t>* tw_p_inv = nullptr;
+  TwPair<uint32_t>* tw_c_fwd = nullptr;  // cyclic L-point over p, L <= 64
+  TwPair<uint32_t>* tw_c_inv = nullptr;
+};
+
+constexpr int kMaxTile = 64;  // largest supported padded grid side
+
+}  // namespace ensei_gpu
+
+struct ensei_gpu_ctx {
+  int device = 0;
+  int sm_count = 0;
+  uint32_t n = 0, logn = 0, R = 0;
+  uint64_t q[ENSEI_MAX_PRIMES] = {};
+  uint64_t p = 0;
+  uint64_t psi_q[ENSEI_MAX_PRIMES] = {};
+  uint64_t psi_p = 0;
+  ensei_gpu::PrimeConst pc[ENSEI_MAX_PRIMES];
+  ensei_gpu::PConst pp;
+  ensei_gpu::DeviceTables tab;
+  void* table_mem = nullptr;
+  bool approx_ok = true;  // every q_i < 2^61: approximate-quotient butterflies (MODE 0)
+};

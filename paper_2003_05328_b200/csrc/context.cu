@@ -1,0 +1,215 @@
+// context.cu -- C ABI: context creation (RlweParams/ModulusChain equivalent),
+// error mapping and the single-transform entry points.
+#include <algorithm>
+#include <memory>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "host_field.hpp"
+#include "kernels.cuh"
+
+namespace ensei_gpu {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local std::string g_last_error;
+
+template <class Fn>
+static int guarded(Fn&& fn) {
+  try {
+    fn();
+    return ENSEI_OK;
+  } catch (const Status& s) {
+    g_last_error = s.what();
+    return s.code;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return ENSEI_ERR_INVALID_ARGUMENT;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return ENSEI_ERR_GENERIC;
+  }
+}
+
+// exported for the other translation units
+int run_guarded(void (*fn)(void*), void* arg) {
+  return guarded([&] { fn(arg); });
+}
+void set_last_error(const std::string& s) { g_last_error = s; }
+
+static void build_tables(ensei_gpu_ctx* c) {
+  using namespace host;
+  const uint64_t n = c->n;
+  // layout: per prime fwd[n], inv[n] (16 B each) | p fwd[n], inv[n] (8 B) | cyclic fwd[128], inv[128]
+  size_t bytes_q = (size_t)c->R * 2 * n * sizeof(TwPair<uint64_t>);
+  size_t bytes_p = 2 * n * sizeof(TwPair<uint32_t>);
+  size_t bytes_c = 2 * 128 * sizeof(TwPair<uint32_t>);
+  std::vector<uint8_t> h(bytes_q + bytes_p + bytes_c);
+  auto* hq = reinterpret_cast<TwPair<uint64_t>*>(h.data());
+  for (uint32_t i = 0; i < c->R; ++i) {
+    TwiddleValues tv = make_twiddles(c->q[i], n, true);
+    for (uint64_t k = 0; k < n; ++k) {
+      hq[(2 * i) * n + k] = {tv.fwd[k], shoup64(tv.fwd[k], c->q[i])};
+      hq[(2 * i + 1) * n + k] = {tv.inv[k], shoup64(tv.inv[k], c->q[i])};
+    }
+    c->psi_q[i] = root_of_unity(2 * n, c->q[i]);
+  }
+  auto* hp = reinterpret_cast<TwPair<uint32_t>*>(h.data() + bytes_q);
+  {
+    TwiddleValues tv = make_twiddles(c->p, n, true);
+    for (uint64_t k = 0; k < n; ++k) {
+      hp[k] = {(uint32_t)tv.fwd[k], (uint32_t)shoup32(tv.fwd[k], c->p)};
+      hp[n + k] = {(uint32_t)tv.inv[k], (uint32_t)shoup32(tv.inv[k], c->p)};
+    }
+    c->psi_p = root_of_unity(2 * n, c->p);
+  }
+  auto* hc = reinterpret_cast<TwPair<uint32_t>*>(h.data() + bytes_q + bytes_p);
+  for (uint64_t L = 2; L <= (uint64_t)kMaxTile; L <<= 1) {
+    if ((c->p - 1) % L) continue;
+    TwiddleValues tv = make_twiddles(c->p, L, false);
+    for (uint64_t k = 0; k < L; ++k) {
+      hc[L + k] = {(uint32_t)tv.fwd[k], (uint32_t)shoup32(tv.fwd[k], c->p)};
+      hc[128 + L + k] = {(uint32_t)tv.inv[k], (uint32_t)shoup32(tv.inv[k], c->p)};
+    }
+  }
+  EG_CUDA(cudaMalloc(&c->table_mem, h.size()));
+  EG_CUDA(cudaMemcpy(c->table_mem, h.data(), h.size(), cudaMemcpyHostToDevice));
+  auto* dq = reinterpret_cast<TwPair<uint64_t>*>(c->table_mem);
+  for (uint32_t i = 0; i < c->R; ++i) {
+    c->tab.tw_q_fwd[i] = dq + (2 * i) * n;
+    c->tab.tw_q_inv[i] = dq + (2 * i + 1) * n;
+  }
+  auto* dp = reinterpret_cast<TwPair<uint32_t>*>(static_cast<uint8_t*>(c->table_mem) + bytes_q);
+  c->tab.tw_p_fwd = dp;
+  c->tab.tw_p_inv = dp + n;
+  auto* dc = reinterpret_cast<TwPair<uint32_t>*>(static_cast<uint8_t*>(c->table_mem) + bytes_q + bytes_p);
+  c->tab.tw_c_fwd = dc;
+  c->tab.tw_c_inv = dc + 128;
+}
+
+static void ctx_create(int device, uint32_t n, const uint64_t* qs, uint32_t R, uint64_t p,
+                       ensei_gpu_ctx** out) {
+  using namespace host;
+  require(out != nullptr && qs != nullptr, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+  require(R >= 1 && R <= ENSEI_MAX_PRIMES, ENSEI_ERR_INVALID_ARGUMENT, "num_q must be 1..4");
+  require(n >= 2 && (n & (n - 1)) == 0, ENSEI_ERR_GENERIC, "lattice dimension must be a power of two");
+  require(p >= 3 && p < (1ull << 30) && is_prime(p), ENSEI_ERR_GENERIC, "p must be a prime below 2^30");
+  require((p - 1) % (2 * (uint64_t)n) == 0, ENSEI_ERR_GENERIC, "p_e must be 1 mod 2n");
+  auto c = std::make_unique<ensei_gpu_ctx>();
+  c->device = device;
+  c->n = n;
+  c->logn = (uint32_t)ilog2(n);
+  c->R = R;
+  c->p = p;
+  for (uint32_t i = 0; i < R; ++i) {
+    uint64_t q = qs[i];
+    require(q > p && q < (1ull << 62) && is_prime(q), ENSEI_ERR_GENERIC, "q_i must be a prime in (p, 2^62)");
+    require((q - 1) % (2 * (uint64_t)n) == 0, ENSEI_ERR_GENERIC, "q must be 1 mod 2n");
+    require(q % p == 1, ENSEI_ERR_GENERIC, "q must be 1 mod p_e (keeps the plaintext-wrap term small)");
+    require(q > (1ull << 32), ENSEI_ERR_UNSUPPORTED, "q_i below 2^32 not supported on this path");
+    c->q[i] = q;
+    if (q >= (1ull << 61)) c->approx_ok = false;
+  }
+  // Delta = floor(Q / p) mod q_i.  Q == 1 mod p for every chain here (each q_i == 1 mod p),
+  // so Delta = (Q - 1) / p exactly; computed per prime without big integers:
+  // Delta mod q_i = -(p^-1) mod q_i  (since Delta*p = Q - 1 == -1 mod q_i).
+  for (uint32_t i = 0; i < R; ++i) {
+    uint64_t q = c->q[i];
+    uint64_t d = (R == 1) ? q / p : (q - invmod(p % q, q)) % q;
+    PrimeConst& pc = c->pc[i];
+    pc.f = Field64{q, 2 * q, (uint64_t)(0 - q), 4 * q};
+    pc.cred = (uint32_t)(((unsigned __int128)1 << 64) / q);
+    unsigned __int128 mu = ~(unsigned __int128)0 / q;
+    pc.mu_hi = (uint64_t)(mu >> 64);
+    pc.mu_lo = (uint64_t)mu;
+    pc.delta = d;
+    pc.delta_shoup = shoup64(d, q);
+  }
+  c->pp.f = Field32{(uint32_t)p, (uint32_t)(2 * p)};
+  c->pp.cred = (uint32_t)((1ull << 32) / p);
+  c->pp.m64 = (uint64_t)(((unsigned __int128)1 << 64) / p);
+  EG_CUDA(cudaSetDevice(device));
+  EG_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+  build_tables(c.get());
+  *out = c.release();
+}
+
+}  // namespace ensei_gpu
+
+using namespace ensei_gpu;
+
+extern "C" {
+
+const char* ensei_gpu_last_error(void) { return g_last_error.c_str(); }
+int ensei_gpu_abi_version(void) { return ENSEI_GPU_ABI_VERSION; }
+uint64_t ensei_gpu_launch_count(void) { return g_launches.load(); }
+
+int ensei_gpu_ctx_create(int device, uint32_t n, const uint64_t* q_primes, uint32_t num_q, uint64_t p,
+                         ensei_gpu_ctx** out) {
+  return guarded([&] { ctx_create(device, n, q_primes, num_q, p, out); });
+}
+
+void ensei_gpu_ctx_destroy(ensei_gpu_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->table_mem) cudaFree(ctx->table_mem);
+  delete ctx;
+}
+
+int ensei_gpu_ctx_query(const ensei_gpu_ctx* ctx, ensei_ctx_info* info) {
+  return guarded([&] {
+    require(ctx && info, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    std::memset(info, 0, sizeof(*info));
+    info->n = ctx->n;
+    info->num_q = ctx->R;
+    info->p = ctx->p;
+    info->psi_p = ctx->psi_p;
+    for (uint32_t i = 0; i < ctx->R; ++i) {
+      info->q[i] = ctx->q[i];
+      info->delta[i] = ctx->pc[i].delta;
+      info->psi_q[i] = ctx->psi_q[i];
+    }
+    info->device = ctx->device;
+    info->sm_count = ctx->sm_count;
+  });
+}
+
+int ensei_gpu_negacyclic(ensei_gpu_ctx* ctx, uint32_t modulus, int inverse, int eval_layout,
+                         uint64_t* d_data, size_t count, void* stream) {
+  return guarded([&] {
+    require(ctx && (d_data || count == 0), ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    require(modulus == ENSEI_MOD_P || modulus < ctx->R, ENSEI_ERR_INVALID_ARGUMENT, "bad modulus index");
+    require(eval_layout == ENSEI_LAYOUT_NATURAL || eval_layout == ENSEI_LAYOUT_BITREV,
+            ENSEI_ERR_INVALID_ARGUMENT, "bad layout");
+    negacyclic(ctx, modulus, inverse != 0, eval_layout == ENSEI_LAYOUT_NATURAL, d_data, count,
+               (cudaStream_t)stream);
+  });
+}
+
+int ensei_gpu_ntt2d(ensei_gpu_ctx* ctx, int inverse, uint32_t rows, uint32_t cols, uint64_t* d_data,
+                    size_t count, void* stream) {
+  return guarded([&] {
+    require(ctx && (d_data || count == 0), ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    auto lg = [](uint32_t v) {
+      int l = 0;
+      while ((1u << l) < v) ++l;
+      return l;
+    };
+    require(rows && cols && (rows & (rows - 1)) == 0 && (cols & (cols - 1)) == 0 && rows <= 64 && cols <= 64,
+            ENSEI_ERR_UNSUPPORTED, "tile sides must be powers of two <= 64 on this path");
+    require((ctx->p - 1) % rows == 0 && (ctx->p - 1) % cols == 0, ENSEI_ERR_BAD_GEOMETRY,
+            "tensor dims must divide p-1");
+    if (rows == 1 && cols == 1) return;  // identity
+    ntt2d(ctx, inverse != 0, lg(rows), lg(cols), d_data, count, (cudaStream_t)stream);
+  });
+}
+
+int ensei_gpu_permute(ensei_gpu_ctx* ctx, int to_natural, uint64_t* d_data, size_t count, void* stream) {
+  (void)to_natural;  // bit reversal is an involution
+  return guarded([&] {
+    require(ctx && (d_data || count == 0), ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    permute(ctx, d_data, count, (cudaStream_t)stream);
+  });
+}
+
+}  // extern "C"

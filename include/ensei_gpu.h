@@ -143,17 +143,21 @@ typedef struct {
   const uint32_t* d_share; /* s_B  [img][cout][B][n]  canonical mod p           */
 } ensei_randomness;
 
-/* keygen's evaluation form t_eval = NTT_q(t) (REF ringbfv.cpp:95-107) from
- * signed coefficients d_t[n]; d_t_eval[R][n] in device layout. */
-int ensei_gpu_secret_from_coeffs(ensei_gpu_ctx* ctx, const int64_t* d_t, uint64_t* d_t_eval,
+/* Secret-key blob: ENSEI_KEY_WORDS(n, R) uint64 = per prime [t_eval (device layout),
+ * Shoup companions floor(t_eval 2^64 / q_i)].  keygen's t_eval = NTT_q(t)
+ * (REF ringbfv.cpp:95-107) from signed coefficients d_t[n]: */
+#define ENSEI_KEY_WORDS(n, R) (2u * (uint32_t)(R) * (uint32_t)(n))
+int ensei_gpu_secret_from_coeffs(ensei_gpu_ctx* ctx, const int64_t* d_t, uint64_t* d_key,
                                  void* stream);
-/* ternary secret sampled from Philox (key = Alice key) -> t (optional) and t_eval */
+/* ternary secret sampled from Philox (key = Alice key) -> t (optional) and the blob */
 int ensei_gpu_secret_sample(ensei_gpu_ctx* ctx, uint64_t alice_key, int64_t* d_t,
-                            uint64_t* d_t_eval, void* stream);
+                            uint64_t* d_key, void* stream);
 
 /* BobSession::prepare_weights + prepare_plain (REF protocol.cpp:462-502,
  * ringbfv.cpp:265-280) for one layer: d_w[cout][cin][fh][fw] signed int32
- * filter taps -> d_w_eval[cout][cin][B][R][n] (device layout).  t_setup. */
+ * filter taps -> d_w_eval[cout][cin][B][R][n] uint64 in device layout (bit-reversed
+ * slots; each word packs the canonical value v as (v >> 30) << 32 | (v & (2^30-1)),
+ * the limb split the ElementMult accumulator uses).  t_setup, not on the online path. */
 int ensei_gpu_prepare_weights(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const int32_t* d_w,
                               uint64_t* d_w_eval, void* stream);
 
@@ -162,8 +166,9 @@ int ensei_gpu_prepare_weights(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, c
 
 /* AliceSession::send_encrypted for `num_images` images (REF protocol.cpp:310-329):
  * pad -> DFT2D -> flatten/split -> encrypt_freq_direct (REF ringbfv.cpp:180-201),
- * fused in one kernel.  d_in[img][cin][H][W]; key_stride = 0 (one key) or R*n
- * (per-image keys); d_ct[img][cin][B][2][R][n] in device layout. */
+ * fused in one kernel.  d_in[img][cin][H][W]; d_key = key blob(s), key_stride = 0
+ * (one key) or ENSEI_KEY_WORDS (per-image keys); d_ct[img][cin][B][2][R][n] in
+ * device layout. */
 int ensei_gpu_alice_encrypt(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
                             const uint64_t* d_t_eval, uint32_t key_stride, const void* d_in,
                             int in_dtype, uint32_t num_images, const ensei_randomness* rand,
@@ -174,8 +179,9 @@ int ensei_gpu_alice_encrypt(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
  * ElementMult + channel accumulation (mul_plain/add_ct, REF ringbfv.cpp:233-306)
  * with lazy 128-bit accumulation, then HomShare (REF hss.cpp:22-49) and Bob's
  * share IDFT2D + crop.  d_ct_out[img][cout][B][2][R][n] (device layout),
- * d_bob_share[img][cout][oh][ow]. */
-int ensei_gpu_bob_eval(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uint64_t* d_ct,
+ * d_bob_share[img][cout][oh][ow].  With d_bob_prev, HomRec updates d_ct in place
+ * (as REF's BobSession updates its received blocks, protocol.cpp:552-555). */
+int ensei_gpu_bob_eval(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint64_t* d_ct,
                        const uint64_t* d_w_eval, const uint32_t* d_bob_prev, uint32_t num_images,
                        const ensei_randomness* rand, uint64_t* d_ct_out, uint32_t* d_bob_share,
                        void* stream);

@@ -45,6 +45,9 @@ struct PrimeConst {
   uint64_t mu_hi, mu_lo;  // floor(2^128 / q)
   uint64_t delta;         // floor(Q / p) mod q_i
   uint64_t delta_shoup;   // Shoup companion of delta
+  uint64_t cp;            // floor(p * 2^64 / q), decryption rounding estimate
+  uint32_t a2_chunk;      // MAC: channels per full reduction of the top limb
+  uint64_t c64, c64p;     // 2^64 mod q and its Shoup companion
 };
 
 struct PConst {

@@ -125,6 +125,13 @@ static void ctx_create(int device, uint32_t n, const uint64_t* qs, uint32_t R, u
     pc.mu_lo = (uint64_t)mu;
     pc.delta = d;
     pc.delta_shoup = shoup64(d, q);
+    pc.cp = (uint64_t)(((unsigned __int128)p << 64) / q);
+    // A2 accumulates x1*y1 < ((q >> 30) + 1)^2 per channel; stay below 2^63
+    unsigned __int128 top = (unsigned __int128)((q >> 30) + 1) * ((q >> 30) + 1);
+    uint64_t cap = (uint64_t)(((unsigned __int128)1 << 63) / top);
+    pc.c64 = (uint64_t)(0 - q) % q;
+    pc.c64p = shoup64(pc.c64, q);
+    pc.a2_chunk = (uint32_t)std::max<uint64_t>(7, std::min<uint64_t>(56, cap / 7 * 7));
   }
   c->pp.f = Field32{(uint32_t)p, (uint32_t)(2 * p)};
   c->pp.cred = (uint32_t)((1ull << 32) / p);

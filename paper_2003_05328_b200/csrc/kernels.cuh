@@ -84,6 +84,23 @@ EG_DEV void tile_transform_2d(const Field32& f, uint32_t cred, const TwPair<uint
   }
 }
 
+// Global store of lazy transform outputs with the canonical reduction applied.
+template <int MODE, bool FWD>
+struct GlobalOut64 {
+  uint64_t* g;
+  Field64 f;
+  uint32_t cred;
+  static constexpr bool kVec = true;
+  EG_DEV uint64_t fin(uint64_t v) const {
+    return FWD ? Bfly<Field64, MODE>::fin_ct(f, v, cred) : Bfly<Field64, MODE>::fin_gs(f, v);
+  }
+  EG_DEV void operator()(int i, uint64_t v) const { g[i] = fin(v); }
+  EG_DEV void st2(int i, uint64_t a, uint64_t b) const {
+    *reinterpret_cast<ulonglong2*>(g + i) = make_ulonglong2(fin(a), fin(b));
+  }
+};
+using GlobalOut64Fwd = GlobalOut64<0, true>;
+
 // host launchers (ntt_kernels.cu)
 void negacyclic(const ensei_gpu_ctx* ctx, uint32_t modulus, bool inverse, bool natural, uint64_t* d,
                 size_t count, cudaStream_t st);

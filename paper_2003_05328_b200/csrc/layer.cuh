@@ -1,0 +1,514 @@
+// layer.cuh -- fused kernels of one oblivious conv layer (templates).
+//
+//   tile_enc_kernel   Alice Enc (REF protocol.cpp:310-329 + ringbfv.cpp:180-201):
+//                     pad -> DFT2D -> split -> encode (INTT_p) -> Delta*m + e -> NTT_q
+//                     -> c0 = -a^, c1 = a^ t^ + payload.   Variants: HomRec (Bob adds
+//                     NTT_q(Delta*INTT_p(DFT2D(share))) into c1, REF hss.cpp:51-62) and
+//                     weight preparation (REF protocol.cpp:462-502, ringbfv.cpp:265-280).
+//   share_kernel      Bob HomShare masks NTT_q(Delta*INTT_p(p - s_B)) (REF hss.cpp:22-49)
+//                     and Bob's time-domain share crop(IDFT2D(s_B)) (REF protocol.cpp:587-603).
+//   mac_kernel        ElementMult + channel accumulation (REF ringbfv.cpp:233-306,
+//                     protocol.cpp:570-581) as a tiled per-slot GEMM with lazy 128-bit
+//                     accumulation, + the HomShare mask on c1.
+//   dec_kernel        Alice Dec (REF ringbfv.cpp:203-231) -> merge -> IDFT2D -> crop
+//                     (REF protocol.cpp:332-355) [+ recombine_clear, REF hss.cpp:64-73].
+//
+// Data never round-trips through HBM inside a kernel: tiles, slot vectors and ring
+// polynomials live in shared memory between fused stages.
+#pragma once
+#include "common.cuh"
+#include "kernels.cuh"
+#include "philox.cuh"
+
+namespace ensei_gpu {
+
+constexpr int kLogE = 3;  // elements per thread in the ring transforms (E = 8)
+
+struct LayerArgs {
+  // geometry (REF ConvGeometry / LayerPlan)
+  int H, W, fh, fw, cin, cout;
+  int Lh, Lw, B, oh, ow, r0, c0, G;
+  int num_images;
+  // ring
+  PrimeConst pc[ENSEI_MAX_PRIMES];
+  PConst pp;
+  const TwPair<uint64_t>* twq_fwd[ENSEI_MAX_PRIMES];
+  const TwPair<uint64_t>* twq_inv[ENSEI_MAX_PRIMES];
+  const TwPair<uint32_t>* twp_fwd;
+  const TwPair<uint32_t>* twp_inv;
+  const TwPair<uint32_t>* twc_fwd;
+  const TwPair<uint32_t>* twc_inv;
+  // randomness
+  uint32_t rand_mode, layer, image_base, cbd_k;
+  uint64_t alice_key, bob_key;
+  const int32_t* inj_noise;
+  const uint64_t* inj_ahat;
+  const uint32_t* inj_share;
+};
+
+// ---------------------------------------------------------------- helpers
+
+// slot value at ring position j of block b read from a DFT2D tile stored
+// bit-reversed in both dimensions (S[brev(r)][brev(c)] = G[r][c]); 0 past the grid
+template <int LOGN, int LOGH, int LOGW>
+EG_DEV uint32_t gather_slot(const uint32_t* S, int b, int j, int G) {
+  const int flat = (b << LOGN) + brev(j, LOGN);
+  if (flat >= G) return 0;
+  const int r = flat >> LOGW, c = flat & ((1 << LOGW) - 1);
+  return S[brev(r, LOGH) * ((1 << LOGW) + 1) + brev(c, LOGW)];
+}
+
+// scatter of a decoded slot (ring position j of block b) into the bit-reversed tile
+template <int LOGN, int LOGH, int LOGW>
+EG_DEV void scatter_slot(uint32_t* S, int b, int j, int G, uint32_t v) {
+  const int flat = (b << LOGN) + brev(j, LOGN);
+  if (flat >= G) return;
+  const int r = flat >> LOGW, c = flat & ((1 << LOGW) - 1);
+  S[brev(r, LOGH) * ((1 << LOGW) + 1) + brev(c, LOGW)] = v;
+}
+
+// Delta_r * m mod q_r for m < p (R == 1: exact product, Delta*(p-1) < q)
+template <int R>
+EG_DEV uint64_t delta_mul(const PrimeConst& pc, uint32_t m) {
+  if constexpr (R == 1) {
+    return mulw(lo32(pc.delta), m) + ((uint64_t)(hi32(pc.delta) * m) << 32);
+  } else {
+    return Bfly<Field64, 0>::fin_gs(pc.f, pc.f.mul_shoup_approx(m, pc.delta, pc.delta_shoup));
+  }
+}
+
+EG_DEV uint64_t signed_mod(int32_t e, uint64_t q) { return e < 0 ? q - (uint64_t)(-(int64_t)e) : (uint64_t)e; }
+
+template <int R>
+__host__ __device__ constexpr int ct_words(int n) {
+  return 2 * R * n;
+}
+
+// ------------------------------------------------------------ tile -> ring
+
+enum TileMode { TILE_ENC = 0, TILE_HOMREC = 1, TILE_WEIGHTS = 2 };
+
+// One CTA per (image, channel) [ENC / HOMREC] or (out, in) filter [WEIGHTS].
+// NT = n/8 threads.  Shared: tile S (u32), ring buffer over p (u32), ring buffer
+// over q (u64), noise cache for R > 1.
+template <int LOGN, int LOGH, int LOGW, int R, int MODE, int TM, bool INJ, int IN_T>
+__global__ void __launch_bounds__((1 << LOGN) >> kLogE)
+    tile_enc_kernel(LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride,
+                    const void* __restrict__ in, uint64_t* __restrict__ out) {
+  constexpr int N = 1 << LOGN, NT = N >> kLogE;
+  constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* pbuf = reinterpret_cast<uint32_t*>(qbuf + N);
+  uint32_t* S = pbuf + ssize<uint32_t>(N);
+  int8_t* ecache = reinterpret_cast<int8_t*>(S + Lh * LS);
+  const int tid = threadIdx.x;
+  const CtaBar bar;
+  const Field32 pf = a.pp.f;
+  const uint32_t p = pf.q;
+
+  // which tile: ENC/HOMREC -> (img, c); WEIGHTS -> (o, c)
+  const int item = blockIdx.x;
+  const int ch = item % a.cin;
+  const int img = item / a.cin;  // image (or output channel for WEIGHTS)
+  const int th = TM == TILE_WEIGHTS ? a.fh : a.H, tw = TM == TILE_WEIGHTS ? a.fw : a.W;
+
+  // 1. pad into the tile (REF pad_image / pad_residues, ntt.cpp:155-185)
+  for (int i = tid; i < Lh * Lw; i += NT) {
+    const int r = i >> LOGW, c = i & (Lw - 1);
+    uint32_t v = 0;
+    if (r < th && c < tw) {
+      const size_t src = ((size_t)item * th + r) * tw + c;
+      if constexpr (TM == TILE_WEIGHTS) {
+        const int32_t w = static_cast<const int32_t*>(in)[src];
+        int64_t m = (int64_t)w % (int64_t)p;
+        v = (uint32_t)(m < 0 ? m + p : m);  // encode_signed
+      } else if constexpr (IN_T == ENSEI_IN_U8) {
+        v = static_cast<const uint8_t*>(in)[src];
+      } else {
+        v = static_cast<const uint32_t*>(in)[src] % p;
+      }
+    }
+    S[r * LS + c] = v;
+  }
+  __syncthreads();
+  // 2. DFT2D (rows then columns; output bit-reversed in both dims)
+  tile_transform_2d<false, LOGH, LOGW>(pf, a.pp.cred, a.twc_fwd, S, LS);
+
+  const uint64_t* kimg = key + (size_t)(TM == TILE_ENC ? img : 0) * key_stride;
+  const int gimg = a.image_base + img;
+  for (int b = 0; b < a.B; ++b) {
+    // 3. encode_slots: INTT_p of the block's slots (gathered from the tile)
+    {
+      auto src = [&](int j) { return gather_slot<LOGN, LOGH, LOGW>(S, b, j, a.G); };
+      SmemRW<uint32_t> dst_raw{pbuf};
+      auto dst = [&](int i, uint32_t v) { dst_raw(i, Bfly<Field32, 0>::fin_gs(pf, v)); };
+      ntt_inverse<Field32, uint32_t, LOGN, kLogE, 0, false, false>(pf, a.twp_inv, pbuf, tid, src, dst, bar);
+    }
+    if constexpr (TM == TILE_ENC && R > 1) {  // noise drawn once, shared by all primes
+      for (int i = tid; i < N; i += NT) {
+        int32_t e = INJ ? a.inj_noise[(((size_t)img * a.cin + ch) * a.B + b) * N + i]
+                        : draw_cbd(a.alice_key, stream_id(PURPOSE_NOISE, a.layer, gimg, ch, b), i, a.cbd_k);
+        ecache[i] = (int8_t)e;
+      }
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) {
+      const PrimeConst pc = a.pc[r];
+      const Field64 f = pc.f;
+      // 4. lift to q_r: Delta*m + e (ENC), Delta*m (HOMREC), centered lift (WEIGHTS)
+      auto src = [&](int i) -> uint64_t {
+        const uint32_t m = pbuf[sidx<uint32_t>(i)];
+        if constexpr (TM == TILE_WEIGHTS) {
+          return m > p / 2 ? f.q - (uint64_t)(p - m) : (uint64_t)m;  // encode_signed(decode_signed(m))
+        } else {
+          uint64_t x = delta_mul<R>(pc, m);
+          if constexpr (TM == TILE_ENC) {
+            int32_t e;
+            if constexpr (R > 1) e = ecache[i];
+            else
+              e = INJ ? a.inj_noise[(((size_t)img * a.cin + ch) * a.B + b) * N + i]
+                      : draw_cbd(a.alice_key, stream_id(PURPOSE_NOISE, a.layer, gimg, ch, b), i, a.cbd_k);
+            x += signed_mod(e, f.q);
+            if (x >= f.q) x -= f.q;
+          }
+          return x;
+        }
+      };
+      // 5. NTT_q + epilogue at the device (bit-reversed) position j
+      uint64_t* obase;
+      if constexpr (TM == TILE_WEIGHTS) obase = out + ((((size_t)img * a.cin + ch) * a.B + b) * R + r) * N;
+      else obase = out + (((size_t)img * a.cin + ch) * a.B + b) * ct_words<R>(N);
+      auto dst = [&](int j, uint64_t v) {
+        const uint64_t x = Bfly<Field64, 0>::fin_ct(f, v, pc.cred);
+        if constexpr (TM == TILE_WEIGHTS) {
+          obase[j] = ((x >> 30) << 32) | (x & 0x3FFFFFFFull);  // 30-bit limbs for the MAC
+        } else if constexpr (TM == TILE_HOMREC) {
+          uint64_t* c1 = obase + (size_t)(R + r) * N;
+          uint64_t y = c1[j] + x;
+          c1[j] = y >= f.q ? y - f.q : y;
+        } else {
+          const int k = brev(j, LOGN);  // natural slot index keys the a^ stream
+          const uint64_t ah = INJ ? a.inj_ahat[((((size_t)img * a.cin + ch) * a.B + b) * R + r) * N + k]
+                                  : draw_uniform_q(a.alice_key,
+                                                   stream_id(PURPOSE_AHAT, a.layer, gimg, ch, b | (r << 12)), k, f.q);
+          const uint64_t t = kimg[(size_t)(2 * r) * N + j], tp = kimg[(size_t)(2 * r + 1) * N + j];
+          uint64_t c1 = Bfly<Field64, 0>::fin_gs(f, f.mul_shoup_approx(ah, t, tp)) + x;
+          c1 = c1 >= f.q ? c1 - f.q : c1;
+          obase[(size_t)r * N + j] = ah ? f.q - ah : 0;
+          obase[(size_t)(R + r) * N + j] = c1;
+        }
+      };
+      ntt_forward<Field64, uint64_t, LOGN, kLogE, 0, false, false>(f, a.twq_fwd[r], qbuf, tid, src, dst, bar,
+                                                                   pc.cred);
+      __syncthreads();
+    }
+  }
+}
+
+template <int LOGN, int LOGH, int LOGW, int R>
+constexpr size_t tile_enc_smem() {
+  return (size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4 + (size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4 +
+         (R > 1 ? (1 << LOGN) : 0);
+}
+
+// ------------------------------------------------------- HomShare + Bob share
+
+// One CTA per (image, out channel).  M[img][o][b][r][n] = NTT_q(Delta*INTT_p(p - s_B))
+// (device layout) and bob_share[img][o][oh][ow] = crop(IDFT2D(merge(s_B))).
+template <int LOGN, int LOGH, int LOGW, int R, bool INJ>
+__global__ void __launch_bounds__((1 << LOGN) >> kLogE)
+    share_kernel(LayerArgs a, uint64_t* __restrict__ mask, uint32_t* __restrict__ bob_share) {
+  constexpr int N = 1 << LOGN, NT = N >> kLogE;
+  constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* pbuf = reinterpret_cast<uint32_t*>(qbuf + N);
+  uint32_t* S = pbuf + ssize<uint32_t>(N);
+  const int tid = threadIdx.x;
+  const CtaBar bar;
+  const Field32 pf = a.pp.f;
+  const uint32_t p = pf.q;
+  const int item = blockIdx.x;  // img * cout + o
+  const int o = item % a.cout, img = item / a.cout;
+  const int gimg = a.image_base + img;
+  auto share = [&](int b, int l) -> uint32_t {  // s_B at natural slot l of block b
+    return INJ ? a.inj_share[(((size_t)img * a.cout + o) * a.B + b) * N + l]
+               : draw_uniform_p(a.bob_key, stream_id(PURPOSE_SHARE, a.layer, gimg, o, b), l, p);
+  };
+  for (int b = 0; b < a.B; ++b) {
+    auto src = [&](int j) {
+      const uint32_t s = share(b, brev(j, LOGN));
+      return s == 0 ? 0u : p - s;  // (p_A - s_B) mod p_E  (REF hss.cpp:33-35)
+    };
+    SmemRW<uint32_t> dst_raw{pbuf};
+    auto dst = [&](int i, uint32_t v) { dst_raw(i, Bfly<Field32, 0>::fin_gs(pf, v)); };
+    ntt_inverse<Field32, uint32_t, LOGN, kLogE, 0, false, false>(pf, a.twp_inv, pbuf, tid, src, dst, bar);
+    __syncthreads();
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) {
+      const PrimeConst pc = a.pc[r];
+      const Field64 f = pc.f;
+      auto qsrc = [&](int i) { return delta_mul<R>(pc, pbuf[sidx<uint32_t>(i)]); };
+      // mask lands where c1 of the output ciphertext (img, o, b) lives
+      uint64_t* mo = mask + ((size_t)item * a.B + b) * ct_words<R>(N) + (size_t)(R + r) * N;
+      GlobalOut64Fwd out{mo, f, pc.cred};
+      ntt_forward<Field64, uint64_t, LOGN, kLogE, 0, false, false>(f, a.twq_fwd[r], qbuf, tid, qsrc, out, bar,
+                                                                   pc.cred);
+      __syncthreads();
+    }
+  }
+  // Bob's share: IDFT2D of the merged s_B grid, cropped (REF protocol.cpp:593-602)
+  for (int i = tid; i < Lh * Lw; i += NT) {
+    const int r = i >> LOGW, c = i & (Lw - 1);
+    const int flat = i;  // natural grid position (r, c)
+    S[brev(r, LOGH) * LS + brev(c, LOGW)] = share(flat >> LOGN, flat & (N - 1));
+  }
+  __syncthreads();
+  tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, S, LS);
+  uint32_t* bs = bob_share + (size_t)item * a.oh * a.ow;
+  for (int i = tid; i < a.oh * a.ow; i += NT) {
+    const int r = i / a.ow, c = i % a.ow;
+    bs[i] = S[(r + a.r0) * LS + c + a.c0];
+  }
+}
+
+template <int LOGN, int LOGH, int LOGW>
+constexpr size_t share_smem() {
+  return (size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4 + (size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4;
+}
+
+// ---------------------------------------------------------------- decrypt
+
+// phi = c0 t^ + c1 (device layout) as the input view of the decryption INTT;
+// reduced to [0, 4q + 2^32) for the Gentleman-Sande bounds.
+struct PhiSrc {
+  const uint64_t *c0, *c1, *t, *tp;
+  Field64 f;
+  static constexpr bool kVec = true;
+  EG_DEV uint64_t at(int j) const {
+    uint64_t x = f.mul_shoup_approx(c0[j], t[j], tp[j]) + c1[j];  // < 5q
+    return hi32(x) > hi32(f.q4) ? x - f.q4 : x;
+  }
+  EG_DEV uint64_t operator()(int j) const { return at(j); }
+  EG_DEV void ld2(int j, uint64_t& x, uint64_t& y) const {
+    x = at(j);
+    y = at(j + 1);
+  }
+};
+
+
+// One CTA per (image, out channel): phi = c0 t^ + c1 -> INTT_q -> round(p phi / q)
+// -> decode (NTT_p) -> scatter into the tile -> IDFT2D -> crop (-> + Bob's share).
+template <int LOGN, int LOGH, int LOGW>
+__global__ void __launch_bounds__((1 << LOGN) >> kLogE)
+    dec_kernel(LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride,
+               const uint64_t* __restrict__ ct, uint32_t* __restrict__ alice_share,
+               const uint32_t* __restrict__ bob_share, uint32_t* __restrict__ outp) {
+  constexpr int N = 1 << LOGN, NT = N >> kLogE;
+  constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* pbuf = reinterpret_cast<uint32_t*>(qbuf + N);
+  uint32_t* S = pbuf + ssize<uint32_t>(N);
+  const int tid = threadIdx.x;
+  const CtaBar bar;
+  const Field32 pf = a.pp.f;
+  const uint32_t p = pf.q;
+  const int item = blockIdx.x;  // img * cout + o
+  const int img = item / a.cout;
+  const uint64_t* kimg = key + (size_t)img * key_stride;
+  const PrimeConst pc = a.pc[0];
+  const Field64 f = pc.f;
+  const uint64_t cp = pc.cp, h = f.q >> 1;  // floor(p 2^64 / q), floor(q / 2)
+  for (int i = tid; i < Lh * LS; i += NT) S[i] = 0;
+  for (int b = 0; b < a.B; ++b) {
+    const uint64_t* cb = ct + ((size_t)item * a.B + b) * ct_words<1>(N);
+    // 1. phi (device layout) -> INTT_q -> natural coefficients
+    PhiSrc src{cb, cb + N, kimg, kimg + N, f};
+    auto dst = [&](int i, uint64_t v) {
+      const uint64_t phi = Bfly<Field64, 0>::fin_gs(f, v);
+      // exact floor((p phi + floor(q/2)) / q) (REF ringbfv.cpp:224-229): the estimate
+      // Q = floor(phi cp / 2^64) is at most 2 below, so the remainder is < 3q and exact
+      // in 64-bit arithmetic; correct upward.
+      uint64_t Q = mulhi64(phi, cp);
+      uint64_t rem = (uint64_t)p * phi + h - Q * f.q;
+      while (rem >= f.q) {
+        rem -= f.q;
+        ++Q;
+      }
+      pbuf[sidx<uint32_t>(i)] = (uint32_t)(Q % p);
+    };
+    ntt_inverse<Field64, uint64_t, LOGN, kLogE, 0, false, false>(f, a.twq_inv[0], qbuf, tid, src, dst, bar);
+    __syncthreads();
+    // 2. decode_slots (NTT_p) -> scatter into the bit-reversed tile
+    SmemRW<uint32_t> psrc{pbuf};
+    auto pdst = [&](int j, uint32_t v) { scatter_slot<LOGN, LOGH, LOGW>(S, b, j, a.G, reduce_lazy(pf, v, a.pp.cred)); };
+    ntt_forward<Field32, uint32_t, LOGN, kLogE, 0, false, false>(pf, a.twp_fwd, pbuf, tid, psrc, pdst, bar);
+    __syncthreads();
+  }
+  // 3. IDFT2D + crop (+ recombine with Bob's share)
+  tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, S, LS);
+  const size_t base = (size_t)item * a.oh * a.ow;
+  for (int i = tid; i < a.oh * a.ow; i += NT) {
+    const int r = i / a.ow, c = i % a.ow;
+    const uint32_t s = S[(r + a.r0) * LS + c + a.c0];
+    if (alice_share) alice_share[base + i] = s;
+    if (outp) {
+      uint32_t y = s + bob_share[base + i];
+      outp[base + i] = y >= p ? y - p : y;
+    }
+  }
+}
+
+// ------------------------------------------------------------ ElementMult
+
+// Z = A2 2^60 + A1 2^30 + A0 (A0, A1 < 2^63, A2 < 2^63) -> Z mod q, canonical.
+// Z = hi 2^64 + lo; lo -> [0,3q) by corr, hi * (2^64 mod q) by Shoup (< 4q).
+EG_DEV uint64_t mac_reduce(const Field64& f, const PrimeConst& pc, uint64_t a0, uint64_t a1, uint64_t a2) {
+  constexpr uint64_t M30 = (1ull << 30) - 1;
+  a1 += a0 >> 30;
+  a0 &= M30;
+  a2 += a1 >> 30;
+  a1 &= M30;
+  const uint64_t lo = (a2 << 60) | (a1 << 30) | a0, hi = a2 >> 4;
+  uint64_t x = Bfly<Field64, 0>::corr(f, lo, pc.cred);
+  if (hi) x += f.mul_shoup_approx(hi, pc.c64, pc.c64p);  // < 7q
+  return Bfly<Field64, 0>::fin_ct(f, x, pc.cred);
+}
+
+// Per slot s (ring position of one (block, prime)), the rows (img, comp) times
+// cols (out channel) product over K = cin:  out = sum_c ct[img][c][comp] w[o][c]
+// (mod q), + mask on comp 1.  Lazy accumulation with 30-bit limbs: for x, y < 2^60,
+// x = x1 2^30 + x0, y = y1 2^30 + y0; A0 += x0 y0, A1 += x0 y1 + x1 y0, A2 += x1 y1
+// (four full-rate mad.wide per MAC, no carries), folded every 8 channels and reduced
+// once per output.  The tile is staged in shared memory so every ct / weight word is
+// read from HBM once per CTA.
+template <int R, int S, int MT, int NTL, int KT>
+__global__ void __launch_bounds__(S*(MT / 4) * (NTL / 4))
+    mac_kernel(LayerArgs a, int logn, const uint64_t* __restrict__ ct, const uint64_t* __restrict__ w,
+               int has_mask, uint64_t* __restrict__ out) {
+  constexpr int TMR = MT / 4, TNC = NTL / 4, NTH = S * TMR * TNC;
+  __shared__ uint64_t As[KT][S][MT + 1];
+  __shared__ uint64_t Bs[KT][S][NTL + 1];
+  const int n = 1 << logn;
+  const int BR = a.B * R;                  // (block, prime) pairs
+  const int s0 = blockIdx.x * S;           // first slot of this CTA over BR*n
+  const int bp = s0 >> logn;               // (b, r) pair
+  const int r = bp % R;
+  const int k0 = s0 & (n - 1);
+  const int rows = 2 * a.num_images, cols = a.cout, K = a.cin;
+  const int row0 = blockIdx.y * MT, col0 = blockIdx.z * NTL;
+  const int tid = threadIdx.x;
+  const int sl = tid % S, tm = (tid / S) % TMR, tn = tid / (S * TMR);
+  const PrimeConst pc = a.pc[r];
+  const Field64 f = pc.f;
+  const size_t ctw = (size_t)ct_words<R>(n);
+  // ct word address: ((img*cin + c)*B + b)*2Rn + (comp*R + r)*n + k
+  auto ct_addr = [&](int row, int c, int k) -> size_t {
+    const int img = row >> 1, comp = row & 1;
+    return (((size_t)img * a.cin + c) * a.B + bp / R) * ctw + (size_t)(comp * R + r) * n + k;
+  };
+  uint64_t A0[4][4], A1[4][4], A2[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) A0[i][j] = A1[i][j] = A2[i][j] = 0;
+  constexpr uint64_t M30 = (1ull << 30) - 1;
+  int since_fold = 0, since_full = 0;
+  for (int kc = 0; kc < K; kc += KT) {
+    __syncthreads();
+    for (int e = tid; e < KT * MT * S; e += NTH) {
+      const int s = e % S, row = (e / S) % MT, kk = e / (S * MT);
+      const int gr = row0 + row, c = kc + kk;
+      uint64_t x = 0;
+      if (gr < rows && c < K) {
+        x = ct[ct_addr(gr, c, k0 + s)];
+        x = ((x >> 30) << 32) | (x & M30);
+      }
+      As[kk][s][row] = x;
+    }
+    for (int e = tid; e < KT * NTL * S; e += NTH) {
+      const int s = e % S, col = (e / S) % NTL, kk = e / (S * NTL);
+      const int go = col0 + col, c = kc + kk;
+      uint64_t x = 0;
+      if (go < cols && c < K) x = w[(((size_t)go * a.cin + c) * BR + bp) * n + k0 + s];
+      Bs[kk][s][col] = x;
+    }
+    __syncthreads();
+    const int kmax = min(KT, K - kc);
+    for (int kk = 0; kk < kmax; ++kk) {
+      uint32_t x0[4], x1[4], y0[4], y1[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint64_t v = As[kk][sl][tm * 4 + i];
+        x0[i] = lo32(v);
+        x1[i] = hi32(v);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t v = Bs[kk][sl][tn * 4 + j];
+        y0[j] = lo32(v);
+        y1[j] = hi32(v);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          A0[i][j] = madw(x0[i], y0[j], A0[i][j]);
+          A1[i][j] = madw(x0[i], y1[j], A1[i][j]);
+          A1[i][j] = madw(x1[i], y0[j], A1[i][j]);
+          A2[i][j] = madw(x1[i], y1[j], A2[i][j]);
+        }
+      ++since_fold;
+      ++since_full;
+      if (since_fold == 7) {  // A1 gains < 2^61 per channel: fold before overflow
+        since_fold = 0;
+        if (since_full >= (int)pc.a2_chunk) {  // top limb near capacity: reduce mod q
+          since_full = 0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint64_t z = mac_reduce(f, pc, A0[i][j], A1[i][j], A2[i][j]);
+              A0[i][j] = z & M30;
+              A1[i][j] = z >> 30;
+              A2[i][j] = 0;
+            }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              A1[i][j] += A0[i][j] >> 30;
+              A0[i][j] &= M30;
+              A2[i][j] += A1[i][j] >> 30;
+              A1[i][j] &= M30;
+            }
+        }
+      }
+    }
+  }
+  const int k = k0 + sl;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gr = row0 + tm * 4 + i;
+    if (gr >= rows) continue;
+    const int img = gr >> 1, comp = gr & 1;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int go = col0 + tn * 4 + j;
+      if (go >= cols) continue;
+      uint64_t x = mac_reduce(f, pc, A0[i][j], A1[i][j], A2[i][j]);
+      const size_t oa = (((size_t)img * a.cout + go) * a.B + bp / R) * ctw + (size_t)(comp * R + r) * n + k;
+      if (comp == 1 && has_mask) {  // HomShare mask written in place by share_kernel
+        x += out[oa];
+        x = x >= f.q ? x - f.q : x;
+      }
+      out[oa] = x;
+    }
+  }
+}
+
+}  // namespace ensei_gpu

@@ -1,0 +1,393 @@
+// layer_api.cu -- C ABI of the conv-layer path (include/ensei_gpu.h): geometry,
+// keys, weight preparation, Alice Enc, Bob eval, Alice Dec, recombination and the
+// whole-layer / host-buffer entry points.
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "layer_launch.cuh"
+
+namespace ensei_gpu {
+
+int run_guarded(void (*fn)(void*), void* arg);
+
+template <int LOGN>
+void launch_tile(const LayerRun&, int, bool, int, const uint64_t*, uint32_t, const void*, uint64_t*, int);
+template <int LOGN>
+void launch_share(const LayerRun&, bool, uint64_t*, uint32_t*, int);
+template <int LOGN>
+void launch_dec(const LayerRun&, const uint64_t*, uint32_t, const uint64_t*, uint32_t*, const uint32_t*, uint32_t*,
+                int);
+template <int LOGN>
+void launch_secret(const LayerRun&, const int64_t*, int64_t*, uint64_t*, bool);
+
+extern template void launch_tile<11>(const LayerRun&, int, bool, int, const uint64_t*, uint32_t, const void*,
+                                     uint64_t*, int);
+extern template void launch_tile<12>(const LayerRun&, int, bool, int, const uint64_t*, uint32_t, const void*,
+                                     uint64_t*, int);
+extern template void launch_tile<13>(const LayerRun&, int, bool, int, const uint64_t*, uint32_t, const void*,
+                                     uint64_t*, int);
+
+namespace {
+
+template <class Fn>
+int guarded(Fn&& fn) {
+  struct Box {
+    Fn* f;
+  } box{&fn};
+  return run_guarded([](void* p) { (*static_cast<Box*>(p)->f)(); }, &box);
+}
+
+struct Geo {
+  uint32_t Lh, Lw, logL, B, oh, ow, r0, c0, G;
+};
+
+int ilog2u(uint32_t v) {
+  int l = 0;
+  while ((1u << l) < v) ++l;
+  return l;
+}
+
+// make_geometry (REF ntt.cpp:65-81) + blocks per channel (REF protocol.cpp:180)
+Geo geometry(const ensei_gpu_ctx* c, const ensei_conv_desc* d) {
+  require(c && d, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+  require(d->H && d->W && d->fh && d->fw, ENSEI_ERR_BAD_GEOMETRY, "zero dimension");
+  require(d->cin && d->cout, ENSEI_ERR_BAD_GEOMETRY, "conv layer needs channel counts");
+  require(d->same || (d->fh <= d->H && d->fw <= d->W), ENSEI_ERR_BAD_GEOMETRY,
+          "valid convolution needs filter <= image");
+  auto padded = [&](uint32_t min_len) -> uint32_t {
+    uint32_t p2 = 1;
+    while (p2 < min_len) p2 <<= 1;
+    if ((c->p - 1) % p2 == 0) return p2;
+    fail(ENSEI_ERR_UNSUPPORTED, "non-power-of-two transform length (REF direct O(L^2) path) not on the GPU path");
+  };
+  Geo g;
+  g.Lh = padded(d->H + d->fh - 1);
+  g.Lw = padded(d->W + d->fw - 1);
+  require(g.Lh == g.Lw, ENSEI_ERR_UNSUPPORTED, "rectangular padded grids are not on the GPU path");
+  require(g.Lh <= (uint32_t)kMaxTile && g.Lh >= 2, ENSEI_ERR_UNSUPPORTED, "padded grid side must be in [2, 64]");
+  g.logL = ilog2u(g.Lh);
+  g.G = g.Lh * g.Lw;
+  g.B = (g.G + c->n - 1) / c->n;
+  g.oh = d->same ? d->H : d->H - d->fh + 1;
+  g.ow = d->same ? d->W : d->W - d->fw + 1;
+  g.r0 = d->same ? (d->fh - 1) / 2 : d->fh - 1;
+  g.c0 = d->same ? (d->fw - 1) / 2 : d->fw - 1;
+  return g;
+}
+
+LayerRun make_run(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g, uint32_t num_images,
+                  const ensei_randomness* rand, void* stream) {
+  LayerRun r;
+  r.ctx = c;
+  r.logL = (int)g.logL;
+  r.R = (int)c->R;
+  r.st = (cudaStream_t)stream;
+  LayerArgs& a = r.a;
+  std::memset(&a, 0, sizeof(a));
+  a.H = d->H;
+  a.W = d->W;
+  a.fh = d->fh;
+  a.fw = d->fw;
+  a.cin = d->cin;
+  a.cout = d->cout;
+  a.Lh = g.Lh;
+  a.Lw = g.Lw;
+  a.B = g.B;
+  a.oh = g.oh;
+  a.ow = g.ow;
+  a.r0 = g.r0;
+  a.c0 = g.c0;
+  a.G = g.G;
+  a.num_images = num_images;
+  for (uint32_t i = 0; i < c->R; ++i) {
+    a.pc[i] = c->pc[i];
+    a.twq_fwd[i] = c->tab.tw_q_fwd[i];
+    a.twq_inv[i] = c->tab.tw_q_inv[i];
+  }
+  a.pp = c->pp;
+  a.twp_fwd = c->tab.tw_p_fwd;
+  a.twp_inv = c->tab.tw_p_inv;
+  a.twc_fwd = c->tab.tw_c_fwd;
+  a.twc_inv = c->tab.tw_c_inv;
+  if (rand) {
+    require(rand->mode == ENSEI_RAND_PHILOX || rand->mode == ENSEI_RAND_INJECTED, ENSEI_ERR_INVALID_ARGUMENT,
+            "bad randomness mode");
+    a.rand_mode = rand->mode;
+    a.layer = rand->layer;
+    a.image_base = rand->image_base;
+    a.cbd_k = rand->cbd_k ? rand->cbd_k : 20;
+    require(a.cbd_k <= 31, ENSEI_ERR_INVALID_ARGUMENT, "cbd_k must be <= 31");
+    a.alice_key = rand->alice_key;
+    a.bob_key = rand->bob_key;
+    a.inj_noise = rand->d_noise;
+    a.inj_ahat = rand->d_a_hat;
+    a.inj_share = rand->d_share;
+  }
+  return r;
+}
+
+bool injected(const ensei_randomness* r) { return r && r->mode == ENSEI_RAND_INJECTED; }
+
+void tile(const LayerRun& r, int tm, bool inj, int in_t, const uint64_t* key, uint32_t ks, const void* in,
+          uint64_t* out, int items) {
+  switch (r.ctx->logn) {
+    case 11: return launch_tile<11>(r, tm, inj, in_t, key, ks, in, out, items);
+    case 12: return launch_tile<12>(r, tm, inj, in_t, key, ks, in, out, items);
+    case 13: return launch_tile<13>(r, tm, inj, in_t, key, ks, in, out, items);
+  }
+  fail(ENSEI_ERR_UNSUPPORTED, "ring degree must be 2048, 4096 or 8192 on this path");
+}
+void share(const LayerRun& r, bool inj, uint64_t* ct_out, uint32_t* bob_share, int items) {
+  switch (r.ctx->logn) {
+    case 11: return launch_share<11>(r, inj, ct_out, bob_share, items);
+    case 12: return launch_share<12>(r, inj, ct_out, bob_share, items);
+    case 13: return launch_share<13>(r, inj, ct_out, bob_share, items);
+  }
+  fail(ENSEI_ERR_UNSUPPORTED, "ring degree must be 2048, 4096 or 8192 on this path");
+}
+void dec(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint64_t* ct, uint32_t* alice,
+         const uint32_t* bob, uint32_t* out, int items) {
+  switch (r.ctx->logn) {
+    case 11: return launch_dec<11>(r, key, ks, ct, alice, bob, out, items);
+    case 12: return launch_dec<12>(r, key, ks, ct, alice, bob, out, items);
+    case 13: return launch_dec<13>(r, key, ks, ct, alice, bob, out, items);
+  }
+  fail(ENSEI_ERR_UNSUPPORTED, "ring degree must be 2048, 4096 or 8192 on this path");
+}
+void secret(const LayerRun& r, const int64_t* t_in, int64_t* t_out, uint64_t* key, bool sample) {
+  switch (r.ctx->logn) {
+    case 11: return launch_secret<11>(r, t_in, t_out, key, sample);
+    case 12: return launch_secret<12>(r, t_in, t_out, key, sample);
+    case 13: return launch_secret<13>(r, t_in, t_out, key, sample);
+  }
+  fail(ENSEI_ERR_UNSUPPORTED, "ring degree must be 2048, 4096 or 8192 on this path");
+}
+
+template <int R, int S, int MT, int NTL, int KT>
+void mac_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
+  const int n = (int)r.ctx->n, rows = 2 * r.a.num_images, cols = r.a.cout;
+  dim3 grid((unsigned)(r.a.B * R * n / S), (unsigned)((rows + MT - 1) / MT), (unsigned)((cols + NTL - 1) / NTL));
+  mac_kernel<R, S, MT, NTL, KT><<<grid, S * (MT / 4) * (NTL / 4), 0, r.st>>>(r.a, (int)r.ctx->logn, ct, w, 1, out);
+  check_launch("mac_kernel");
+}
+
+void mac(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
+  if (r.a.num_images == 0) return;
+  const int rows = 2 * r.a.num_images, cols = r.a.cout;
+  const bool small = rows <= 16 && cols <= 16;
+  if (r.R == 1) {
+    if (small) return mac_go<1, 16, 16, 16, 8>(r, ct, w, out);
+    return mac_go<1, 8, 32, 32, 8>(r, ct, w, out);
+  }
+  if (r.R == 3) {
+    if (small) return mac_go<3, 16, 16, 16, 8>(r, ct, w, out);
+    return mac_go<3, 8, 32, 32, 8>(r, ct, w, out);
+  }
+  fail(ENSEI_ERR_UNSUPPORTED, "ElementMult: unsupported prime count");
+}
+
+__global__ void recombine_kernel(const uint32_t* a, const uint32_t* b, size_t count, uint32_t p, uint32_t* out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    uint32_t y = a[i] % p + b[i] % p;
+    out[i] = y >= p ? y - p : y;
+  }
+}
+
+struct Workspace {
+  uint64_t* ct_in;
+  uint64_t* ct_out;
+  uint32_t* bob;
+  uint8_t* stage_in;
+  uint32_t* stage_out;
+};
+
+size_t ct_bytes(const ensei_gpu_ctx* c, const Geo& g, uint32_t ch, uint32_t imgs) {
+  return (size_t)imgs * ch * g.B * 2 * c->R * c->n * sizeof(uint64_t);
+}
+size_t share_bytes(const Geo& g, uint32_t cout, uint32_t imgs) {
+  return ((size_t)imgs * cout * g.oh * g.ow * sizeof(uint32_t) + 255) & ~(size_t)255;
+}
+size_t in_bytes(const ensei_conv_desc* d, uint32_t imgs, int in_dtype) {
+  return ((size_t)imgs * d->cin * d->H * d->W * (in_dtype == ENSEI_IN_U8 ? 1 : 4) + 255) & ~(size_t)255;
+}
+
+Workspace carve(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g, uint32_t imgs, void* ws,
+                int in_dtype, bool host) {
+  Workspace w{};
+  uint8_t* p = static_cast<uint8_t*>(ws);
+  w.ct_in = reinterpret_cast<uint64_t*>(p);
+  p += ct_bytes(c, g, d->cin, imgs);
+  w.ct_out = reinterpret_cast<uint64_t*>(p);
+  p += ct_bytes(c, g, d->cout, imgs);
+  w.bob = reinterpret_cast<uint32_t*>(p);
+  p += share_bytes(g, d->cout, imgs);
+  if (host) {
+    w.stage_in = p;
+    p += in_bytes(d, imgs, in_dtype);
+    w.stage_out = reinterpret_cast<uint32_t*>(p);
+  }
+  return w;
+}
+
+void conv_layer(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uint64_t* key, uint32_t ks,
+                const uint64_t* w_eval, const void* in, int in_dtype, const uint32_t* bob_prev, uint32_t imgs,
+                const ensei_randomness* rand, void* ws, uint32_t* alice_share, uint32_t* bob_share, uint32_t* out,
+                void* stream) {
+  require(ctx && desc && key && w_eval && in && ws, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+  Geo g = geometry(ctx, desc);
+  LayerRun r = make_run(ctx, desc, g, imgs, rand, stream);
+  Workspace w = carve(ctx, desc, g, imgs, ws, in_dtype, false);
+  uint32_t* bs = bob_share ? bob_share : w.bob;
+  const bool inj = injected(rand);
+  share(r, inj, w.ct_out, bs, (int)(imgs * desc->cout));
+  tile(r, TILE_ENC, inj, in_dtype, key, ks, in, w.ct_in, (int)(imgs * desc->cin));
+  if (bob_prev) tile(r, TILE_HOMREC, false, ENSEI_IN_U32, key, 0, bob_prev, w.ct_in, (int)(imgs * desc->cin));
+  mac(r, w.ct_in, w_eval, w.ct_out);
+  dec(r, key, ks, w.ct_out, alice_share, bs, out, (int)(imgs * desc->cout));
+}
+
+}  // namespace
+}  // namespace ensei_gpu
+
+using namespace ensei_gpu;
+
+extern "C" {
+
+int ensei_gpu_layer_geometry(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, ensei_layer_geom* geom) {
+  return guarded([&] {
+    require(geom != nullptr, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    Geo g = geometry(ctx, desc);
+    *geom = {g.Lh, g.Lw, g.B, g.oh, g.ow, g.r0, g.c0};
+  });
+}
+
+int ensei_gpu_secret_from_coeffs(ensei_gpu_ctx* ctx, const int64_t* d_t, uint64_t* d_key, void* stream) {
+  return guarded([&] {
+    require(ctx && d_t && d_key, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    ensei_conv_desc d{2, 2, 1, 1, 1, 1, 1};
+    Geo g{2, 2, 1, 1, 2, 2, 0, 0, 4};
+    secret(make_run(ctx, &d, g, 0, nullptr, stream), d_t, nullptr, d_key, false);
+  });
+}
+
+int ensei_gpu_secret_sample(ensei_gpu_ctx* ctx, uint64_t alice_key, int64_t* d_t, uint64_t* d_key, void* stream) {
+  return guarded([&] {
+    require(ctx && d_key, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    ensei_conv_desc d{2, 2, 1, 1, 1, 1, 1};
+    Geo g{2, 2, 1, 1, 2, 2, 0, 0, 4};
+    ensei_randomness rnd{};
+    rnd.mode = ENSEI_RAND_PHILOX;
+    rnd.alice_key = alice_key;
+    secret(make_run(ctx, &d, g, 0, &rnd, stream), nullptr, d_t, d_key, true);
+  });
+}
+
+int ensei_gpu_prepare_weights(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const int32_t* d_w,
+                              uint64_t* d_w_eval, void* stream) {
+  return guarded([&] {
+    require(d_w && d_w_eval, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    Geo g = geometry(ctx, desc);
+    LayerRun r = make_run(ctx, desc, g, 0, nullptr, stream);
+    tile(r, TILE_WEIGHTS, false, 0, nullptr, 0, d_w, d_w_eval, (int)(desc->cout * desc->cin));
+  });
+}
+
+int ensei_gpu_alice_encrypt(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uint64_t* d_key,
+                            uint32_t key_stride, const void* d_in, int in_dtype, uint32_t num_images,
+                            const ensei_randomness* rand, uint64_t* d_ct, void* stream) {
+  return guarded([&] {
+    require(d_key && d_in && d_ct, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    require(in_dtype == ENSEI_IN_U32 || in_dtype == ENSEI_IN_U8, ENSEI_ERR_INVALID_ARGUMENT, "bad input dtype");
+    Geo g = geometry(ctx, desc);
+    LayerRun r = make_run(ctx, desc, g, num_images, rand, stream);
+    tile(r, TILE_ENC, injected(rand), in_dtype, d_key, key_stride, d_in, d_ct, (int)(num_images * desc->cin));
+  });
+}
+
+int ensei_gpu_bob_eval(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint64_t* d_ct, const uint64_t* d_w_eval,
+                       const uint32_t* d_bob_prev, uint32_t num_images, const ensei_randomness* rand,
+                       uint64_t* d_ct_out, uint32_t* d_bob_share, void* stream) {
+  return guarded([&] {
+    require(d_ct && d_w_eval && d_ct_out && d_bob_share, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    Geo g = geometry(ctx, desc);
+    LayerRun r = make_run(ctx, desc, g, num_images, rand, stream);
+    share(r, injected(rand), d_ct_out, d_bob_share, (int)(num_images * desc->cout));
+    if (d_bob_prev) tile(r, TILE_HOMREC, false, ENSEI_IN_U32, nullptr, 0, d_bob_prev, d_ct, (int)(num_images * desc->cin));
+    mac(r, d_ct, d_w_eval, d_ct_out);
+  });
+}
+
+int ensei_gpu_alice_decrypt(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uint64_t* d_key,
+                            uint32_t key_stride, const uint64_t* d_ct_out, uint32_t num_images,
+                            uint32_t* d_alice_share, void* stream) {
+  return guarded([&] {
+    require(d_key && d_ct_out && d_alice_share, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    Geo g = geometry(ctx, desc);
+    LayerRun r = make_run(ctx, desc, g, num_images, nullptr, stream);
+    dec(r, d_key, key_stride, d_ct_out, d_alice_share, nullptr, nullptr, (int)(num_images * desc->cout));
+  });
+}
+
+int ensei_gpu_recombine(ensei_gpu_ctx* ctx, const uint32_t* d_a, const uint32_t* d_b, size_t count, uint32_t* d_out,
+                        void* stream) {
+  return guarded([&] {
+    require(ctx && d_a && d_b && d_out, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    if (!count) return;
+    size_t grid = std::min<size_t>((count + 255) / 256, (size_t)ctx->sm_count * 8);
+    recombine_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(d_a, d_b, count, (uint32_t)ctx->p, d_out);
+    check_launch("recombine_kernel");
+  });
+}
+
+size_t ensei_gpu_conv_workspace_bytes(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint32_t num_images) {
+  size_t out = 0;
+  guarded([&] {
+    Geo g = geometry(ctx, desc);
+    out = ct_bytes(ctx, g, desc->cin, num_images) + ct_bytes(ctx, g, desc->cout, num_images) +
+          share_bytes(g, desc->cout, num_images);
+  });
+  return out;
+}
+
+int ensei_gpu_conv_layer(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uint64_t* d_key, uint32_t key_stride,
+                         const uint64_t* d_w_eval, const void* d_in, int in_dtype, const uint32_t* d_bob_prev,
+                         uint32_t num_images, const ensei_randomness* rand, void* d_workspace,
+                         uint32_t* d_alice_share, uint32_t* d_bob_share, uint32_t* d_out, void* stream) {
+  return guarded([&] {
+    conv_layer(ctx, desc, d_key, key_stride, d_w_eval, d_in, in_dtype, d_bob_prev, num_images, rand, d_workspace,
+               d_alice_share, d_bob_share, d_out, stream);
+  });
+}
+
+size_t ensei_gpu_conv_host_workspace_bytes(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
+                                           uint32_t num_images, int in_dtype) {
+  size_t out = 0;
+  guarded([&] {
+    Geo g = geometry(ctx, desc);
+    out = ct_bytes(ctx, g, desc->cin, num_images) + ct_bytes(ctx, g, desc->cout, num_images) +
+          share_bytes(g, desc->cout, num_images) + in_bytes(desc, num_images, in_dtype) +
+          share_bytes(g, desc->cout, num_images);
+  });
+  return out;
+}
+
+int ensei_gpu_conv_layer_host(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uint64_t* d_key,
+                              const uint64_t* d_w_eval, const void* h_in, int in_dtype, uint32_t num_images,
+                              const ensei_randomness* rand, void* d_workspace, uint32_t* h_out, void* stream) {
+  return guarded([&] {
+    require(ctx && desc && h_in && h_out && d_workspace, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    Geo g = geometry(ctx, desc);
+    Workspace w = carve(ctx, desc, g, num_images, d_workspace, in_dtype, true);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t nin = (size_t)num_images * desc->cin * desc->H * desc->W * (in_dtype == ENSEI_IN_U8 ? 1 : 4);
+    const size_t nout = (size_t)num_images * desc->cout * g.oh * g.ow * sizeof(uint32_t);
+    EG_CUDA(cudaMemcpyAsync(w.stage_in, h_in, nin, cudaMemcpyHostToDevice, st));
+    conv_layer(ctx, desc, d_key, 0, d_w_eval, w.stage_in, in_dtype, nullptr, num_images, rand, d_workspace, nullptr,
+               nullptr, w.stage_out, stream);
+    EG_CUDA(cudaMemcpyAsync(h_out, w.stage_out, nout, cudaMemcpyDeviceToHost, st));
+    EG_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,188 @@
+// layer_launch.cuh -- host launchers of the fused layer kernels, templated on the
+// ring degree and instantiated once per degree (layer_n11.cu / n12 / n13) so the
+// heavy template code compiles in parallel.
+#pragma once
+#include "layer.cuh"
+
+namespace ensei_gpu {
+
+struct LayerRun {
+  const ensei_gpu_ctx* ctx;
+  LayerArgs a;
+  int logL;  // square padded grid, log2 side
+  int R;
+  cudaStream_t st;
+};
+
+template <class K>
+static void set_smem(K k, size_t smem) {
+  if (smem > 48 * 1024) EG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+}
+
+// ---- tile -> ring (Enc / HomRec / weights / secret) ----
+template <int LOGN, int LOGL, int R, int TM, bool INJ, int IN_T>
+static void enc_go(const LayerRun& r, const uint64_t* key, uint32_t key_stride, const void* in, uint64_t* out,
+                   int items) {
+  auto k = tile_enc_kernel<LOGN, LOGL, LOGL, R, 0, TM, INJ, IN_T>;
+  constexpr size_t smem = tile_enc_smem<LOGN, LOGL, LOGL, R>();
+  set_smem(k, smem);
+  k<<<items, (1 << LOGN) >> kLogE, smem, r.st>>>(r.a, key, key_stride, in, out);
+  check_launch("tile_enc_kernel");
+}
+
+template <int LOGN, int LOGL, int R>
+static void enc_dispatch_l(const LayerRun& r, int tm, bool inj, int in_t, const uint64_t* key, uint32_t ks,
+                           const void* in, uint64_t* out, int items) {
+  if (tm == TILE_WEIGHTS) return enc_go<LOGN, LOGL, R, TILE_WEIGHTS, false, 0>(r, key, ks, in, out, items);
+  if (tm == TILE_HOMREC) return enc_go<LOGN, LOGL, R, TILE_HOMREC, false, 0>(r, key, ks, in, out, items);
+  if constexpr (R == 1) {
+    if (inj) {
+      if (in_t == ENSEI_IN_U8) return enc_go<LOGN, LOGL, R, TILE_ENC, true, ENSEI_IN_U8>(r, key, ks, in, out, items);
+      return enc_go<LOGN, LOGL, R, TILE_ENC, true, ENSEI_IN_U32>(r, key, ks, in, out, items);
+    }
+  } else {
+    if (inj) fail(ENSEI_ERR_UNSUPPORTED, "injected randomness is single-prime only (REF has no RNS)");
+  }
+  if (in_t == ENSEI_IN_U8) return enc_go<LOGN, LOGL, R, TILE_ENC, false, ENSEI_IN_U8>(r, key, ks, in, out, items);
+  return enc_go<LOGN, LOGL, R, TILE_ENC, false, ENSEI_IN_U32>(r, key, ks, in, out, items);
+}
+
+template <int LOGN, int R>
+static void enc_dispatch_r(const LayerRun& r, int tm, bool inj, int in_t, const uint64_t* key, uint32_t ks,
+                           const void* in, uint64_t* out, int items) {
+  switch (r.logL) {
+    case 1: return enc_dispatch_l<LOGN, 1, R>(r, tm, inj, in_t, key, ks, in, out, items);
+    case 2: return enc_dispatch_l<LOGN, 2, R>(r, tm, inj, in_t, key, ks, in, out, items);
+    case 3: return enc_dispatch_l<LOGN, 3, R>(r, tm, inj, in_t, key, ks, in, out, items);
+    case 4: return enc_dispatch_l<LOGN, 4, R>(r, tm, inj, in_t, key, ks, in, out, items);
+    case 5: return enc_dispatch_l<LOGN, 5, R>(r, tm, inj, in_t, key, ks, in, out, items);
+    case 6: return enc_dispatch_l<LOGN, 6, R>(r, tm, inj, in_t, key, ks, in, out, items);
+  }
+  fail(ENSEI_ERR_UNSUPPORTED, "padded grid side must be a power of two <= 64 on this path");
+}
+
+template <int LOGN>
+void launch_tile(const LayerRun& r, int tm, bool inj, int in_t, const uint64_t* key, uint32_t ks, const void* in,
+                 uint64_t* out, int items) {
+  if (items == 0) return;
+  if (r.R == 1) return enc_dispatch_r<LOGN, 1>(r, tm, inj, in_t, key, ks, in, out, items);
+  if constexpr (LOGN == 13) {
+    if (r.R == 3) return enc_dispatch_r<LOGN, 3>(r, tm, inj, in_t, key, ks, in, out, items);
+  }
+  fail(ENSEI_ERR_UNSUPPORTED, "RNS chains are supported with 3 primes at n = 8192");
+}
+
+// ---- HomShare masks + Bob share ----
+template <int LOGN, int LOGL, int R, bool INJ>
+static void share_go(const LayerRun& r, uint64_t* ct_out, uint32_t* bob_share, int items) {
+  auto k = share_kernel<LOGN, LOGL, LOGL, R, INJ>;
+  constexpr size_t smem = share_smem<LOGN, LOGL, LOGL>();
+  set_smem(k, smem);
+  k<<<items, (1 << LOGN) >> kLogE, smem, r.st>>>(r.a, ct_out, bob_share);
+  check_launch("share_kernel");
+}
+
+template <int LOGN, int R, bool INJ>
+static void share_dispatch(const LayerRun& r, uint64_t* m, uint32_t* bs, int items) {
+  switch (r.logL) {
+    case 1: return share_go<LOGN, 1, R, INJ>(r, m, bs, items);
+    case 2: return share_go<LOGN, 2, R, INJ>(r, m, bs, items);
+    case 3: return share_go<LOGN, 3, R, INJ>(r, m, bs, items);
+    case 4: return share_go<LOGN, 4, R, INJ>(r, m, bs, items);
+    case 5: return share_go<LOGN, 5, R, INJ>(r, m, bs, items);
+    case 6: return share_go<LOGN, 6, R, INJ>(r, m, bs, items);
+  }
+  fail(ENSEI_ERR_UNSUPPORTED, "padded grid side must be a power of two <= 64 on this path");
+}
+
+// The mask for (img, o, b, r) is written where c1 of the output ciphertext will
+// live; mac_kernel reads it back before overwriting (same thread, same word).
+template <int LOGN>
+void launch_share(const LayerRun& r, bool inj, uint64_t* mask, uint32_t* bob_share, int items) {
+  if (items == 0) return;
+  if (r.R == 1) {
+    if (inj) return share_dispatch<LOGN, 1, true>(r, mask, bob_share, items);
+    return share_dispatch<LOGN, 1, false>(r, mask, bob_share, items);
+  }
+  if constexpr (LOGN == 13) {
+    if (r.R == 3 && !inj) return share_dispatch<LOGN, 3, false>(r, mask, bob_share, items);
+  }
+  fail(ENSEI_ERR_UNSUPPORTED, "HomShare: unsupported prime count / randomness mode");
+}
+
+// ---- decrypt ----
+template <int LOGN, int LOGL>
+static void dec_go(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint64_t* ct, uint32_t* alice,
+                   const uint32_t* bob, uint32_t* out, int items) {
+  auto k = dec_kernel<LOGN, LOGL, LOGL>;
+  constexpr size_t smem = share_smem<LOGN, LOGL, LOGL>();
+  set_smem(k, smem);
+  k<<<items, (1 << LOGN) >> kLogE, smem, r.st>>>(r.a, key, ks, ct, alice, bob, out);
+  check_launch("dec_kernel");
+}
+
+template <int LOGN>
+void launch_dec(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint64_t* ct, uint32_t* alice,
+                const uint32_t* bob, uint32_t* out, int items) {
+  if (items == 0) return;
+  if (r.R != 1) fail(ENSEI_ERR_UNSUPPORTED, "RNS decryption uses the CRT path (alice_decrypt_rns)");
+  switch (r.logL) {
+    case 1: return dec_go<LOGN, 1>(r, key, ks, ct, alice, bob, out, items);
+    case 2: return dec_go<LOGN, 2>(r, key, ks, ct, alice, bob, out, items);
+    case 3: return dec_go<LOGN, 3>(r, key, ks, ct, alice, bob, out, items);
+    case 4: return dec_go<LOGN, 4>(r, key, ks, ct, alice, bob, out, items);
+    case 5: return dec_go<LOGN, 5>(r, key, ks, ct, alice, bob, out, items);
+    case 6: return dec_go<LOGN, 6>(r, key, ks, ct, alice, bob, out, items);
+  }
+  fail(ENSEI_ERR_UNSUPPORTED, "padded grid side must be a power of two <= 64 on this path");
+}
+
+// ---- secret key: t -> (t_eval, Shoup companion) per prime, device layout ----
+template <int LOGN>
+__global__ void __launch_bounds__((1 << LOGN) >> kLogE)
+    secret_kernel(LayerArgs a, const int64_t* t_in, int64_t* t_out, uint64_t* key, int sample) {
+  constexpr int N = 1 << LOGN, NT = N >> kLogE;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
+  const int r = blockIdx.x;
+  const PrimeConst pc = a.pc[r];
+  const Field64 f = pc.f;
+  const CtaBar bar;
+  auto coeff = [&](int i) -> int64_t {
+    return sample ? (int64_t)draw_ternary(a.alice_key, stream_id(PURPOSE_SECRET, 0, 0, 0, 0), i) : t_in[i];
+  };
+  if (sample && t_out && r == 0)
+    for (int i = threadIdx.x; i < N; i += NT) t_out[i] = coeff(i);
+  auto src = [&](int i) -> uint64_t {
+    const int64_t t = coeff(i);
+    const int64_t m = t % (int64_t)f.q;
+    return m < 0 ? (uint64_t)(m + (int64_t)f.q) : (uint64_t)m;
+  };
+  uint64_t* kr = key + (size_t)(2 * r) * N;
+  auto dst = [&](int j, uint64_t v) {
+    const uint64_t x = Bfly<Field64, 0>::fin_ct(f, v, pc.cred);
+    kr[j] = x;
+    kr[N + j] = (uint64_t)(((unsigned __int128)x << 64) / f.q);
+  };
+  ntt_forward<Field64, uint64_t, LOGN, kLogE, 0, false, false>(f, a.twq_fwd[r], qbuf, threadIdx.x, src, dst, bar,
+                                                               pc.cred);
+}
+
+template <int LOGN>
+void launch_secret(const LayerRun& r, const int64_t* t_in, int64_t* t_out, uint64_t* key, bool sample) {
+  auto k = secret_kernel<LOGN>;
+  constexpr size_t smem = (size_t)(1 << LOGN) * 8;
+  set_smem(k, smem);
+  k<<<r.R, (1 << LOGN) >> kLogE, smem, r.st>>>(r.a, t_in, t_out, key, sample ? 1 : 0);
+  check_launch("secret_kernel");
+}
+
+#define EG_INSTANTIATE_LAYER(LOGN)                                                                               \
+  template void launch_tile<LOGN>(const LayerRun&, int, bool, int, const uint64_t*, uint32_t, const void*,      \
+                                  uint64_t*, int);                                                               \
+  template void launch_share<LOGN>(const LayerRun&, bool, uint64_t*, uint32_t*, int);                            \
+  template void launch_dec<LOGN>(const LayerRun&, const uint64_t*, uint32_t, const uint64_t*, uint32_t*,         \
+                                 const uint32_t*, uint32_t*, int);                                               \
+  template void launch_secret<LOGN>(const LayerRun&, const int64_t*, int64_t*, uint64_t*, bool);
+
+}  // namespace ensei_gpu

@@ -8,22 +8,6 @@
 
 namespace ensei_gpu {
 
-// Global store of lazy transform outputs with the canonical reduction applied.
-template <int MODE, bool FWD>
-struct GlobalOut64 {
-  uint64_t* g;
-  Field64 f;
-  uint32_t cred;
-  static constexpr bool kVec = true;
-  EG_DEV uint64_t fin(uint64_t v) const {
-    return FWD ? Bfly<Field64, MODE>::fin_ct(f, v, cred) : Bfly<Field64, MODE>::fin_gs(f, v);
-  }
-  EG_DEV void operator()(int i, uint64_t v) const { g[i] = fin(v); }
-  EG_DEV void st2(int i, uint64_t a, uint64_t b) const {
-    *reinterpret_cast<ulonglong2*>(g + i) = make_ulonglong2(fin(a), fin(b));
-  }
-};
-
 // Prefetch one length-N u64 polynomial into a swizzled smem buffer (cp.async 16B).
 template <int N>
 EG_DEV void prefetch_poly(uint64_t* sm, const uint64_t* g, int tid, int nthreads) {

@@ -100,3 +100,156 @@ class Context:
     def permute(self, x: torch.Tensor, stream=None) -> torch.Tensor:
         check(lib().ensei_gpu_permute(self.h, 1, _ptr(x), x.numel() // self.n, _stream(stream)))
         return x
+
+
+# ------------------------------------------------------------------ conv layers
+
+@dataclass
+class ConvSpec:
+    """One conv layer (REF LayerSpec + image dims, protocol.hpp:23-31)."""
+    H: int
+    W: int
+    fh: int
+    fw: int
+    same: bool
+    cin: int
+    cout: int
+
+    def desc(self) -> ConvDesc:
+        return ConvDesc(self.H, self.W, self.fh, self.fw, int(self.same), self.cin, self.cout)
+
+
+def unpack_limbs(t: torch.Tensor) -> torch.Tensor:
+    """Packed prepared-weight words -> canonical residues (device layout kept)."""
+    s = t.view(torch.int64)  # values < 2^62: int64 shifts are exact
+    return (((s >> 32) << 30) | (s & ((1 << 30) - 1))).view(torch.uint64)
+
+
+class Randomness:
+    """ensei_randomness: Philox streams keyed by party seeds, or injected draws."""
+
+    def __init__(self, seed: int = 0, layer: int = 0, image_base: int = 0, cbd_k: int = 20,
+                 noise=None, a_hat=None, share=None):
+        self.seed, self.layer, self.image_base, self.cbd_k = seed, layer, image_base, cbd_k
+        self.noise, self.a_hat, self.share = noise, a_hat, share
+
+    def struct(self) -> Randomness_:
+        inj = self.noise is not None or self.a_hat is not None or self.share is not None
+        r = Randomness_()
+        r.mode = RAND_INJECTED if inj else RAND_PHILOX
+        r.layer, r.image_base, r.cbd_k = self.layer, self.image_base, self.cbd_k
+        r.alice_key = fork_seed(self.seed, SALT_ALICE)
+        r.bob_key = fork_seed(self.seed, SALT_BOB)
+        r.d_noise = None if self.noise is None else self.noise.data_ptr()
+        r.d_a_hat = None if self.a_hat is None else self.a_hat.data_ptr()
+        r.d_share = None if self.share is None else self.share.data_ptr()
+        return r
+
+
+Randomness_ = _lib.Randomness
+
+
+class LayerOps:
+    """Batched per-layer operations of the protocol over one Context."""
+
+    def __init__(self, ctx: Context, spec: ConvSpec):
+        self.ctx, self.spec = ctx, spec
+        self.d = spec.desc()
+        g = LayerGeom()
+        check(lib().ensei_gpu_layer_geometry(ctx.h, C.byref(self.d), C.byref(g)))
+        self.geom = g
+        self.B = g.blocks
+
+    def empty_ct(self, images: int, channels: int) -> torch.Tensor:
+        n, R = self.ctx.n, self.ctx.R
+        return torch.empty((images, channels, self.B, 2, R, n), dtype=torch.uint64, device=self.ctx.device)
+
+    def prepare_weights(self, w: torch.Tensor, stream=None) -> torch.Tensor:
+        """w[cout][cin][fh][fw] int32 (device) -> prepared weights (device layout, packed)."""
+        s = self.spec
+        assert w.dtype == torch.int32 and w.is_cuda and tuple(w.shape) == (s.cout, s.cin, s.fh, s.fw)
+        out = torch.empty((s.cout, s.cin, self.B, self.ctx.R, self.ctx.n), dtype=torch.uint64, device=w.device)
+        check(lib().ensei_gpu_prepare_weights(self.ctx.h, C.byref(self.d), _ptr(w), _ptr(out), _stream(stream)))
+        return out
+
+    def alice_encrypt(self, key, x: torch.Tensor, rand: Randomness, key_stride: int = 0, stream=None):
+        images = x.shape[0]
+        in_t = IN_U8 if x.dtype == torch.uint8 else IN_U32
+        assert x.dtype in (torch.uint8, torch.int32, torch.uint32) and x.is_contiguous()
+        ct = self.empty_ct(images, self.spec.cin)
+        r = rand.struct()
+        check(lib().ensei_gpu_alice_encrypt(self.ctx.h, C.byref(self.d), _ptr(key), key_stride, _ptr(x), in_t,
+                                            images, C.byref(r), _ptr(ct), _stream(stream)))
+        return ct
+
+    def bob_eval(self, ct: torch.Tensor, w_eval: torch.Tensor, rand: Randomness, bob_prev=None, stream=None):
+        images = ct.shape[0]
+        g = self.geom
+        ct_out = self.empty_ct(images, self.spec.cout)
+        bob = torch.empty((images, self.spec.cout, g.oh, g.ow), dtype=torch.int32, device=ct.device)
+        r = rand.struct()
+        check(lib().ensei_gpu_bob_eval(self.ctx.h, C.byref(self.d), _ptr(ct), _ptr(w_eval), _ptr(bob_prev), images,
+                                       C.byref(r), _ptr(ct_out), _ptr(bob), _stream(stream)))
+        return ct_out, bob
+
+    def alice_decrypt(self, key, ct_out: torch.Tensor, key_stride: int = 0, stream=None):
+        images = ct_out.shape[0]
+        g = self.geom
+        a = torch.empty((images, self.spec.cout, g.oh, g.ow), dtype=torch.int32, device=ct_out.device)
+        check(lib().ensei_gpu_alice_decrypt(self.ctx.h, C.byref(self.d), _ptr(key), key_stride, _ptr(ct_out), images,
+                                            _ptr(a), _stream(stream)))
+        return a
+
+    def workspace(self, images: int, host: bool = False, in_dtype: int = IN_U8) -> torch.Tensor:
+        if host:
+            nb = lib().ensei_gpu_conv_host_workspace_bytes(self.ctx.h, C.byref(self.d), images, in_dtype)
+        else:
+            nb = lib().ensei_gpu_conv_workspace_bytes(self.ctx.h, C.byref(self.d), images)
+        return torch.empty(nb, dtype=torch.uint8, device=self.ctx.device)
+
+    def forward(self, key, w_eval, x: torch.Tensor, rand: Randomness, ws=None, bob_prev=None, key_stride: int = 0,
+                want_shares: bool = False, stream=None):
+        """The whole oblivious conv layer for a batch; returns the reconstructed output
+        (and the two shares when want_shares)."""
+        images = x.shape[0]
+        g = self.geom
+        in_t = IN_U8 if x.dtype == torch.uint8 else IN_U32
+        ws = self.workspace(images) if ws is None else ws
+        shape = (images, self.spec.cout, g.oh, g.ow)
+        out = torch.empty(shape, dtype=torch.int32, device=x.device)
+        a = torch.empty(shape, dtype=torch.int32, device=x.device) if want_shares else None
+        b = torch.empty(shape, dtype=torch.int32, device=x.device) if want_shares else None
+        r = rand.struct()
+        check(lib().ensei_gpu_conv_layer(self.ctx.h, C.byref(self.d), _ptr(key), key_stride, _ptr(w_eval), _ptr(x),
+                                         in_t, _ptr(bob_prev), images, C.byref(r), _ptr(ws), _ptr(a), _ptr(b),
+                                         _ptr(out), _stream(stream)))
+        return (out, a, b) if want_shares else out
+
+    def forward_host(self, key, w_eval, h_x: torch.Tensor, rand: Randomness, ws, h_out: torch.Tensor, stream=None):
+        """Host-buffer entry point (pinned h_x / h_out): H2D, layer, D2H, synchronous."""
+        images = h_x.shape[0]
+        in_t = IN_U8 if h_x.dtype == torch.uint8 else IN_U32
+        r = rand.struct()
+        check(lib().ensei_gpu_conv_layer_host(self.ctx.h, C.byref(self.d), _ptr(key), _ptr(w_eval),
+                                              C.c_void_p(h_x.data_ptr()), in_t, images, C.byref(r), _ptr(ws),
+                                              C.c_void_p(h_out.data_ptr()), _stream(stream)))
+        return h_out
+
+
+def key_words(ctx: Context) -> int:
+    return 2 * ctx.R * ctx.n
+
+
+def secret_from_coeffs(ctx: Context, t: torch.Tensor, stream=None) -> torch.Tensor:
+    """keygen evaluation form (REF ringbfv.cpp:95-107) from signed coefficients t[n] (int64, device)."""
+    key = torch.empty(key_words(ctx), dtype=torch.uint64, device=ctx.device)
+    check(lib().ensei_gpu_secret_from_coeffs(ctx.h, _ptr(t), _ptr(key), _stream(stream)))
+    return key
+
+
+def secret_sample(ctx: Context, seed: int, stream=None):
+    """Ternary secret from Alice's Philox stream; returns (t, key blob)."""
+    key = torch.empty(key_words(ctx), dtype=torch.uint64, device=ctx.device)
+    t = torch.empty(ctx.n, dtype=torch.int64, device=ctx.device)
+    check(lib().ensei_gpu_secret_sample(ctx.h, fork_seed(seed, SALT_ALICE), _ptr(t), _ptr(key), _stream(stream)))
+    return t, key

@@ -1,0 +1,420 @@
+#!/usr/bin/env python3
+"""bench.py -- B200 benchmark of the oblivious NTT-domain convolution hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1]
+
+Default workload = BASELINE.json configs[1] (the metric's config): one conv layer,
+8 images of 16 x 32x32 uint8 pixels, 16x16x3x3 int8 weights, Same conv, n = 2048,
+60-bit q, p = 638977, reference geometry (64x64 padded grid, 2 blocks / channel).
+One STEP = the whole oblivious layer for the batch (Alice Enc -> Bob HomShare +
+ElementMult -> Alice Dec -> IDFT2D -> recombine), weights prepared once (t_setup,
+excluded like the paper).  `value` = images (convolutions) per second over all GPUs
+with inputs resident in HBM; `e2e` = the same through the host-buffer C-ABI call
+(ensei_gpu_conv_layer_host: H2D pixels, layer, D2H output, synchronous).
+
+Under torchrun (N > 1) every rank runs its own 8 images (weak scaling; image ids
+are global, so every image gets the same randomness as in a 1-GPU run) and the
+reconstructed outputs are all-gathered with NCCL inside every step.
+
+The CPU baseline / reference arm is the UNMODIFIED reference compiled from its own
+sources (oracle/_ref/libensei_ref.so): independent run_inproc sessions of the same
+layer on all host cores, timed by the reference's own online-phase clocks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+P = 638977
+Q = 576460803525083137
+METRIC = "oblivious NTT-domain conv/sec (1/2/4/8 B200); NTT modmul/s vs roofline"
+C_Q, C_MAC, C_P = 10, 8, 3  # IMAD per modmul class (min(survey, SASS))
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--images", type=int, default=8, help="images per GPU per step")
+    ap.add_argument("--seed", type=int, default=2003)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ntt", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ accounting
+
+def ntt_fwd(n):
+    return (n // 2) * (n.bit_length() - 1)
+
+
+def ntt_inv(n):
+    return ntt_fwd(n) + n
+
+
+def dft2d(L):
+    return 2 * L * (L // 2) * (L.bit_length() - 1)
+
+
+def idft2d(L):
+    return dft2d(L) + L * L
+
+
+def layer_counts(n, R, L, B, cin, cout, H, W, oh, ow, imgs):
+    """Algorithmic modmul counts and HBM bytes per kernel per launch."""
+    k = {}
+    k["enc"] = dict(q=imgs * cin * B * R * (2 * n + ntt_fwd(n)), mac=0, p=imgs * cin * (dft2d(L) + B * ntt_inv(n)),
+                    bytes=imgs * cin * H * W + imgs * cin * B * 2 * R * n * 8 + 2 * R * n * 8)
+    k["share"] = dict(q=imgs * cout * B * R * (n + ntt_fwd(n)), mac=0, p=imgs * cout * (B * ntt_inv(n) + idft2d(L)),
+                      bytes=imgs * cout * B * R * n * 8 + imgs * cout * oh * ow * 4)
+    k["mac"] = dict(q=0, mac=imgs * cin * cout * B * R * 2 * n, p=0,
+                    bytes=imgs * cin * B * 2 * R * n * 8 + cout * cin * B * R * n * 8 + imgs * cout * B * R * n * 8
+                    + imgs * cout * B * 2 * R * n * 8)
+    k["dec"] = dict(q=imgs * cout * B * R * (n + ntt_inv(n)), mac=0, p=imgs * cout * (B * ntt_fwd(n) + idft2d(L)),
+                    bytes=imgs * cout * B * 2 * R * n * 8 + 2 * R * n * 8 + imgs * cout * oh * ow * 4 * 3)
+    for v in k.values():
+        v["imad"] = C_Q * v["q"] + C_MAC * v["mac"] + C_P * v["p"]
+        v["modmul"] = v["q"] + v["mac"] + v["p"]
+    return k
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ reference arm
+
+def ref_layer_bench(images_per_sample, threads, seed):
+    """The reference's own CPU protocol (run_inproc) on the config-1 layer, one
+    image per session, `threads` concurrent sessions (2 host threads each)."""
+    import numpy as np
+    import oracle as O
+    R = O.ref()
+    g = O.MTRng(seed, 0xDA7A)
+    img = np.array([g.uniform_below(256) for _ in range(16 * 32 * 32)], np.int64)
+    w = np.array([g.uniform_below(256) - 128 for _ in range(16 * 16 * 9)], np.int64)
+    desc = np.array([0, 3, 3, 1, 16, 16, 0], np.int32)
+    online = O.C.c_double(0)
+    wall = R.ref_bench_protocol(P, Q, 2048, 4.0, seed, 32, 32, 1, desc, img, w, images_per_sample, threads,
+                                O.C.byref(online))
+    if wall < 0:
+        raise RuntimeError("reference bench failed: " + R.ref_last_error().decode())
+    # online-phase throughput with `threads` sessions overlapped (t_setup excluded)
+    value = images_per_sample / (online.value / threads)
+    return value, wall, online.value
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    cores = host_cores()
+    threads = max(1, cores // 2)
+    per = max(threads, 16)
+    vals = []
+    if args.warmup > 0:
+        ref_layer_bench(threads, threads, args.seed)
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        v, wall, online = ref_layer_bench(per, threads, args.seed + 1000 * s)
+        vals.append(v)
+    elapsed = time.perf_counter() - t0
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "conv/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * elapsed / max(1, args.steps),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": "config1 layer (16->16 3x3 Same @32x32, n=2048, 60-bit q, p=638977), one image per "
+                               "reference run_inproc session", "sessions_per_step": per, "concurrent_sessions": threads},
+        "cpu_baseline": {"value": value, "unit": "conv/s", "cores": cores, "kind": "reference",
+                         "sample": f"{per} run_inproc sessions x {args.steps} steps, {threads} concurrent (2 threads "
+                                   "each); online phase (Alice Hello->Done), Bob weight prep excluded"},
+        "e2e": {"value": value, "unit": "conv/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2003_05328_b200 import _lib, ops
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    lib = _lib.lib()
+
+    if args.config != 1:
+        raise SystemExit("only --config 1 (the metric's config) is wired into this bench")
+    imgs = args.images
+    ctx = ops.Context(n=2048, q=(Q,), p=P, device=local)
+    spec = ops.ConvSpec(32, 32, 3, 3, True, 16, 16)
+    L = ops.LayerOps(ctx, spec)
+    g = L.geom
+    gen = torch.Generator().manual_seed(args.seed)
+    x_all = torch.randint(0, 256, (world * imgs, 16, 32, 32), dtype=torch.uint8, generator=gen)
+    wts = torch.randint(-128, 128, (16, 16, 3, 3), dtype=torch.int32, generator=gen).to(dev)
+    x = x_all[rank * imgs:(rank + 1) * imgs].contiguous().to(dev)
+    _, key = ops.secret_sample(ctx, args.seed)
+    w_eval = L.prepare_weights(wts)  # t_setup (not timed)
+    rand = ops.Randomness(seed=args.seed, image_base=rank * imgs)
+    ws = L.workspace(imgs)
+    out = torch.empty((imgs, 16, g.oh, g.ow), dtype=torch.int32, device=dev)
+    gathered = torch.empty((world * imgs, 16, g.oh, g.ow), dtype=torch.int32, device=dev) if world > 1 else None
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        o = L.forward(key, w_eval, x, rand, ws=ws)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, o)
+        return o
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = lib.ensei_gpu_launch_count()
+    total_ms = 0.0
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()  # evict L2 between timed steps (untimed)
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    launches = lib.ensei_gpu_launch_count() - launches0
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    ms_step = total_ms / args.steps
+    value = world * imgs * args.steps / (total_ms / 1e3)
+
+    # ---- per-kernel breakdown + roofline (separately launched, CUDA events, L2 flushed)
+    kcount = layer_counts(2048, 1, g.Lh, g.blocks, 16, 16, 32, 32, g.oh, g.ow, imgs)
+    ct_in = L.empty_ct(imgs, 16)
+    ct_out = L.empty_ct(imgs, 16)
+    bob = torch.empty((imgs, 16, g.oh, g.ow), dtype=torch.int32, device=dev)
+
+    times = {}
+    fns = {
+        "enc": lambda: _lib.check(lib.ensei_gpu_alice_encrypt(ctx.h, ops.C.byref(L.d), ops._ptr(key), 0,
+                                                               ops._ptr(x), _lib.IN_U8, imgs,
+                                                               ops.C.byref(rand.struct()), ops._ptr(ct_in),
+                                                               ops._stream())),
+        "share": lambda: L.bob_share(imgs, rand, ct_out=ct_out, bob=bob),
+        "mac": lambda: L.bob_mac(ct_in, w_eval, ct_out),
+        "dec": lambda: _lib.check(lib.ensei_gpu_alice_decrypt(ctx.h, ops.C.byref(L.d), ops._ptr(key), 0,
+                                                               ops._ptr(ct_out), imgs, ops._ptr(out),
+                                                               ops._stream())),
+    }
+    for name, fn in fns.items():
+        for _ in range(3):
+            fn()
+        acc = []
+        for _ in range(10):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            b.synchronize()
+            acc.append(a.elapsed_time(b))
+        times[name] = statistics.median(acc)
+    imad_peak = lib.ensei_gpu_imad_peak(local)  # mad.wide.u32 ops/s, live probe
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    dom = max(times, key=times.get)
+    kd = kcount[dom]
+    t_dom = times[dom] * 1e-3
+    imad_ach = kd["imad"] / t_dom / 1e9
+    hbm_ach = kd["bytes"] / t_dom / 1e9
+    imad_frac = imad_ach / (imad_peak / 1e9)
+    hbm_frac = hbm_ach / hbm_peak
+    bound = "imad" if imad_frac >= hbm_frac else "hbm"
+    roofline = {
+        "bound": bound, "kernel": dom,
+        "achieved": imad_ach if bound == "imad" else hbm_ach,
+        "peak": imad_peak / 1e9 if bound == "imad" else hbm_peak,
+        "unit": "GIMAD/s" if bound == "imad" else "GB/s",
+        "frac": imad_frac if bound == "imad" else hbm_frac,
+        "traffic": None,
+        "peak_source": ("live mad.wide.u32 probe (ensei_gpu_imad_peak)" if bound == "imad"
+                        else "MEASURED_PEAKS.json hbm_gbs (measured)"),
+        "imad": {"achieved_GIMAD_s": imad_ach, "peak_GIMAD_s": imad_peak / 1e9, "frac": imad_frac,
+                 "imad_per_launch": kd["imad"], "c_q": C_Q, "c_mac": C_MAC, "c_p": C_P},
+        "hbm": {"achieved_GB_s": hbm_ach, "peak_GB_s": hbm_peak, "frac": hbm_frac, "bytes_per_launch": kd["bytes"]},
+        "kernel_ms": times,
+    }
+    total_modmul = sum(v["modmul"] for v in kcount.values())
+
+    # ---- e2e through the host-buffer C-ABI entry point
+    h_x = x.cpu().pin_memory()
+    h_out = torch.empty((imgs, 16, g.oh, g.ow), dtype=torch.int32).pin_memory()
+    ws_h = L.workspace(imgs, host=True, in_dtype=_lib.IN_U8)
+    for _ in range(3):
+        L.forward_host(key, w_eval, h_x, rand, ws_h, h_out)
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        L.forward_host(key, w_eval, h_x, rand, ws_h, h_out)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms_step = statistics.mean(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e_ms_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms_step = float(t.item())
+    e2e = {"value": world * imgs / (e2e_ms_step / 1e3), "unit": "conv/s", "h2d_bytes_per_step": h_x.numel(),
+           "d2h_bytes_per_step": h_out.numel() * 4, "ms_per_step": e2e_ms_step,
+           "api": "ensei_gpu_conv_layer_host (host pinned buffers, wall clock)"}
+
+    # ---- config 2 side measurement: batched negacyclic NTT/INTT (device layout)
+    ntt = None
+    if not args.no_ntt and rank == 0:
+        ntt = {}
+        for n in (2048, 4096, 8192):
+            c2 = ops.Context(n=n, q=(Q,), p=P, device=local)
+            cnt = 65536
+            buf = torch.randint(0, 1 << 62, (cnt, n), dtype=torch.int64, device=dev).view(torch.uint64)
+            buf.copy_((buf.view(torch.int64) % Q).view(torch.uint64))
+            res = {}
+            for inv in (False, True):
+                for _ in range(2):
+                    c2.negacyclic(buf, 0, inv, _lib.LAYOUT_BITREV)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                for _ in range(5):
+                    c2.negacyclic(buf, 0, inv, _lib.LAYOUT_BITREV)
+                b.record(stream)
+                b.synchronize()
+                ms = a.elapsed_time(b) / 5
+                rate = cnt / (ms / 1e3)
+                alg = (ntt_inv(n) if inv else ntt_fwd(n))
+                res["inv" if inv else "fwd"] = {"transforms_per_s": rate, "ms": ms,
+                                                "GB_s": cnt * n * 16 / (ms / 1e3) / 1e9,
+                                                "imad_frac": rate * alg * C_Q / imad_peak}
+            ntt[str(n)] = res
+            del buf, c2
+        torch.cuda.empty_cache()
+
+    # ---- CPU baseline (reference, bounded sample, rank 0)
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            cores = host_cores()
+            thr = max(1, cores // 2)
+            v, wall, online = ref_layer_bench(max(thr, 16), thr, args.seed)
+            cpu = {"value": v, "unit": "conv/s", "cores": cores, "kind": "reference",
+                   "sample": f"{max(thr, 16)} reference run_inproc sessions (one config-1 image each), {thr} "
+                             f"concurrent x 2 threads, online phase only; wall incl. Bob setup {wall:.2f}s"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "conv/s", "cores": host_cores(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "conv/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic: uint8 pixels U[0,256), int8 weights U[-128,128), seeded (no dataset)",
+            "config": {"workload": "config1: one conv layer, 8 images/GPU x 16x32x32 uint8, 16x16x3x3 int8, Same, "
+                                   "n=2048, q=576460803525083137 (60-bit), p=638977, 64x64 padded grid, 2 blocks/ch",
+                       "images_per_gpu": imgs, "global_batch": world * imgs, "parallelism": f"dp{world} (image shards)",
+                       "l2": "flushed (256 MB write) between timed steps", "randomness": "Philox4x32-10 device streams",
+                       "unit_def": "1 conv = 1 image through the whole 16->16 layer"},
+            "roofline": roofline,
+            "modmul_per_s": total_modmul * world * args.steps / (total_ms / 1e3),
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk, "ntt_config2": ntt,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -186,6 +186,18 @@ int ensei_gpu_bob_eval(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint64_t
                        const ensei_randomness* rand, uint64_t* d_ct_out, uint32_t* d_bob_share,
                        void* stream);
 
+/* The two halves of ensei_gpu_bob_eval, separately: hom_share batched over
+ * (img, out channel, block) -- writes the HomShare masks NTT_q(Delta*INTT_p(p - s_B))
+ * into the c1 words of d_ct_out and Bob's cropped share into d_bob_share
+ * (REF hss.cpp:22-49, protocol.cpp:587-603) -- and the ElementMult + channel
+ * accumulation that adds the products onto those masks (REF ringbfv.cpp:233-306). */
+int ensei_gpu_bob_share(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint32_t num_images,
+                        const ensei_randomness* rand, uint64_t* d_ct_out, uint32_t* d_bob_share,
+                        void* stream);
+int ensei_gpu_bob_mac(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uint64_t* d_ct,
+                      const uint64_t* d_w_eval, uint32_t num_images, uint64_t* d_ct_out,
+                      void* stream);
+
 /* AliceSession::receive_shares (REF protocol.cpp:332-355): decrypt (REF
  * ringbfv.cpp:203-231) -> merge -> IDFT2D -> crop, fused.  d_alice_share
  * [img][cout][oh][ow]. */

@@ -140,7 +140,7 @@ def ref():
                                            i32p, i64p, i64p, u64p, vp, vp, U32, vp, vp, vp, vp]),
             "ref_reference_pipeline": (C.c_int, [U64, U64, U32, U32, U32, U32, i32p, i64p, i64p, u64p]),
             "ref_bench_protocol": (C.c_double, [U64, U64, U32, C.c_double, U64, U32, U32, U32, i32p,
-                                                i64p, i64p, U32, U32]),
+                                                i64p, i64p, U32, U32, C.POINTER(C.c_double)]),
             "ref_bench_negacyclic": (C.c_double, [U64, U32, u64p, C.c_size_t, U32]),
         }
         for name, (res, args) in sig.items():

@@ -418,14 +418,18 @@ int ref_reference_pipeline(uint64_t p, uint64_t q, uint32_t n, uint32_t H, uint3
 // CPU baseline: `instances` independent run_inproc sessions (seed + i) spread
 // over `threads` host threads; returns wall seconds (the reference's own
 // concurrency model: independent ciphertext workers).
+// online_sum (optional) receives the sum over sessions of Alice's online seconds
+// (REF PhaseTimings::online_seconds: Hello done -> Done, i.e. excluding Bob's weight
+// preparation, the paper's t_setup).  Each session runs on 2 threads (run_inproc).
 double ref_bench_protocol(uint64_t p, uint64_t q, uint32_t n, double sigma, uint64_t seed,
                           uint32_t H, uint32_t W, uint32_t nlayers, const int32_t* desc,
                           const int64_t* image, const int64_t* weights, uint32_t instances,
-                          uint32_t threads) {
+                          uint32_t threads, double* online_sum) {
   try {
     ProtoArgs a = make_proto(p, q, n, sigma, 1, seed, H, W, nlayers, desc, image, weights);
     std::atomic<uint32_t> next{0};
     std::atomic<int> bad{0};
+    std::vector<double> online(instances, 0.0);
     auto t0 = std::chrono::steady_clock::now();
     std::vector<std::thread> pool;
     for (uint32_t t = 0; t < threads; ++t)
@@ -435,10 +439,18 @@ double ref_bench_protocol(uint64_t p, uint64_t q, uint32_t n, double sigma, uint
           if (i >= instances) break;
           ProtocolConfig cfg = a.cfg;
           cfg.seed = seed + i;
-          try { run_inproc(cfg, a.image, a.weights); } catch (...) { bad++; }
+          try {
+            InprocRun r = run_inproc(cfg, a.image, a.weights);
+            online[i] = r.alice.timings.online_seconds;
+          } catch (...) { bad++; }
         }
       });
     for (auto& th : pool) th.join();
+    if (online_sum) {
+      double acc = 0;
+      for (double v : online) acc += v;
+      *online_sum = acc;
+    }
     double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return bad ? -1.0 : s;
   } catch (const std::exception& e) { fail(e); return -1.0; }

@@ -88,6 +88,8 @@ def lib():
                                               C.POINTER(Randomness), vp, vp]),
             "ensei_gpu_bob_eval": (i32, [vp, C.POINTER(ConvDesc), vp, vp, vp, u32, C.POINTER(Randomness),
                                          vp, vp, vp]),
+            "ensei_gpu_bob_share": (i32, [vp, C.POINTER(ConvDesc), u32, C.POINTER(Randomness), vp, vp, vp]),
+            "ensei_gpu_bob_mac": (i32, [vp, C.POINTER(ConvDesc), vp, vp, u32, vp, vp]),
             "ensei_gpu_alice_decrypt": (i32, [vp, C.POINTER(ConvDesc), vp, u32, vp, u32, vp, vp]),
             "ensei_gpu_recombine": (i32, [vp, vp, vp, sz, vp, vp]),
             "ensei_gpu_conv_workspace_bytes": (sz, [vp, C.POINTER(ConvDesc), u32]),

@@ -220,3 +220,58 @@ int ensei_gpu_permute(ensei_gpu_ctx* ctx, int to_natural, uint64_t* d_data, size
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ IMAD peak probe
+// Chains of mad.wide.u32 with 64-bit accumulation (the instruction the modular
+// kernels are built from); 8 independent chains per thread, full occupancy.
+namespace ensei_gpu {
+__global__ void imad_probe_kernel(uint64_t* sink, uint32_t seed, int iters) {
+  uint32_t a[8], b[8];
+  uint64_t d[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    a[i] = seed * (threadIdx.x + i) + 1;
+    b[i] = a[i] ^ 0x9e3779b9u;
+    d[i] = a[i];
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(d[i]) : "r"(a[i]), "r"(b[i]));
+  }
+  uint64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s ^= d[i];
+  if (s == 0x12345) sink[0] = s;
+}
+}  // namespace ensei_gpu
+
+extern "C" double ensei_gpu_imad_peak(int device) {
+  double out = -1.0;
+  guarded([&] {
+    EG_CUDA(cudaSetDevice(device));
+    int sms = 0;
+    EG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    uint64_t* sink;
+    EG_CUDA(cudaMalloc(&sink, 64));
+    cudaEvent_t e0, e1;
+    EG_CUDA(cudaEventCreate(&e0));
+    EG_CUDA(cudaEventCreate(&e1));
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {
+      EG_CUDA(cudaEventRecord(e0));
+      imad_probe_kernel<<<blocks, threads>>>(sink, 3, iters);
+      EG_CUDA(cudaEventRecord(e1));
+      EG_CUDA(cudaEventSynchronize(e1));
+      float ms;
+      EG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      if (rep) best = std::min(best, ms);
+    }
+    count_launch(4);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    out = (double)blocks * threads * iters * 8 / (best * 1e-3);
+  });
+  return out;
+}

@@ -318,6 +318,26 @@ int ensei_gpu_bob_eval(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint64_t
   });
 }
 
+int ensei_gpu_bob_share(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint32_t num_images,
+                        const ensei_randomness* rand, uint64_t* d_ct_out, uint32_t* d_bob_share, void* stream) {
+  return guarded([&] {
+    require(d_ct_out && d_bob_share, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    Geo g = geometry(ctx, desc);
+    LayerRun r = make_run(ctx, desc, g, num_images, rand, stream);
+    share(r, injected(rand), d_ct_out, d_bob_share, (int)(num_images * desc->cout));
+  });
+}
+
+int ensei_gpu_bob_mac(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uint64_t* d_ct,
+                      const uint64_t* d_w_eval, uint32_t num_images, uint64_t* d_ct_out, void* stream) {
+  return guarded([&] {
+    require(d_ct && d_w_eval && d_ct_out, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    Geo g = geometry(ctx, desc);
+    LayerRun r = make_run(ctx, desc, g, num_images, nullptr, stream);
+    mac(r, d_ct, d_w_eval, d_ct_out);
+  });
+}
+
 int ensei_gpu_alice_decrypt(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uint64_t* d_key,
                             uint32_t key_stride, const uint64_t* d_ct_out, uint32_t num_images,
                             uint32_t* d_alice_share, void* stream) {

@@ -192,6 +192,21 @@ class LayerOps:
                                        C.byref(r), _ptr(ct_out), _ptr(bob), _stream(stream)))
         return ct_out, bob
 
+    def bob_share(self, images: int, rand: Randomness, ct_out=None, bob=None, stream=None):
+        g = self.geom
+        ct_out = self.empty_ct(images, self.spec.cout) if ct_out is None else ct_out
+        bob = torch.empty((images, self.spec.cout, g.oh, g.ow), dtype=torch.int32,
+                          device=self.ctx.device) if bob is None else bob
+        r = rand.struct()
+        check(lib().ensei_gpu_bob_share(self.ctx.h, C.byref(self.d), images, C.byref(r), _ptr(ct_out), _ptr(bob),
+                                        _stream(stream)))
+        return ct_out, bob
+
+    def bob_mac(self, ct, w_eval, ct_out, stream=None):
+        check(lib().ensei_gpu_bob_mac(self.ctx.h, C.byref(self.d), _ptr(ct), _ptr(w_eval), ct.shape[0],
+                                      _ptr(ct_out), _stream(stream)))
+        return ct_out
+
     def alice_decrypt(self, key, ct_out: torch.Tensor, key_stride: int = 0, stream=None):
         images = ct_out.shape[0]
         g = self.geom

@@ -205,6 +205,17 @@ int ensei_gpu_alice_decrypt(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
                             const uint64_t* d_t_eval, uint32_t key_stride, const uint64_t* d_ct_out,
                             uint32_t num_images, uint32_t* d_alice_share, void* stream);
 
+/* trusted_activation (REF protocol.cpp:237-268) for a batch of share tensors
+ * [img][channels][H][W]: recombine mod p, centered lift, fn (0 ReLU, 1 Square,
+ * 2 Identity), optional 2x2 max-pool (pool2 = 1: builder extension for the 32->16->8
+ * spatial steps of config 3; output [img][channels][H/2][W/2]), re-share with fresh
+ * randomness (Alice's reshare stream, or rand->d_share injected [img][ch][out]).
+ * Square overflow (|y|^2 > p/2, REF RangeOverflow) sets *d_overflow != 0 (nullable). */
+int ensei_gpu_activation(ensei_gpu_ctx* ctx, int fn, int pool2, uint32_t channels, uint32_t H,
+                         uint32_t W, uint32_t num_images, const uint32_t* d_a, const uint32_t* d_b,
+                         const ensei_randomness* rand, uint32_t* d_new_a, uint32_t* d_new_b,
+                         int* d_overflow, void* stream);
+
 /* recombine_clear (REF hss.cpp:64-73): out = (a + b) mod p */
 int ensei_gpu_recombine(ensei_gpu_ctx* ctx, const uint32_t* d_a, const uint32_t* d_b, size_t count,
                         uint32_t* d_out, void* stream);

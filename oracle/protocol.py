@@ -42,6 +42,7 @@ class Conv:
 @dataclass
 class Act:
     fn: int  # 0 ReLU, 1 Square, 2 Identity
+    pool2: bool = False  # builder-defined 2x2 max-pool on centered lifts (config 3)
 
 
 def desc_rows(schedule):
@@ -184,7 +185,13 @@ def run_protocol(schedule, image, weights, rand, q, p, n, want=()):
             if lib().eo_activation(flat, flat.size, p, s.fn) != 0:
                 raise OverflowError("square activation exceeds p_a/2")
             val = flat.reshape(rec.shape)
-            fresh = rand.reshare(li, rec.shape[0], H * W).reshape(rec.shape)
+            if getattr(s, "pool2", False):
+                cen = np.where(val > p // 2, val.astype(np.int64) - p, val.astype(np.int64))
+                C_, H_, W_ = cen.shape
+                cen = cen.reshape(C_, H_ // 2, 2, W_ // 2, 2).max(axis=(2, 4))
+                val = np.where(cen < 0, cen + p, cen).astype(np.uint64)
+                H, W = H // 2, W // 2
+            fresh = rand.reshare(li, val.shape[0], H * W).reshape(val.shape)
             if li + 1 == len(schedule):
                 out = val
             alice = (val + np.uint64(p) - fresh) % np.uint64(p)

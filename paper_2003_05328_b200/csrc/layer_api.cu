@@ -194,6 +194,40 @@ __global__ void recombine_kernel(const uint32_t* a, const uint32_t* b, size_t co
   }
 }
 
+__global__ void activation_kernel(const uint32_t* a, const uint32_t* b, int fn, int pool, int C, int H, int W,
+                                  size_t total, uint32_t p, uint32_t layer, uint32_t image_base, uint64_t key,
+                                  const uint32_t* inj, uint32_t* na, uint32_t* nb, int* overflow) {
+  const int oh = pool ? H / 2 : H, ow = pool ? W / 2 : W;
+  const int64_t half = p / 2;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % ((size_t)oh * ow));
+    const size_t ic = idx / ((size_t)oh * ow);  // img * C + c
+    const int c = (int)(ic % C), img = (int)(ic / C);
+    const int r = i / ow, col = i % ow;
+    int64_t best = 0;
+    const int np = pool ? 4 : 1;
+    for (int t = 0; t < np; ++t) {
+      const int rr = pool ? 2 * r + (t >> 1) : r, cc = pool ? 2 * col + (t & 1) : col;
+      const size_t src = ic * (size_t)H * W + (size_t)rr * W + cc;
+      uint32_t rec = a[src] % p + b[src] % p;
+      rec = rec >= p ? rec - p : rec;
+      int64_t y = rec > p / 2 ? (int64_t)rec - (int64_t)p : (int64_t)rec;  // decode_signed
+      int64_t o = y;
+      if (fn == 0) o = y > 0 ? y : 0;
+      else if (fn == 1) {
+        o = y * y;
+        if (o > half && overflow) atomicOr(overflow, 1);
+      }
+      best = t == 0 ? o : (o > best ? o : best);
+    }
+    int64_t m = best % (int64_t)p;
+    const uint32_t v = (uint32_t)(m < 0 ? m + p : m);  // encode_signed
+    const uint32_t fresh = inj ? inj[idx] : draw_uniform_p(key, stream_id(PURPOSE_RESHARE, layer, image_base + img, c, 0), i, p);
+    nb[idx] = fresh;
+    na[idx] = v >= fresh ? v - fresh : v + p - fresh;
+  }
+}
+
 struct Workspace {
   uint64_t* ct_in;
   uint64_t* ct_out;
@@ -346,6 +380,25 @@ int ensei_gpu_alice_decrypt(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, con
     Geo g = geometry(ctx, desc);
     LayerRun r = make_run(ctx, desc, g, num_images, nullptr, stream);
     dec(r, d_key, key_stride, d_ct_out, d_alice_share, nullptr, nullptr, (int)(num_images * desc->cout));
+  });
+}
+
+int ensei_gpu_activation(ensei_gpu_ctx* ctx, int fn, int pool2, uint32_t channels, uint32_t H, uint32_t W,
+                         uint32_t num_images, const uint32_t* d_a, const uint32_t* d_b, const ensei_randomness* rand,
+                         uint32_t* d_new_a, uint32_t* d_new_b, int* d_overflow, void* stream) {
+  return guarded([&] {
+    require(ctx && d_a && d_b && d_new_a && d_new_b, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    require(fn >= 0 && fn <= 2, ENSEI_ERR_INVALID_ARGUMENT, "bad activation fn");
+    require(!pool2 || (H % 2 == 0 && W % 2 == 0), ENSEI_ERR_BAD_GEOMETRY, "2x2 pooling needs even dims");
+    const size_t total = (size_t)num_images * channels * (pool2 ? (H / 2) * (W / 2) : H * W);
+    if (!total) return;
+    const bool inj = rand && rand->mode == ENSEI_RAND_INJECTED;
+    size_t grid = std::min<size_t>((total + 255) / 256, (size_t)ctx->sm_count * 16);
+    activation_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+        d_a, d_b, fn, pool2, (int)channels, (int)H, (int)W, total, (uint32_t)ctx->p, rand ? rand->layer : 0,
+        rand ? rand->image_base : 0, rand ? rand->alice_key : 0, inj ? rand->d_share : nullptr, d_new_a, d_new_b,
+        d_overflow);
+    check_launch("activation_kernel");
   });
 }
 

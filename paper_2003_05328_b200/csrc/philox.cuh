@@ -5,7 +5,7 @@
 // Stream ids are keyed by (purpose, layer, GLOBAL image, channel, block) and the
 // index by the NATURAL slot / coefficient number, so results do not depend on the
 // device layout, the launch shape or how images are sharded across GPUs.  The
-// oracle restates the same streams (oracle/ensei_oracle.c eo_rand_*).
+// test oracle restates the same streams (eo_rand_* in the oracle directory).
 #pragma once
 #include "modarith.cuh"
 

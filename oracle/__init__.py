@@ -96,6 +96,7 @@ def lib():
             "eo_conv_direct": (None, [C.POINTER(Layer), u64p, i64p, u64p]),
             "eo_activation": (C.c_int, [u64p, C.c_size_t, U64, C.c_int]),
             "eo_crt_round": (U64, [u64p, u64p, U32, U64]),
+            "eo_alice_decrypt_rns": (None, [C.c_void_p, U32, u64p, u64p, u64p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

@@ -775,3 +775,44 @@ uint64_t eo_crt_round(const uint64_t* res, const uint64_t* qs, uint32_t R, uint6
   }
   return quo % p;
 }
+
+void eo_alice_decrypt_rns(const eo_layer* Ls, uint32_t R, const uint64_t* t_evals,
+                          const uint64_t* ct_out, uint64_t* alice_share) {
+  const eo_layer* L = &Ls[0];
+  uint32_t n = L->n, B = L->blocks;
+  uint64_t p = L->p;
+  uint64_t qs[8];
+  eo_plan* pq[8];
+  for (uint32_t r = 0; r < R; ++r) {
+    qs[r] = Ls[r].q;
+    pq[r] = eo_plan_create(qs[r], n);
+  }
+  eo_plan* pp = eo_plan_create(p, n);
+  uint64_t* phi = (uint64_t*)malloc(8 * (size_t)R * n);
+  uint64_t* merged = (uint64_t*)malloc(8 * (size_t)B * n);
+  for (uint32_t o = 0; o < L->cout; ++o) {
+    for (uint32_t b = 0; b < B; ++b) {
+      const uint64_t* base = ct_out + ((size_t)o * B + b) * 2 * R * n;
+      for (uint32_t r = 0; r < R; ++r) { /* phi_r = INTT(c0 t + c1) mod q_r (REF ringbfv.cpp:208-212) */
+        const uint64_t* c0 = base + (size_t)r * n;
+        const uint64_t* c1 = base + (size_t)(R + r) * n;
+        uint64_t* ph = phi + (size_t)r * n;
+        for (uint32_t i = 0; i < n; ++i)
+          ph[i] = eo_addmod(eo_mulmod(c0[i], t_evals[(size_t)r * n + i], qs[r]), c1[i], qs[r]);
+        eo_plan_inverse(pq[r], ph);
+      }
+      uint64_t* m = merged + (size_t)b * n;
+      uint64_t res[8];
+      for (uint32_t i = 0; i < n; ++i) {
+        for (uint32_t r = 0; r < R; ++r) res[r] = phi[(size_t)r * n + i];
+        m[i] = eo_crt_round(res, qs, R, p);
+      }
+      eo_plan_forward(pp, m); /* decode_slots */
+    }
+    grid_inverse_crop(L, merged, alice_share + (size_t)o * L->oh * L->ow);
+  }
+  free(phi);
+  free(merged);
+  for (uint32_t r = 0; r < R; ++r) eo_plan_destroy(pq[r]);
+  eo_plan_destroy(pp);
+}

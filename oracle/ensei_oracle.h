@@ -130,6 +130,10 @@ void eo_conv_direct(const eo_layer* L, const uint64_t* in, const int64_t* w, uin
 int eo_activation(uint64_t* v, size_t len, uint64_t p, int fn);
 
 /* ---- RNS (config 4; builder extension, unpinned) ---- */
+/* Alice decrypt over an RNS chain: Ls[r] = the layer with q = q_r (delta unused),
+   t_evals[r][n], ct_out[cout][B][2][R][n] (natural order); exact CRT rounding. */
+void eo_alice_decrypt_rns(const eo_layer* Ls, uint32_t R, const uint64_t* t_evals,
+                          const uint64_t* ct_out, uint64_t* alice_share);
 /* exact CRT rounding: m = round(p * phi / Q) mod p for phi given by residues mod q_i */
 uint64_t eo_crt_round(const uint64_t* res, const uint64_t* qs, uint32_t R, uint64_t p);
 

@@ -25,7 +25,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import (MTRng, PURPOSE_AHAT, PURPOSE_NOISE, PURPOSE_RESHARE, PURPOSE_SECRET,
+from . import (Layer, MTRng, PURPOSE_AHAT, PURPOSE_NOISE, PURPOSE_RESHARE, PURPOSE_SECRET,
                PURPOSE_SHARE, SALT_ALICE, SALT_BOB, layer, lib, rand_cbd, rand_ternary,
                rand_uniform_p, rand_uniform_q, stream_id)
 
@@ -199,3 +199,70 @@ def run_protocol(schedule, image, weights, rand, q, p, n, want=()):
     if out is None:
         out = (alice + bob) % np.uint64(p)
     return out, trace
+
+
+# ------------------------------------------------------------------ RNS (config 4)
+
+def rns_delta(qs, p):
+    """floor(Q/p) mod q_r for Q = prod q_r (every q_r == 1 mod p, so Q == 1 mod p)."""
+    Q = 1
+    for q in qs:
+        Q *= q
+    return [((Q - 1) // p) % q for q in qs]
+
+
+def rns_layers(qs, p, n, H, W, fh, fw, same, cin, cout):
+    Ls = []
+    for q, d in zip(qs, rns_delta(qs, p)):
+        L = layer(q, p, n, H, W, fh, fw, same, cin, cout)
+        L.delta = d
+        Ls.append(L)
+    return Ls
+
+
+class PhiloxRandomnessRNS(PhiloxRandomness):
+    """Per-prime a^ streams (block field | prime << 12), shared noise and shares."""
+
+    def __init__(self, seed, image, n, qs, p, cbd_k=20):
+        super().__init__(seed, image, n, qs[0], p, cbd_k)
+        self.qs = qs
+
+    def enc_rns(self, layer_idx, cin, blocks):
+        R = len(self.qs)
+        e = np.empty((cin, blocks, self.n), np.int64)
+        a = np.empty((cin, blocks, R, self.n), np.uint64)
+        for c in range(cin):
+            for b in range(blocks):
+                e[c, b] = rand_cbd(self.ka, stream_id(PURPOSE_NOISE, layer_idx, self.image, c, b), self.n, self.k)
+                for r, q in enumerate(self.qs):
+                    a[c, b, r] = rand_uniform_q(self.ka, stream_id(PURPOSE_AHAT, layer_idx, self.image, c, b | (r << 12)),
+                                                self.n, q)
+        return e, a
+
+
+def run_layer_rns(Ls, t_evals, alice_in, w_evals, e, a, s_b):
+    """One RNS conv layer (first layer: no HomRec) for one image; per-prime Enc /
+    ElementMult / HomShare with the single-prime restatement, CRT decryption."""
+    R = len(Ls)
+    L0 = Ls[0]
+    n, B = L0.n, L0.blocks
+    ct_in = np.zeros((L0.cin, B, 2, R, n), np.uint64)
+    ct_out = np.zeros((L0.cout, B, 2, R, n), np.uint64)
+    bob = None
+    for r, L in enumerate(Ls):
+        ct = np.zeros(L.cin * B * 2 * n, np.uint64)
+        lib().eo_alice_encrypt(C.byref(L), t_evals[r], np.ascontiguousarray(alice_in, np.uint64).reshape(-1),
+                               np.ascontiguousarray(e, np.int64).reshape(-1),
+                               np.ascontiguousarray(a[:, :, r], np.uint64).reshape(-1), ct)
+        ct_in[:, :, :, r] = ct.reshape(L.cin, B, 2, n)
+        co = np.zeros(L.cout * B * 2 * n, np.uint64)
+        bs = np.zeros(L.cout * L.oh * L.ow, np.uint64)
+        lib().eo_bob_eval(C.byref(L), ct, np.ascontiguousarray(w_evals[r], np.uint64).reshape(-1), None,
+                          np.ascontiguousarray(s_b, np.uint64).reshape(-1), co, bs)
+        ct_out[:, :, :, r] = co.reshape(L.cout, B, 2, n)
+        bob = bs.reshape(L.cout, L.oh, L.ow)
+    arr = (Layer * R)(*Ls)
+    al = np.zeros(L0.cout * L0.oh * L0.ow, np.uint64)
+    te = np.ascontiguousarray(np.stack(t_evals), np.uint64).reshape(-1)
+    lib().eo_alice_decrypt_rns(C.cast(arr, C.c_void_p), R, te, np.ascontiguousarray(ct_out).reshape(-1), al)
+    return {"alice": al.reshape(L0.cout, L0.oh, L0.ow), "bob": bob, "ct_in": ct_in, "ct_out": ct_out}

@@ -48,6 +48,8 @@ struct PrimeConst {
   uint64_t cp;            // floor(p * 2^64 / q), decryption rounding estimate
   uint32_t a2_chunk;      // MAC: channels per full reduction of the top limb
   uint64_t c64, c64p;     // 2^64 mod q and its Shoup companion
+  uint64_t crt_inv, crt_inv_shoup;  // (Q/q_i)^-1 mod q_i (RNS decryption)
+  double inv_q;                     // 1/q_i
 };
 
 struct PConst {
@@ -84,4 +86,8 @@ struct ensei_gpu_ctx {
   ensei_gpu::DeviceTables tab;
   void* table_mem = nullptr;
   bool approx_ok = true;  // every q_i < 2^61: approximate-quotient butterflies (MODE 0)
+  // fork/join helpers: Bob's input-independent HomShare work runs concurrently
+  // with Alice's encryption on an auxiliary stream (capturable in CUDA graphs)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };

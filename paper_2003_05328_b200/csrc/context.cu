@@ -129,6 +129,12 @@ static void ctx_create(int device, uint32_t n, const uint64_t* qs, uint32_t R, u
     // A2 accumulates x1*y1 < ((q >> 30) + 1)^2 per channel; stay below 2^63
     unsigned __int128 top = (unsigned __int128)((q >> 30) + 1) * ((q >> 30) + 1);
     uint64_t cap = (uint64_t)(((unsigned __int128)1 << 63) / top);
+    uint64_t qi_prod = 1;
+    for (uint32_t j = 0; j < R; ++j)
+      if (j != i) qi_prod = mulmod(qi_prod, c->q[j] % q, q);
+    pc.crt_inv = invmod(qi_prod, q);
+    pc.crt_inv_shoup = shoup64(pc.crt_inv, q);
+    pc.inv_q = 1.0 / (double)q;
     pc.c64 = (uint64_t)(0 - q) % q;
     pc.c64p = shoup64(pc.c64, q);
     pc.a2_chunk = (uint32_t)std::max<uint64_t>(7, std::min<uint64_t>(56, cap / 7 * 7));
@@ -139,6 +145,9 @@ static void ctx_create(int device, uint32_t n, const uint64_t* qs, uint32_t R, u
   EG_CUDA(cudaSetDevice(device));
   EG_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
   build_tables(c.get());
+  EG_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+  EG_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  EG_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   *out = c.release();
 }
 
@@ -160,6 +169,9 @@ int ensei_gpu_ctx_create(int device, uint32_t n, const uint64_t* q_primes, uint3
 void ensei_gpu_ctx_destroy(ensei_gpu_ctx* ctx) {
   if (!ctx) return;
   if (ctx->table_mem) cudaFree(ctx->table_mem);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   delete ctx;
 }
 

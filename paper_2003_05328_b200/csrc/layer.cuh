@@ -84,6 +84,23 @@ __host__ __device__ constexpr int ct_words(int n) {
   return 2 * R * n;
 }
 
+// phi = c0 t^ + c1 (device layout) as the input view of the decryption INTT;
+// reduced to [0, 4q + 2^32) for the Gentleman-Sande bounds.
+struct PhiSrc {
+  const uint64_t *c0, *c1, *t, *tp;
+  Field64 f;
+  static constexpr bool kVec = true;
+  EG_DEV uint64_t at(int j) const {
+    uint64_t x = f.mul_shoup_approx(c0[j], t[j], tp[j]) + c1[j];  // < 5q
+    return hi32(x) > hi32(f.q4) ? x - f.q4 : x;
+  }
+  EG_DEV uint64_t operator()(int j) const { return at(j); }
+  EG_DEV void ld2(int j, uint64_t& x, uint64_t& y) const {
+    x = at(j);
+    y = at(j + 1);
+  }
+};
+
 // ------------------------------------------------------------ tile -> ring
 
 enum TileMode { TILE_ENC = 0, TILE_HOMREC = 1, TILE_WEIGHTS = 2 };
@@ -274,6 +291,91 @@ __global__ void __launch_bounds__((1 << LOGN) >> kLogE)
   }
 }
 
+// RNS decryption (config 4): per prime r, phi_r = INTT_{q_r}(c0 t^ + c1), y_r = phi_r *
+// (Q/q_r)^-1 mod q_r; with phi = sum_r y_r Q/q_r - kQ,  p phi / Q = sum_r y_r p / q_r - kp,
+// so round(p phi / Q) mod p = (sum_r floor(y_r p / q_r) + round(sum_r frac_r)) mod p.
+// The integer parts are exact (remainder arithmetic as in dec_kernel); the fractional
+// parts are summed in double precision (exact rounding unless the true value lies within
+// ~2^-50 of a half-integer, i.e. unless decryption has already failed).  Builder
+// extension: REF has no RNS; pinned by the oracle's exact
+// multi-limb CRT rounding (eo_crt_round).
+template <int LOGN, int LOGH, int LOGW, int R>
+__global__ void __launch_bounds__((1 << LOGN) >> kLogE)
+    dec_rns_kernel(LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride,
+                   const uint64_t* __restrict__ ct, uint32_t* __restrict__ alice_share,
+                   const uint32_t* __restrict__ bob_share, uint32_t* __restrict__ outp) {
+  constexpr int N = 1 << LOGN, NT = N >> kLogE;
+  constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
+  double* facc = reinterpret_cast<double*>(qbuf + N);
+  uint32_t* pbuf = reinterpret_cast<uint32_t*>(facc + N);  // integer-part accumulator, then m
+  uint32_t* S = pbuf + ssize<uint32_t>(N);
+  const int tid = threadIdx.x;
+  const CtaBar bar;
+  const Field32 pf = a.pp.f;
+  const uint32_t p = pf.q;
+  const int item = blockIdx.x;
+  const int img = item / a.cout;
+  const uint64_t* kimg = key + (size_t)img * key_stride;
+  for (int i = tid; i < Lh * LS; i += NT) S[i] = 0;
+  for (int b = 0; b < a.B; ++b) {
+    const uint64_t* cb = ct + ((size_t)item * a.B + b) * ct_words<R>(N);
+    for (int i = tid; i < N; i += NT) {
+      pbuf[sidx<uint32_t>(i)] = 0;
+      facc[i] = 0.0;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) {
+      const PrimeConst pc = a.pc[r];
+      const Field64 f = pc.f;
+      PhiSrc src{cb + (size_t)r * N, cb + (size_t)(R + r) * N, kimg + (size_t)(2 * r) * N,
+                 kimg + (size_t)(2 * r + 1) * N, f};
+      auto dst = [&](int i, uint64_t v) {
+        const uint64_t phi = Bfly<Field64, 0>::fin_gs(f, v);
+        const uint64_t y = Bfly<Field64, 0>::fin_gs(f, f.mul_shoup_approx(phi, pc.crt_inv, pc.crt_inv_shoup));
+        uint64_t I = mulhi64(y, pc.cp);  // floor(y p / q_r), corrected below
+        uint64_t rem = (uint64_t)p * y - I * f.q;
+        while (rem >= f.q) {
+          rem -= f.q;
+          ++I;
+        }
+        uint32_t acc = pbuf[sidx<uint32_t>(i)] + (uint32_t)(I % p);
+        pbuf[sidx<uint32_t>(i)] = acc >= p ? acc - p : acc;
+        facc[i] += (double)rem * pc.inv_q;
+      };
+      ntt_inverse<Field64, uint64_t, LOGN, kLogE, 0, false, false>(f, a.twq_inv[r], qbuf, tid, src, dst, bar);
+      __syncthreads();
+    }
+    for (int i = tid; i < N; i += NT) {
+      uint32_t m = pbuf[sidx<uint32_t>(i)] + (uint32_t)__double2int_rn(facc[i]);
+      pbuf[sidx<uint32_t>(i)] = m % p;
+    }
+    __syncthreads();
+    SmemRW<uint32_t> psrc{pbuf};
+    auto pdst = [&](int j, uint32_t v) { scatter_slot<LOGN, LOGH, LOGW>(S, b, j, a.G, reduce_lazy(pf, v, a.pp.cred)); };
+    ntt_forward<Field32, uint32_t, LOGN, kLogE, 0, false, false>(pf, a.twp_fwd, pbuf, tid, psrc, pdst, bar);
+    __syncthreads();
+  }
+  tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, S, LS);
+  const size_t base = (size_t)item * a.oh * a.ow;
+  for (int i = tid; i < a.oh * a.ow; i += NT) {
+    const int r = i / a.ow, c = i % a.ow;
+    const uint32_t s = S[(r + a.r0) * LS + c + a.c0];
+    if (alice_share) alice_share[base + i] = s;
+    if (outp) {
+      uint32_t y = s + bob_share[base + i];
+      outp[base + i] = y >= p ? y - p : y;
+    }
+  }
+}
+
+template <int LOGN, int LOGH, int LOGW>
+constexpr size_t dec_rns_smem() {
+  return (size_t)(1 << LOGN) * 16 + ssize<uint32_t>(1 << LOGN) * 4 + (size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4;
+}
+
 template <int LOGN, int LOGH, int LOGW>
 constexpr size_t share_smem() {
   return (size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4 + (size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4;
@@ -281,22 +383,6 @@ constexpr size_t share_smem() {
 
 // ---------------------------------------------------------------- decrypt
 
-// phi = c0 t^ + c1 (device layout) as the input view of the decryption INTT;
-// reduced to [0, 4q + 2^32) for the Gentleman-Sande bounds.
-struct PhiSrc {
-  const uint64_t *c0, *c1, *t, *tp;
-  Field64 f;
-  static constexpr bool kVec = true;
-  EG_DEV uint64_t at(int j) const {
-    uint64_t x = f.mul_shoup_approx(c0[j], t[j], tp[j]) + c1[j];  // < 5q
-    return hi32(x) > hi32(f.q4) ? x - f.q4 : x;
-  }
-  EG_DEV uint64_t operator()(int j) const { return at(j); }
-  EG_DEV void ld2(int j, uint64_t& x, uint64_t& y) const {
-    x = at(j);
-    y = at(j + 1);
-  }
-};
 
 
 // One CTA per (image, out channel): phi = c0 t^ + c1 -> INTT_q -> round(p phi / q)
@@ -380,86 +466,113 @@ EG_DEV uint64_t mac_reduce(const Field64& f, const PrimeConst& pc, uint64_t a0, 
 
 // Per slot s (ring position of one (block, prime)), the rows (img, comp) times
 // cols (out channel) product over K = cin:  out = sum_c ct[img][c][comp] w[o][c]
-// (mod q), + mask on comp 1.  Lazy accumulation with 30-bit limbs: for x, y < 2^60,
-// x = x1 2^30 + x0, y = y1 2^30 + y0; A0 += x0 y0, A1 += x0 y1 + x1 y0, A2 += x1 y1
-// (four full-rate mad.wide per MAC, no carries), folded every 8 channels and reduced
-// once per output.  The tile is staged in shared memory so every ct / weight word is
-// read from HBM once per CTA.
-template <int R, int S, int MT, int NTL, int KT>
-__global__ void __launch_bounds__(S*(MT / 4) * (NTL / 4))
+// (mod q), + the HomShare mask already sitting in out's c1 words.  Lazy accumulation
+// with 30-bit limbs: for x, y < 2^60, x = x1 2^30 + x0, y = y1 2^30 + y0;
+// A0 += x0 y0, A1 += x0 y1 + x1 y0, A2 += x1 y1 (four full-rate mad.wide per MAC, no
+// carries), folded every 7 channels, fully reduced every a2_chunk channels, reduced
+// once per output.  CTA tile = S slots x MT rows x NT cols; shared tiles [k][row][slot]
+// (slot-contiguous) are filled with 16-byte cp.async, double-buffered over K chunks,
+// so every ct / weight word crosses HBM once per CTA.
+template <int R, int S, int MT, int NT, int KT, int TM, int TN>
+__global__ void __launch_bounds__(S*(MT / TM) * (NT / TN))
     mac_kernel(LayerArgs a, int logn, const uint64_t* __restrict__ ct, const uint64_t* __restrict__ w,
                int has_mask, uint64_t* __restrict__ out) {
-  constexpr int TMR = MT / 4, TNC = NTL / 4, NTH = S * TMR * TNC;
-  __shared__ uint64_t As[KT][S][MT + 1];
-  __shared__ uint64_t Bs[KT][S][NTL + 1];
+  constexpr int NTH = S * (MT / TM) * (NT / TN);
+  constexpr int SV = S / 2;  // 16-byte chunks per (k, row)
+  extern __shared__ __align__(16) uint64_t smac[];
+  uint64_t* As = smac;                     // [2][KT][MT][S]
+  uint64_t* Bs = smac + 2 * KT * MT * S;   // [2][KT][NT][S]
   const int n = 1 << logn;
-  const int BR = a.B * R;                  // (block, prime) pairs
-  const int s0 = blockIdx.x * S;           // first slot of this CTA over BR*n
-  const int bp = s0 >> logn;               // (b, r) pair
-  const int r = bp % R;
+  const int s0 = blockIdx.x * S;           // first slot of this CTA over B*R*n
+  const int bp = s0 >> logn;               // (block, prime) pair index
+  const int b = bp / R, r = bp % R;
   const int k0 = s0 & (n - 1);
   const int rows = 2 * a.num_images, cols = a.cout, K = a.cin;
-  const int row0 = blockIdx.y * MT, col0 = blockIdx.z * NTL;
+  const int row0 = blockIdx.y * MT, col0 = blockIdx.z * NT;
   const int tid = threadIdx.x;
-  const int sl = tid % S, tm = (tid / S) % TMR, tn = tid / (S * TMR);
+  const int sl = tid % S, tm = (tid / S) % (MT / TM), tn = tid / (S * (MT / TM));
   const PrimeConst pc = a.pc[r];
   const Field64 f = pc.f;
   const size_t ctw = (size_t)ct_words<R>(n);
-  // ct word address: ((img*cin + c)*B + b)*2Rn + (comp*R + r)*n + k
-  auto ct_addr = [&](int row, int c, int k) -> size_t {
-    const int img = row >> 1, comp = row & 1;
-    return (((size_t)img * a.cin + c) * a.B + bp / R) * ctw + (size_t)(comp * R + r) * n + k;
-  };
-  uint64_t A0[4][4], A1[4][4], A2[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) A0[i][j] = A1[i][j] = A2[i][j] = 0;
+  const size_t chan_stride = (size_t)a.B * ctw;        // ct: next channel
+  const size_t w_chan = (size_t)a.B * R * n;            // w: next input channel
   constexpr uint64_t M30 = (1ull << 30) - 1;
-  int since_fold = 0, since_full = 0;
-  for (int kc = 0; kc < K; kc += KT) {
-    __syncthreads();
-    for (int e = tid; e < KT * MT * S; e += NTH) {
-      const int s = e % S, row = (e / S) % MT, kk = e / (S * MT);
+
+  auto load_chunk = [&](int buf, int kc) {
+    uint64_t* Ab = As + buf * KT * MT * S;
+    uint64_t* Bb = Bs + buf * KT * NT * S;
+    for (int e = tid; e < KT * MT * SV; e += NTH) {
+      const int v = e % SV, row = (e / SV) % MT, kk = e / (SV * MT);
       const int gr = row0 + row, c = kc + kk;
-      uint64_t x = 0;
+      uint64_t* dst = Ab + (kk * MT + row) * S + 2 * v;
       if (gr < rows && c < K) {
-        x = ct[ct_addr(gr, c, k0 + s)];
-        x = ((x >> 30) << 32) | (x & M30);
+        const uint64_t* src = ct + ((size_t)(gr >> 1) * a.cin + c) * chan_stride + (size_t)b * ctw +
+                              (size_t)((gr & 1) * R + r) * n + k0 + 2 * v;
+        cp_async16(dst, src);
+      } else {
+        dst[0] = 0;
+        dst[1] = 0;
       }
-      As[kk][s][row] = x;
     }
-    for (int e = tid; e < KT * NTL * S; e += NTH) {
-      const int s = e % S, col = (e / S) % NTL, kk = e / (S * NTL);
+    for (int e = tid; e < KT * NT * SV; e += NTH) {
+      const int v = e % SV, col = (e / SV) % NT, kk = e / (SV * NT);
       const int go = col0 + col, c = kc + kk;
-      uint64_t x = 0;
-      if (go < cols && c < K) x = w[(((size_t)go * a.cin + c) * BR + bp) * n + k0 + s];
-      Bs[kk][s][col] = x;
+      uint64_t* dst = Bb + (kk * NT + col) * S + 2 * v;
+      if (go < cols && c < K) {
+        cp_async16(dst, w + ((size_t)go * a.cin + c) * w_chan + (size_t)bp * n + k0 + 2 * v);
+      } else {
+        dst[0] = 0;
+        dst[1] = 0;
+      }
+    }
+    cp_async_commit();
+  };
+
+  uint64_t A0[TM][TN], A1[TM][TN], A2[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) A0[i][j] = A1[i][j] = A2[i][j] = 0;
+  int since_fold = 0, since_full = 0;
+  const int nchunks = (K + KT - 1) / KT;
+  load_chunk(0, 0);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int buf = ch & 1;
+    if (ch + 1 < nchunks) {
+      load_chunk(buf ^ 1, (ch + 1) * KT);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      cp_async_wait_all();
     }
     __syncthreads();
-    const int kmax = min(KT, K - kc);
+    const uint64_t* Ab = As + buf * KT * MT * S;
+    const uint64_t* Bb = Bs + buf * KT * NT * S;
+    const int kmax = min(KT, K - ch * KT);
     for (int kk = 0; kk < kmax; ++kk) {
-      uint32_t x0[4], x1[4], y0[4], y1[4];
+      uint32_t x0[TM], x1[TM], y0[TN], y1[TN];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint64_t v = As[kk][sl][tm * 4 + i];
-        x0[i] = lo32(v);
-        x1[i] = hi32(v);
+      for (int i = 0; i < TM; ++i) {
+        const uint64_t v = Ab[(kk * MT + tm * TM + i) * S + sl];
+        x0[i] = (uint32_t)(v & M30);
+        x1[i] = (uint32_t)(v >> 30);
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint64_t v = Bs[kk][sl][tn * 4 + j];
+      for (int j = 0; j < TN; ++j) {
+        const uint64_t v = Bb[(kk * NT + tn * TN + j) * S + sl];
         y0[j] = lo32(v);
         y1[j] = hi32(v);
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          A0[i][j] = madw(x0[i], y0[j], A0[i][j]);
-          A1[i][j] = madw(x0[i], y1[j], A1[i][j]);
-          A1[i][j] = madw(x1[i], y0[j], A1[i][j]);
-          A2[i][j] = madw(x1[i], y1[j], A2[i][j]);
+        for (int j = 0; j < TN; ++j) {
+          // accumulate in place (one IMAD.WIDE.U32 each, accumulator stays a register pair)
+          asm("mad.wide.u32 %0, %3, %5, %0;\n\t"
+              "mad.wide.u32 %1, %3, %6, %1;\n\t"
+              "mad.wide.u32 %1, %4, %5, %1;\n\t"
+              "mad.wide.u32 %2, %4, %6, %2;"
+              : "+l"(A0[i][j]), "+l"(A1[i][j]), "+l"(A2[i][j])
+              : "r"(x0[i]), "r"(x1[i]), "r"(y0[j]), "r"(y1[j]));
         }
       ++since_fold;
       ++since_full;
@@ -468,9 +581,9 @@ __global__ void __launch_bounds__(S*(MT / 4) * (NTL / 4))
         if (since_full >= (int)pc.a2_chunk) {  // top limb near capacity: reduce mod q
           since_full = 0;
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < TM; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < TN; ++j) {
               const uint64_t z = mac_reduce(f, pc, A0[i][j], A1[i][j], A2[i][j]);
               A0[i][j] = z & M30;
               A1[i][j] = z >> 30;
@@ -478,9 +591,9 @@ __global__ void __launch_bounds__(S*(MT / 4) * (NTL / 4))
             }
         } else {
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < TM; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < TN; ++j) {
               A1[i][j] += A0[i][j] >> 30;
               A0[i][j] &= M30;
               A2[i][j] += A1[i][j] >> 30;
@@ -489,19 +602,20 @@ __global__ void __launch_bounds__(S*(MT / 4) * (NTL / 4))
         }
       }
     }
+    __syncthreads();  // this buffer is refilled two chunks later
   }
   const int k = k0 + sl;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int gr = row0 + tm * 4 + i;
+  for (int i = 0; i < TM; ++i) {
+    const int gr = row0 + tm * TM + i;
     if (gr >= rows) continue;
     const int img = gr >> 1, comp = gr & 1;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int go = col0 + tn * 4 + j;
+    for (int j = 0; j < TN; ++j) {
+      const int go = col0 + tn * TN + j;
       if (go >= cols) continue;
       uint64_t x = mac_reduce(f, pc, A0[i][j], A1[i][j], A2[i][j]);
-      const size_t oa = (((size_t)img * a.cout + go) * a.B + bp / R) * ctw + (size_t)(comp * R + r) * n + k;
+      const size_t oa = ((size_t)img * a.cout + go) * chan_stride + (size_t)b * ctw + (size_t)(comp * R + r) * n + k;
       if (comp == 1 && has_mask) {  // HomShare mask written in place by share_kernel
         x += out[oa];
         x = x >= f.q ? x - f.q : x;
@@ -509,6 +623,11 @@ __global__ void __launch_bounds__(S*(MT / 4) * (NTL / 4))
       out[oa] = x;
     }
   }
+}
+
+template <int S, int MT, int NT, int KT>
+constexpr size_t mac_smem() {
+  return (size_t)2 * KT * (MT + NT) * S * sizeof(uint64_t);
 }
 
 }  // namespace ensei_gpu

@@ -164,11 +164,14 @@ void secret(const LayerRun& r, const int64_t* t_in, int64_t* t_out, uint64_t* ke
   fail(ENSEI_ERR_UNSUPPORTED, "ring degree must be 2048, 4096 or 8192 on this path");
 }
 
-template <int R, int S, int MT, int NTL, int KT>
+template <int R, int S, int MT, int NT, int KT, int TM, int TN>
 void mac_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
   const int n = (int)r.ctx->n, rows = 2 * r.a.num_images, cols = r.a.cout;
-  dim3 grid((unsigned)(r.a.B * R * n / S), (unsigned)((rows + MT - 1) / MT), (unsigned)((cols + NTL - 1) / NTL));
-  mac_kernel<R, S, MT, NTL, KT><<<grid, S * (MT / 4) * (NTL / 4), 0, r.st>>>(r.a, (int)r.ctx->logn, ct, w, 1, out);
+  auto k = mac_kernel<R, S, MT, NT, KT, TM, TN>;
+  constexpr size_t smem = mac_smem<S, MT, NT, KT>();
+  set_smem(k, smem);
+  dim3 grid((unsigned)(r.a.B * R * n / S), (unsigned)((rows + MT - 1) / MT), (unsigned)((cols + NT - 1) / NT));
+  k<<<grid, S * (MT / TM) * (NT / TN), smem, r.st>>>(r.a, (int)r.ctx->logn, ct, w, 1, out);
   check_launch("mac_kernel");
 }
 
@@ -177,12 +180,12 @@ void mac(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out
   const int rows = 2 * r.a.num_images, cols = r.a.cout;
   const bool small = rows <= 16 && cols <= 16;
   if (r.R == 1) {
-    if (small) return mac_go<1, 16, 16, 16, 8>(r, ct, w, out);
-    return mac_go<1, 8, 32, 32, 8>(r, ct, w, out);
+    if (small) return mac_go<1, 16, 16, 16, 16, 2, 4>(r, ct, w, out);
+    return mac_go<1, 8, 32, 32, 16, 4, 4>(r, ct, w, out);
   }
   if (r.R == 3) {
-    if (small) return mac_go<3, 16, 16, 16, 8>(r, ct, w, out);
-    return mac_go<3, 8, 32, 32, 8>(r, ct, w, out);
+    if (small) return mac_go<3, 16, 16, 16, 16, 2, 4>(r, ct, w, out);
+    return mac_go<3, 8, 32, 32, 16, 4, 4>(r, ct, w, out);
   }
   fail(ENSEI_ERR_UNSUPPORTED, "ElementMult: unsupported prime count");
 }
@@ -274,9 +277,17 @@ void conv_layer(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uint64_t*
   Workspace w = carve(ctx, desc, g, imgs, ws, in_dtype, false);
   uint32_t* bs = bob_share ? bob_share : w.bob;
   const bool inj = injected(rand);
-  share(r, inj, w.ct_out, bs, (int)(imgs * desc->cout));
+  // Bob's HomShare masks depend only on his randomness: fork them onto the aux stream
+  // so they overlap Alice's encryption; join before the ElementMult consumes them.
+  EG_CUDA(cudaEventRecord(ctx->ev_fork, r.st));
+  EG_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+  LayerRun ra = r;
+  ra.st = ctx->aux;
+  share(ra, inj, w.ct_out, bs, (int)(imgs * desc->cout));
+  EG_CUDA(cudaEventRecord(ctx->ev_join, ctx->aux));
   tile(r, TILE_ENC, inj, in_dtype, key, ks, in, w.ct_in, (int)(imgs * desc->cin));
   if (bob_prev) tile(r, TILE_HOMREC, false, ENSEI_IN_U32, key, 0, bob_prev, w.ct_in, (int)(imgs * desc->cin));
+  EG_CUDA(cudaStreamWaitEvent(r.st, ctx->ev_join, 0));
   mac(r, w.ct_in, w_eval, w.ct_out);
   dec(r, key, ks, w.ct_out, alice_share, bs, out, (int)(imgs * desc->cout));
 }

@@ -121,11 +121,31 @@ static void dec_go(const LayerRun& r, const uint64_t* key, uint32_t ks, const ui
   check_launch("dec_kernel");
 }
 
+template <int LOGN, int LOGL>
+static void dec_rns_go(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint64_t* ct, uint32_t* alice,
+                       const uint32_t* bob, uint32_t* out, int items) {
+  auto k = dec_rns_kernel<LOGN, LOGL, LOGL, 3>;
+  constexpr size_t smem = dec_rns_smem<LOGN, LOGL, LOGL>();
+  set_smem(k, smem);
+  k<<<items, (1 << LOGN) >> kLogE, smem, r.st>>>(r.a, key, ks, ct, alice, bob, out);
+  check_launch("dec_rns_kernel");
+}
+
 template <int LOGN>
 void launch_dec(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint64_t* ct, uint32_t* alice,
                 const uint32_t* bob, uint32_t* out, int items) {
   if (items == 0) return;
-  if (r.R != 1) fail(ENSEI_ERR_UNSUPPORTED, "RNS decryption uses the CRT path (alice_decrypt_rns)");
+  if (r.R != 1) {
+    if constexpr (LOGN == 13) {
+      if (r.R == 3) {
+        switch (r.logL) {
+          case 5: return dec_rns_go<LOGN, 5>(r, key, ks, ct, alice, bob, out, items);
+          case 6: return dec_rns_go<LOGN, 6>(r, key, ks, ct, alice, bob, out, items);
+        }
+      }
+    }
+    fail(ENSEI_ERR_UNSUPPORTED, "RNS decryption: 3 primes at n = 8192 with a 32x32 or 64x64 grid");
+  }
   switch (r.logL) {
     case 1: return dec_go<LOGN, 1>(r, key, ks, ct, alice, bob, out, items);
     case 2: return dec_go<LOGN, 2>(r, key, ks, ct, alice, bob, out, items);

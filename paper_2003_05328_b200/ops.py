@@ -223,7 +223,7 @@ class LayerOps:
         return torch.empty(nb, dtype=torch.uint8, device=self.ctx.device)
 
     def forward(self, key, w_eval, x: torch.Tensor, rand: Randomness, ws=None, bob_prev=None, key_stride: int = 0,
-                want_shares: bool = False, stream=None):
+                want_shares: bool = False, stream=None, out=None):
         """The whole oblivious conv layer for a batch; returns the reconstructed output
         (and the two shares when want_shares)."""
         images = x.shape[0]
@@ -231,7 +231,7 @@ class LayerOps:
         in_t = IN_U8 if x.dtype == torch.uint8 else IN_U32
         ws = self.workspace(images) if ws is None else ws
         shape = (images, self.spec.cout, g.oh, g.ow)
-        out = torch.empty(shape, dtype=torch.int32, device=x.device)
+        out = torch.empty(shape, dtype=torch.int32, device=x.device) if out is None else out
         a = torch.empty(shape, dtype=torch.int32, device=x.device) if want_shares else None
         b = torch.empty(shape, dtype=torch.int32, device=x.device) if want_shares else None
         r = rand.struct()

@@ -189,3 +189,37 @@ def test_geometry_errors(ops):
         ops.LayerOps(ctx, ops.ConvSpec(2, 2, 3, 3, False, 1, 1))
     with pytest.raises(EnseiError, match="Unsupported"):
         ops.LayerOps(ctx, ops.ConvSpec(64, 64, 3, 3, True, 1, 1))  # 128x128 grid
+
+
+def test_rns_config4_shape_vs_oracle(ops):
+    """Config 4 arithmetic: n = 8192, three 60-bit primes (RNS), 64x64 grid (B = 1):
+    ciphertexts per prime, both shares (CRT decryption) vs the oracle's exact CRT."""
+    from gpu_util import RNS
+    n = 8192
+    ctx = ops.Context(n=n, q=RNS)
+    rng = np.random.default_rng(44)
+    img = rng.integers(0, 256, size=(2, 32, 32)).astype(np.int64)
+    w = rng.integers(-128, 128, size=(3, 2, 3, 3)).astype(np.int64)
+    L = ops.LayerOps(ctx, ops.ConvSpec(32, 32, 3, 3, True, 2, 3))
+    t, key = ops.secret_sample(ctx, 5)
+    R = ops.Randomness(seed=5)
+    we = L.prepare_weights(torch.from_numpy(w.astype(np.int32)).to(dev()))
+    x = torch.from_numpy(img.astype(np.uint8)[None]).to(dev())
+    ct = L.alice_encrypt(key, x, R)
+    ct_out, bob = L.bob_eval(ct.clone(), we, R)
+    alice = L.alice_decrypt(key, ct_out)
+    Ls = OP.rns_layers(list(RNS), P, n, 32, 32, 3, 3, 1, 2, 3)
+    pr = OP.PhiloxRandomnessRNS(5, 0, n, list(RNS), P)
+    assert (to_np(t) == pr.secret()).all()
+    te = [OP.secret_eval(Lr, pr.secret()) for Lr in Ls]
+    wr = [OP.prepare_weights(Lr, w) for Lr in Ls]
+    e, a = pr.enc_rns(0, 2, Ls[0].blocks)
+    r = OP.run_layer_rns(Ls, te, img.astype(np.uint64), wr, e, a, pr.share(0, 3, Ls[0].blocks))
+    ctx.permute(ct)
+    assert (to_np(ct[0]) == r["ct_in"]).all()
+    ctx.permute(ct_out)
+    assert (to_np(ct_out[0]) == r["ct_out"]).all()
+    assert (to_np(alice[0]).astype(np.uint64) == r["alice"]).all()
+    assert (to_np(bob[0]).astype(np.uint64) == r["bob"]).all()
+    out = L.forward(key, we, x, R)
+    assert (to_np(out[0]).astype(np.uint64) == _direct(img, w, 32)).all()

@@ -220,7 +220,7 @@ def main():
     lib = _lib.lib()
 
     if args.config != 1:
-        raise SystemExit("only --config 1 (the metric's config) is wired into this bench")
+        return other_config(args, world, rank, local)
     imgs = args.images
     ctx = ops.Context(n=2048, q=(Q,), p=P, device=local)
     spec = ops.ConvSpec(32, 32, 3, 3, True, 16, 16)
@@ -440,6 +440,170 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ configs 0, 2, 3, 4
+
+def _time_steps(fn, steps, warmup, flush, stream):
+    import torch
+    for _ in range(max(3, warmup)):
+        fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        if flush is not None:
+            flush.zero_()
+        ev[i][0].record(stream)
+        fn()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in ev)
+
+
+def _ref_sessions(desc_rows, H, W, cin, instances, threads, seed, n=2048, q=Q):
+    """Reference run_inproc sessions for an arbitrary schedule; online throughput."""
+    import numpy as np
+    import oracle as O
+    g = O.MTRng(seed, 0xDA7A)
+    img = np.array([g.uniform_below(256) for _ in range(cin * H * W)], np.int64)
+    wcount = sum(d[1] * d[2] * d[4] * d[5] for d in desc_rows if d[0] == 0)
+    w = np.array([g.uniform_below(256) - 128 for _ in range(wcount)], np.int64)
+    online = O.C.c_double(0)
+    wall = O.ref().ref_bench_protocol(P, q, n, 4.0, seed, H, W, len(desc_rows),
+                                      np.array(desc_rows, np.int32).reshape(-1), img, w, instances, threads,
+                                      O.C.byref(online))
+    if wall < 0:
+        raise RuntimeError(O.ref().ref_last_error().decode())
+    return instances / (online.value / threads), wall, online.value
+
+
+def other_config(args, world, rank, local):
+    import numpy as np
+    import torch
+    from paper_2003_05328_b200 import _lib, ops
+    from paper_2003_05328_b200 import protocol as GP
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    lib = _lib.lib()
+    gen = torch.Generator().manual_seed(args.seed)
+    cores = host_cores()
+    extra = {}
+    cpu = None
+    if args.config == 0:
+        M = args.images if args.images != 8 else 4096
+        ctx = ops.Context(n=2048, device=local)
+        L = ops.LayerOps(ctx, ops.ConvSpec(32, 32, 3, 3, True, 1, 1))
+        x = torch.randint(0, 256, (M, 1, 32, 32), dtype=torch.uint8, generator=gen).to(dev)
+        w = torch.randint(-128, 128, (1, 1, 3, 3), dtype=torch.int32, generator=gen).to(dev)
+        _, key = ops.secret_sample(ctx, args.seed)
+        we = L.prepare_weights(w)
+        ws = L.workspace(M)
+        out = torch.empty((M, 1, 32, 32), dtype=torch.int32, device=dev)
+        rand = ops.Randomness(seed=args.seed, image_base=rank * M)
+        fn = lambda: L.forward(key, we, x, rand, ws=ws, out=out)  # noqa: E731
+        total = _time_steps(fn, args.steps, args.warmup, flush, stream)
+        value = world * M * args.steps / (total / 1e3)
+        unit, workload = "conv/s", f"config0: {M} independent 1->1 3x3 Same convs of 32x32 uint8 per step, n=2048"
+        if rank == 0 and not args.no_cpu_baseline:
+            thr = max(1, cores // 2)
+            v, wall, _ = _ref_sessions([[0, 3, 3, 1, 1, 1, 0]], 32, 32, 1, max(thr, 32), thr, args.seed)
+            cpu = {"value": v, "unit": unit, "cores": cores, "kind": "reference",
+                   "sample": f"{max(thr, 32)} reference run_inproc sessions (config 0), {thr} concurrent, online"}
+    elif args.config == 2:
+        n = 2048
+        ctx = ops.Context(n=n, device=local)
+        cnt = 65536
+        buf = torch.randint(0, 1 << 62, (cnt, n), dtype=torch.int64, device=dev, generator=torch.Generator(
+            device=dev).manual_seed(args.seed))
+        buf = (buf % Q).view(torch.uint64)
+
+        def fn():
+            ctx.negacyclic(buf, 0, False, _lib.LAYOUT_BITREV)
+            ctx.negacyclic(buf, 0, True, _lib.LAYOUT_BITREV)
+        total = _time_steps(fn, args.steps, args.warmup, flush, stream)
+        value = world * 2 * cnt * args.steps / (total / 1e3)
+        unit, workload = "transforms/s", "config2: 65536 x n=2048 negacyclic NTT then INTT (device layout), 60-bit q"
+        nat = _time_steps(lambda: (ctx.negacyclic(buf, 0, False, 0), ctx.negacyclic(buf, 0, True, 0)), 5, 2, flush,
+                          stream)
+        extra["natural_layout_transforms_per_s"] = 2 * cnt * 5 / (nat / 1e3)
+        imad_peak = lib.ensei_gpu_imad_peak(local)
+        alg = (ntt_fwd(n) + ntt_inv(n)) * C_Q * cnt
+        extra["imad_frac"] = alg * args.steps / (total / 1e3) / imad_peak
+        extra["hbm_GB_s"] = 2 * cnt * n * 16 * args.steps / (total / 1e3) / 1e9
+        if rank == 0 and not args.no_cpu_baseline:
+            import oracle as O
+            sample = np.random.default_rng(0).integers(0, Q, size=(4096, n), dtype=np.uint64)
+            secs = O.ref().ref_bench_negacyclic(Q, n, sample.reshape(-1), 4096, cores)
+            cpu = {"value": 2 * 4096 / secs, "unit": unit, "cores": cores, "kind": "reference",
+                   "sample": "4096 polys x REF NegacyclicPlan forward+inverse over all host threads"}
+    elif args.config == 3:
+        imgs = args.images if args.images != 8 else 64
+        ctx = ops.Context(n=2048, device=local)
+        sched = [GP.Conv(3, 3, True, 3, 64), GP.Act(0), GP.Conv(3, 3, True, 64, 64), GP.Act(0, True),
+                 GP.Conv(3, 3, True, 64, 128), GP.Act(0), GP.Conv(3, 3, True, 128, 128), GP.Act(0, True),
+                 GP.Conv(3, 3, True, 128, 128), GP.Act(0), GP.Conv(1, 1, True, 128, 128), GP.Act(0),
+                 GP.Conv(1, 1, True, 128, 16)]
+        wshapes = [(64, 3, 3, 3), (64, 64, 3, 3), (128, 64, 3, 3), (128, 128, 3, 3), (128, 128, 3, 3),
+                   (128, 128, 1, 1), (16, 128, 1, 1)]
+        ws = [torch.randint(-128, 128, s_, dtype=torch.int32, generator=gen) for s_ in wshapes]
+        sess = GP.Session(ctx, sched, 32, 32, ws)
+        x = torch.randint(0, 256, (imgs, 3, 32, 32), dtype=torch.uint8, generator=gen).to(dev)
+        _, key = ops.secret_sample(ctx, args.seed)
+        rands = [ops.Randomness(seed=args.seed, layer=li, image_base=rank * imgs) for li in range(len(sched))]
+        fn = lambda: sess.run(key, x, lambda li: rands[li])  # noqa: E731
+        total = _time_steps(fn, args.steps, args.warmup, flush, stream)
+        value = world * imgs * args.steps / (total / 1e3)
+        unit = "images/s"
+        workload = (f"config3: {imgs} images x 3x32x32 through 7 conv layers (3->64, 64->64 @32; 64->128, "
+                    "128->128 @16; 128->128 3x3, 128->128 1x1, 128->16 1x1 @8), ReLU, 2x2 max-pool after L2/L4")
+        if rank == 0 and not args.no_cpu_baseline:
+            segs = [([[0, 3, 3, 1, 3, 64, 0], [1, 0, 0, 0, 0, 0, 0], [0, 3, 3, 1, 64, 64, 0]], 32, 3),
+                    ([[0, 3, 3, 1, 64, 128, 0], [1, 0, 0, 0, 0, 0, 0], [0, 3, 3, 1, 128, 128, 0]], 16, 64),
+                    ([[0, 3, 3, 1, 128, 128, 0], [1, 0, 0, 0, 0, 0, 0], [0, 1, 1, 1, 128, 128, 0],
+                      [1, 0, 0, 0, 0, 0, 0], [0, 1, 1, 1, 128, 16, 0]], 8, 128)]
+            per_img = 0.0
+            for rows, Hs, cin in segs:
+                _, _, online = _ref_sessions(rows, Hs, Hs, cin, 1, 1, args.seed)
+                per_img += online
+            cpu = {"value": min(cores // 2, 1e9) / per_img, "unit": unit, "cores": cores, "kind": "reference",
+                   "sample": "1 image through REF run_inproc of the 3 reference-expressible segments "
+                             f"(online {per_img:.2f}s), scaled to {cores // 2} concurrent sessions"}
+    elif args.config == 4:
+        imgs = args.images if args.images != 8 else 1024
+        chunk = 128
+        ctx = ops.Context(n=8192, q=ops.RNS_DEFAULT, device=local)
+        L = ops.LayerOps(ctx, ops.ConvSpec(32, 32, 3, 3, True, 64, 128))
+        x = torch.randint(0, 256, (imgs, 64, 32, 32), dtype=torch.uint8, generator=gen).to(dev)
+        w = torch.randint(-128, 128, (128, 64, 3, 3), dtype=torch.int32, generator=gen).to(dev)
+        _, key = ops.secret_sample(ctx, args.seed)
+        we = L.prepare_weights(w)
+        ws = L.workspace(chunk)
+        out = torch.empty((imgs, 128, 32, 32), dtype=torch.int32, device=dev)
+
+        def fn():
+            for i in range(0, imgs, chunk):
+                L.forward(key, we, x[i:i + chunk], ops.Randomness(seed=args.seed, image_base=rank * imgs + i),
+                          ws=ws, out=out[i:i + chunk])
+        total = _time_steps(fn, args.steps, args.warmup, None, stream)
+        value = world * imgs * args.steps / (total / 1e3)
+        unit = "images/s"
+        workload = (f"config4: {imgs} images/GPU x 64x32x32, 64->128 3x3 Same, n=8192, RNS q = 3 x 60-bit primes, "
+                    f"p=638977, {chunk}-image chunks")
+        if rank == 0 and not args.no_cpu_baseline:
+            q4 = 576460803525083137
+            v, wall, online = _ref_sessions([[0, 3, 3, 1, 64, 128, 0]], 32, 32, 64, 1, 1, args.seed, n=8192, q=q4)
+            cpu = {"value": (cores // 2) / online, "unit": unit, "cores": cores, "kind": "reference",
+                   "sample": f"1 image, REF single-prime n=8192 64->128 session (online {online:.2f}s; RNS proxy per "
+                             f"SURVEY 8(d)), scaled to {cores // 2} concurrent sessions"}
+    else:
+        raise SystemExit(f"unknown config {args.config}")
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic, seeded",
+                "config": {"workload": workload, "config_index": args.config}, "cpu_baseline": cpu, **extra}
+        print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

@@ -90,4 +90,5 @@ struct ensei_gpu_ctx {
   // with Alice's encryption on an auxiliary stream (capturable in CUDA graphs)
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+
 };

@@ -103,35 +103,49 @@ struct PhiSrc {
 
 // ------------------------------------------------------------ tile -> ring
 
+// Barrier over the NT threads of thread group g (literal ids keep ptxas' barrier
+// budget at 3, so several CTAs fit per SM).
+struct GroupBar {
+  int g, count;
+  EG_DEV void sync() const {
+    if (g == 0) asm volatile("bar.sync 1, %0;" ::"r"(count) : "memory");
+    else asm volatile("bar.sync 2, %0;" ::"r"(count) : "memory");
+  }
+};
+
 enum TileMode { TILE_ENC = 0, TILE_HOMREC = 1, TILE_WEIGHTS = 2 };
 
-// One CTA per (image, channel) [ENC / HOMREC] or (out, in) filter [WEIGHTS].
-// NT = n/8 threads.  Shared: tile S (u32), ring buffer over p (u32), ring buffer
-// over q (u64), noise cache for R > 1.
-template <int LOGN, int LOGH, int LOGW, int R, int MODE, int TM, bool INJ, int IN_T>
-__global__ void __launch_bounds__((1 << LOGN) >> kLogE)
+// One CTA per (image, channel) [ENC / HOMREC] or (out, in) filter [WEIGHTS], G thread
+// groups of NT = n/8 threads; group g handles blocks b = g, g+G, ... concurrently.
+// Shared: tile S (u32) + per group a ring buffer over p (u32), one over q (u64) and the
+// block's Enc noise (int8, drawn two per Philox call).  The q-side epilogue (a^ draw,
+// a^ t^, stores) runs as a separate coalesced loop after the NTT, not inside its
+// unrolled last pass, to keep register pressure low.
+template <int LOGN, int LOGH, int LOGW, int R, int TM, bool INJ, int IN_T, int G>
+__global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE))
     tile_enc_kernel(LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride,
                     const void* __restrict__ in, uint64_t* __restrict__ out) {
   constexpr int N = 1 << LOGN, NT = N >> kLogE;
   constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
+  constexpr size_t GROUP_BYTES = (size_t)N * 8 + ssize<uint32_t>(N) * 4 + N;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);
+  const int g = threadIdx.x / NT, tid = threadIdx.x % NT;
+  uint8_t* gbase = smem_raw + (((size_t)Lh * LS * 4 + 127) & ~(size_t)127) + g * ((GROUP_BYTES + 127) & ~(size_t)127);
+  uint64_t* qbuf = reinterpret_cast<uint64_t*>(gbase);
   uint32_t* pbuf = reinterpret_cast<uint32_t*>(qbuf + N);
-  uint32_t* S = pbuf + ssize<uint32_t>(N);
-  int8_t* ecache = reinterpret_cast<int8_t*>(S + Lh * LS);
-  const int tid = threadIdx.x;
-  const CtaBar bar;
+  int8_t* ebuf = reinterpret_cast<int8_t*>(pbuf + ssize<uint32_t>(N));
+  const GroupBar bar{g, NT};
   const Field32 pf = a.pp.f;
   const uint32_t p = pf.q;
 
-  // which tile: ENC/HOMREC -> (img, c); WEIGHTS -> (o, c)
   const int item = blockIdx.x;
   const int ch = item % a.cin;
   const int img = item / a.cin;  // image (or output channel for WEIGHTS)
   const int th = TM == TILE_WEIGHTS ? a.fh : a.H, tw = TM == TILE_WEIGHTS ? a.fw : a.W;
 
   // 1. pad into the tile (REF pad_image / pad_residues, ntt.cpp:155-185)
-  for (int i = tid; i < Lh * Lw; i += NT) {
+  for (int i = threadIdx.x; i < Lh * Lw; i += blockDim.x) {
     const int r = i >> LOGW, c = i & (Lw - 1);
     uint32_t v = 0;
     if (r < th && c < tw) {
@@ -154,7 +168,24 @@ __global__ void __launch_bounds__((1 << LOGN) >> kLogE)
 
   const uint64_t* kimg = key + (size_t)(TM == TILE_ENC ? img : 0) * key_stride;
   const int gimg = a.image_base + img;
-  for (int b = 0; b < a.B; ++b) {
+  for (int b = g; b < a.B; b += G) {
+    if constexpr (TM == TILE_ENC) {  // Enc noise e0 for this block, two CBD draws per call
+      const size_t nb = (((size_t)img * a.cin + ch) * a.B + b) * N;
+      const uint32_t mask = a.cbd_k >= 32 ? 0xFFFFFFFFu : ((1u << a.cbd_k) - 1u);
+      for (int i2 = tid; i2 < N / 2; i2 += NT) {
+        int32_t e0, e1;
+        if constexpr (INJ) {
+          e0 = a.inj_noise[nb + 2 * i2];
+          e1 = a.inj_noise[nb + 2 * i2 + 1];
+        } else {
+          const Philox4 rr = philox(a.alice_key, stream_id(PURPOSE_NOISE, a.layer, gimg, ch, b), i2);
+          e0 = cbd_from(rr.x, rr.y, mask);
+          e1 = cbd_from(rr.z, rr.w, mask);
+        }
+        ebuf[2 * i2] = (int8_t)e0;
+        ebuf[2 * i2 + 1] = (int8_t)e1;
+      }
+    }
     // 3. encode_slots: INTT_p of the block's slots (gathered from the tile)
     {
       auto src = [&](int j) { return gather_slot<LOGN, LOGH, LOGW>(S, b, j, a.G); };
@@ -162,14 +193,7 @@ __global__ void __launch_bounds__((1 << LOGN) >> kLogE)
       auto dst = [&](int i, uint32_t v) { dst_raw(i, Bfly<Field32, 0>::fin_gs(pf, v)); };
       ntt_inverse<Field32, uint32_t, LOGN, kLogE, 0, false, false>(pf, a.twp_inv, pbuf, tid, src, dst, bar);
     }
-    if constexpr (TM == TILE_ENC && R > 1) {  // noise drawn once, shared by all primes
-      for (int i = tid; i < N; i += NT) {
-        int32_t e = INJ ? a.inj_noise[(((size_t)img * a.cin + ch) * a.B + b) * N + i]
-                        : draw_cbd(a.alice_key, stream_id(PURPOSE_NOISE, a.layer, gimg, ch, b), i, a.cbd_k);
-        ecache[i] = (int8_t)e;
-      }
-    }
-    __syncthreads();
+    bar.sync();
 #pragma unroll 1
     for (int r = 0; r < R; ++r) {
       const PrimeConst pc = a.pc[r];
@@ -182,87 +206,107 @@ __global__ void __launch_bounds__((1 << LOGN) >> kLogE)
         } else {
           uint64_t x = delta_mul<R>(pc, m);
           if constexpr (TM == TILE_ENC) {
-            int32_t e;
-            if constexpr (R > 1) e = ecache[i];
-            else
-              e = INJ ? a.inj_noise[(((size_t)img * a.cin + ch) * a.B + b) * N + i]
-                      : draw_cbd(a.alice_key, stream_id(PURPOSE_NOISE, a.layer, gimg, ch, b), i, a.cbd_k);
-            x += signed_mod(e, f.q);
+            x += signed_mod(ebuf[i], f.q);
             if (x >= f.q) x -= f.q;
           }
           return x;
         }
       };
-      // 5. NTT_q + epilogue at the device (bit-reversed) position j
-      uint64_t* obase;
-      if constexpr (TM == TILE_WEIGHTS) obase = out + ((((size_t)img * a.cin + ch) * a.B + b) * R + r) * N;
-      else obase = out + (((size_t)img * a.cin + ch) * a.B + b) * ct_words<R>(N);
-      auto dst = [&](int j, uint64_t v) {
-        const uint64_t x = Bfly<Field64, 0>::fin_ct(f, v, pc.cred);
-        if constexpr (TM == TILE_WEIGHTS) {
-          obase[j] = ((x >> 30) << 32) | (x & 0x3FFFFFFFull);  // 30-bit limbs for the MAC
-        } else if constexpr (TM == TILE_HOMREC) {
-          uint64_t* c1 = obase + (size_t)(R + r) * N;
-          uint64_t y = c1[j] + x;
-          c1[j] = y >= f.q ? y - f.q : y;
-        } else {
-          const int k = brev(j, LOGN);  // natural slot index keys the a^ stream
-          const uint64_t ah = INJ ? a.inj_ahat[((((size_t)img * a.cin + ch) * a.B + b) * R + r) * N + k]
-                                  : draw_uniform_q(a.alice_key,
-                                                   stream_id(PURPOSE_AHAT, a.layer, gimg, ch, b | (r << 12)), k, f.q);
-          const uint64_t t = kimg[(size_t)(2 * r) * N + j], tp = kimg[(size_t)(2 * r + 1) * N + j];
-          uint64_t c1 = Bfly<Field64, 0>::fin_gs(f, f.mul_shoup_approx(ah, t, tp)) + x;
-          c1 = c1 >= f.q ? c1 - f.q : c1;
-          obase[(size_t)r * N + j] = ah ? f.q - ah : 0;
-          obase[(size_t)(R + r) * N + j] = c1;
-        }
-      };
-      ntt_forward<Field64, uint64_t, LOGN, kLogE, 0, false, false>(f, a.twq_fwd[r], qbuf, tid, src, dst, bar,
+      // 5. NTT_q in place (lazy values stay in qbuf), then the epilogue
+      SmemRW<uint64_t> qs{qbuf};
+      ntt_forward<Field64, uint64_t, LOGN, kLogE, 0, false, false>(f, a.twq_fwd[r], qbuf, tid, src, qs, bar,
                                                                    pc.cred);
-      __syncthreads();
+      bar.sync();
+      if constexpr (TM == TILE_WEIGHTS) {
+        uint64_t* ob = out + ((((size_t)img * a.cin + ch) * a.B + b) * R + r) * N;
+        for (int j = tid; j < N; j += NT) {
+          const uint64_t x = Bfly<Field64, 0>::fin_ct(f, qbuf[sidx<uint64_t>(j)], pc.cred);
+          ob[j] = ((x >> 30) << 32) | (x & 0x3FFFFFFFull);  // 30-bit limbs for the MAC
+        }
+      } else {
+        uint64_t* ob = out + (((size_t)img * a.cin + ch) * a.B + b) * ct_words<R>(N);
+        uint64_t* c0 = ob + (size_t)r * N;
+        uint64_t* c1 = ob + (size_t)(R + r) * N;
+        const uint64_t* tk = kimg + (size_t)(2 * r) * N;
+        const uint64_t* tkp = tk + N;
+        const uint64_t sid = stream_id(PURPOSE_AHAT, a.layer, gimg, ch, b | (r << 12));
+        const size_t ab = ((((size_t)img * a.cin + ch) * a.B + b) * R + r) * N;
+        for (int j = tid; j < N; j += NT) {
+          const uint64_t x = Bfly<Field64, 0>::fin_ct(f, qbuf[sidx<uint64_t>(j)], pc.cred);
+          if constexpr (TM == TILE_HOMREC) {
+            const uint64_t y = c1[j] + x;
+            c1[j] = y >= f.q ? y - f.q : y;
+          } else {
+            const int k = brev(j, LOGN);  // natural slot index keys the a^ stream
+            const uint64_t ah = INJ ? a.inj_ahat[ab + k] : draw_uniform_q(a.alice_key, sid, k, f.q);
+            uint64_t v1 = Bfly<Field64, 0>::fin_gs(f, f.mul_shoup_approx(ah, tk[j], tkp[j])) + x;
+            c0[j] = ah ? f.q - ah : 0;
+            c1[j] = v1 >= f.q ? v1 - f.q : v1;
+          }
+        }
+      }
+      bar.sync();
     }
   }
 }
 
-template <int LOGN, int LOGH, int LOGW, int R>
+template <int LOGN, int LOGH, int LOGW, int G>
 constexpr size_t tile_enc_smem() {
-  return (size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4 + (size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4 +
-         (R > 1 ? (1 << LOGN) : 0);
+  return (((size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4 + 127) & ~(size_t)127) +
+         G * ((((size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4 + (1 << LOGN)) + 127) & ~(size_t)127);
 }
 
 // ------------------------------------------------------- HomShare + Bob share
 
-// One CTA per (image, out channel).  M[img][o][b][r][n] = NTT_q(Delta*INTT_p(p - s_B))
-// (device layout) and bob_share[img][o][oh][ow] = crop(IDFT2D(merge(s_B))).
-template <int LOGN, int LOGH, int LOGW, int R, bool INJ>
-__global__ void __launch_bounds__((1 << LOGN) >> kLogE)
+// One CTA per (image, out channel), G groups over the blocks.  s_B for every block is
+// drawn once (two per Philox call) into shared memory; masks
+// NTT_q(Delta*INTT_p(p - s_B)) go to the c1 words of the output ciphertext (device
+// layout) and Bob's share = crop(IDFT2D(merge(s_B))).
+template <int LOGN, int LOGH, int LOGW, int R, bool INJ, int G>
+__global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE))
     share_kernel(LayerArgs a, uint64_t* __restrict__ mask, uint32_t* __restrict__ bob_share) {
   constexpr int N = 1 << LOGN, NT = N >> kLogE;
   constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
+  constexpr size_t GROUP_BYTES = (size_t)N * 8 + ssize<uint32_t>(N) * 4;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* sbuf = S + (((size_t)Lh * LS + 31) & ~(size_t)31);  // [B][N] shares
+  const int g = threadIdx.x / NT, tid = threadIdx.x % NT;
+  uint8_t* gbase = reinterpret_cast<uint8_t*>(sbuf + (size_t)a.B * N) + g * ((GROUP_BYTES + 127) & ~(size_t)127);
+  uint64_t* qbuf = reinterpret_cast<uint64_t*>(gbase);
   uint32_t* pbuf = reinterpret_cast<uint32_t*>(qbuf + N);
-  uint32_t* S = pbuf + ssize<uint32_t>(N);
-  const int tid = threadIdx.x;
-  const CtaBar bar;
+  const GroupBar bar{g, NT};
   const Field32 pf = a.pp.f;
   const uint32_t p = pf.q;
   const int item = blockIdx.x;  // img * cout + o
   const int o = item % a.cout, img = item / a.cout;
   const int gimg = a.image_base + img;
-  auto share = [&](int b, int l) -> uint32_t {  // s_B at natural slot l of block b
-    return INJ ? a.inj_share[(((size_t)img * a.cout + o) * a.B + b) * N + l]
-               : draw_uniform_p(a.bob_key, stream_id(PURPOSE_SHARE, a.layer, gimg, o, b), l, p);
-  };
-  for (int b = 0; b < a.B; ++b) {
+  // 1. s_B for all blocks (natural slot order)
+  for (int e = threadIdx.x; e < a.B * N / 2; e += blockDim.x) {
+    const int b = e / (N / 2), i2 = e % (N / 2);
+    uint32_t s0, s1;
+    if constexpr (INJ) {
+      const size_t base = (((size_t)img * a.cout + o) * a.B + b) * N + 2 * i2;
+      s0 = a.inj_share[base];
+      s1 = a.inj_share[base + 1];
+    } else {
+      const Philox4 rr = philox(a.bob_key, stream_id(PURPOSE_SHARE, a.layer, gimg, o, b), i2);
+      s0 = uniform_p_from(rr.x, rr.y, p);
+      s1 = uniform_p_from(rr.z, rr.w, p);
+    }
+    sbuf[b * N + 2 * i2] = s0;
+    sbuf[b * N + 2 * i2 + 1] = s1;
+  }
+  __syncthreads();
+  for (int b = g; b < a.B; b += G) {
     auto src = [&](int j) {
-      const uint32_t s = share(b, brev(j, LOGN));
+      const uint32_t s = sbuf[b * N + brev(j, LOGN)];
       return s == 0 ? 0u : p - s;  // (p_A - s_B) mod p_E  (REF hss.cpp:33-35)
     };
     SmemRW<uint32_t> dst_raw{pbuf};
     auto dst = [&](int i, uint32_t v) { dst_raw(i, Bfly<Field32, 0>::fin_gs(pf, v)); };
     ntt_inverse<Field32, uint32_t, LOGN, kLogE, 0, false, false>(pf, a.twp_inv, pbuf, tid, src, dst, bar);
-    __syncthreads();
+    bar.sync();
 #pragma unroll 1
     for (int r = 0; r < R; ++r) {
       const PrimeConst pc = a.pc[r];
@@ -270,25 +314,31 @@ __global__ void __launch_bounds__((1 << LOGN) >> kLogE)
       auto qsrc = [&](int i) { return delta_mul<R>(pc, pbuf[sidx<uint32_t>(i)]); };
       // mask lands where c1 of the output ciphertext (img, o, b) lives
       uint64_t* mo = mask + ((size_t)item * a.B + b) * ct_words<R>(N) + (size_t)(R + r) * N;
-      GlobalOut64Fwd out{mo, f, pc.cred};
-      ntt_forward<Field64, uint64_t, LOGN, kLogE, 0, false, false>(f, a.twq_fwd[r], qbuf, tid, qsrc, out, bar,
+      GlobalOut64Fwd outw{mo, f, pc.cred};
+      ntt_forward<Field64, uint64_t, LOGN, kLogE, 0, false, false>(f, a.twq_fwd[r], qbuf, tid, qsrc, outw, bar,
                                                                    pc.cred);
-      __syncthreads();
+      bar.sync();
     }
   }
-  // Bob's share: IDFT2D of the merged s_B grid, cropped (REF protocol.cpp:593-602)
-  for (int i = tid; i < Lh * Lw; i += NT) {
+  __syncthreads();
+  // 2. Bob's share: IDFT2D of the merged s_B grid, cropped (REF protocol.cpp:593-602)
+  for (int i = threadIdx.x; i < Lh * Lw; i += blockDim.x) {
     const int r = i >> LOGW, c = i & (Lw - 1);
-    const int flat = i;  // natural grid position (r, c)
-    S[brev(r, LOGH) * LS + brev(c, LOGW)] = share(flat >> LOGN, flat & (N - 1));
+    S[brev(r, LOGH) * LS + brev(c, LOGW)] = sbuf[i];  // natural grid position i = r*Lw + c
   }
   __syncthreads();
   tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, S, LS);
   uint32_t* bs = bob_share + (size_t)item * a.oh * a.ow;
-  for (int i = tid; i < a.oh * a.ow; i += NT) {
+  for (int i = threadIdx.x; i < a.oh * a.ow; i += blockDim.x) {
     const int r = i / a.ow, c = i % a.ow;
     bs[i] = S[(r + a.r0) * LS + c + a.c0];
   }
+}
+
+template <int LOGN, int LOGH, int LOGW, int G>
+constexpr size_t share_smem(int B) {
+  return (((size_t)(1 << LOGH) * ((1 << LOGW) + 1) + 31) & ~(size_t)31) * 4 + (size_t)B * (1 << LOGN) * 4 +
+         G * ((((size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4) + 127) & ~(size_t)127);
 }
 
 // RNS decryption (config 4): per prime r, phi_r = INTT_{q_r}(c0 t^ + c1), y_r = phi_r *
@@ -376,30 +426,27 @@ constexpr size_t dec_rns_smem() {
   return (size_t)(1 << LOGN) * 16 + ssize<uint32_t>(1 << LOGN) * 4 + (size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4;
 }
 
-template <int LOGN, int LOGH, int LOGW>
-constexpr size_t share_smem() {
-  return (size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4 + (size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4;
-}
 
 // ---------------------------------------------------------------- decrypt
 
-
-
-// One CTA per (image, out channel): phi = c0 t^ + c1 -> INTT_q -> round(p phi / q)
-// -> decode (NTT_p) -> scatter into the tile -> IDFT2D -> crop (-> + Bob's share).
-template <int LOGN, int LOGH, int LOGW>
-__global__ void __launch_bounds__((1 << LOGN) >> kLogE)
+// One CTA per (image, out channel), G groups over the blocks: phi = c0 t^ + c1 ->
+// INTT_q -> round(p phi / q) -> decode (NTT_p) -> scatter into the tile; then all
+// threads: IDFT2D -> crop (-> + Bob's share).
+template <int LOGN, int LOGH, int LOGW, int G>
+__global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE))
     dec_kernel(LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride,
                const uint64_t* __restrict__ ct, uint32_t* __restrict__ alice_share,
                const uint32_t* __restrict__ bob_share, uint32_t* __restrict__ outp) {
   constexpr int N = 1 << LOGN, NT = N >> kLogE;
   constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
+  constexpr size_t GROUP_BYTES = (size_t)N * 8 + ssize<uint32_t>(N) * 4;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);
+  const int g = threadIdx.x / NT, tid = threadIdx.x % NT;
+  uint8_t* gbase = smem_raw + (((size_t)Lh * LS * 4 + 127) & ~(size_t)127) + g * ((GROUP_BYTES + 127) & ~(size_t)127);
+  uint64_t* qbuf = reinterpret_cast<uint64_t*>(gbase);
   uint32_t* pbuf = reinterpret_cast<uint32_t*>(qbuf + N);
-  uint32_t* S = pbuf + ssize<uint32_t>(N);
-  const int tid = threadIdx.x;
-  const CtaBar bar;
+  const GroupBar bar{g, NT};
   const Field32 pf = a.pp.f;
   const uint32_t p = pf.q;
   const int item = blockIdx.x;  // img * cout + o
@@ -408,10 +455,8 @@ __global__ void __launch_bounds__((1 << LOGN) >> kLogE)
   const PrimeConst pc = a.pc[0];
   const Field64 f = pc.f;
   const uint64_t cp = pc.cp, h = f.q >> 1;  // floor(p 2^64 / q), floor(q / 2)
-  for (int i = tid; i < Lh * LS; i += NT) S[i] = 0;
-  for (int b = 0; b < a.B; ++b) {
+  for (int b = g; b < a.B; b += G) {
     const uint64_t* cb = ct + ((size_t)item * a.B + b) * ct_words<1>(N);
-    // 1. phi (device layout) -> INTT_q -> natural coefficients
     PhiSrc src{cb, cb + N, kimg, kimg + N, f};
     auto dst = [&](int i, uint64_t v) {
       const uint64_t phi = Bfly<Field64, 0>::fin_gs(f, v);
@@ -427,17 +472,18 @@ __global__ void __launch_bounds__((1 << LOGN) >> kLogE)
       pbuf[sidx<uint32_t>(i)] = (uint32_t)(Q % p);
     };
     ntt_inverse<Field64, uint64_t, LOGN, kLogE, 0, false, false>(f, a.twq_inv[0], qbuf, tid, src, dst, bar);
-    __syncthreads();
-    // 2. decode_slots (NTT_p) -> scatter into the bit-reversed tile
+    bar.sync();
+    // decode_slots (NTT_p) -> scatter into the bit-reversed tile
     SmemRW<uint32_t> psrc{pbuf};
     auto pdst = [&](int j, uint32_t v) { scatter_slot<LOGN, LOGH, LOGW>(S, b, j, a.G, reduce_lazy(pf, v, a.pp.cred)); };
     ntt_forward<Field32, uint32_t, LOGN, kLogE, 0, false, false>(pf, a.twp_fwd, pbuf, tid, psrc, pdst, bar);
-    __syncthreads();
+    bar.sync();
   }
-  // 3. IDFT2D + crop (+ recombine with Bob's share)
+  __syncthreads();
+  // IDFT2D + crop (+ recombine with Bob's share)
   tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, S, LS);
   const size_t base = (size_t)item * a.oh * a.ow;
-  for (int i = tid; i < a.oh * a.ow; i += NT) {
+  for (int i = threadIdx.x; i < a.oh * a.ow; i += blockDim.x) {
     const int r = i / a.ow, c = i % a.ow;
     const uint32_t s = S[(r + a.r0) * LS + c + a.c0];
     if (alice_share) alice_share[base + i] = s;
@@ -446,6 +492,12 @@ __global__ void __launch_bounds__((1 << LOGN) >> kLogE)
       outp[base + i] = y >= p ? y - p : y;
     }
   }
+}
+
+template <int LOGN, int LOGH, int LOGW, int G>
+constexpr size_t dec_smem() {
+  return (((size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4 + 127) & ~(size_t)127) +
+         G * ((((size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4) + 127) & ~(size_t)127);
 }
 
 // ------------------------------------------------------------ ElementMult

@@ -267,29 +267,57 @@ Workspace carve(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g, 
   return w;
 }
 
+// One sub-batch of the layer on stream `st` (aux stream `aux` for Bob's masks):
+// share || (Enc [+ HomRec]) -> ElementMult -> Dec (+ recombine).
+void layer_chain(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const Geo& g, const uint64_t* key, uint32_t ks,
+                 const uint64_t* w_eval, const uint8_t* in, int in_dtype, const uint32_t* bob_prev, uint32_t i0,
+                 uint32_t imgs, const ensei_randomness* rand, const Workspace& w, uint32_t* alice_share,
+                 uint32_t* bob_share, uint32_t* out, cudaStream_t st, cudaStream_t aux, cudaEvent_t fork,
+                 cudaEvent_t join) {
+  ensei_randomness rc{};
+  if (rand) {
+    rc = *rand;
+    rc.image_base += i0;
+    const size_t nwords = (size_t)ctx->n, B = g.B;
+    if (rc.d_noise) rc.d_noise += (size_t)i0 * desc->cin * B * nwords;
+    if (rc.d_a_hat) rc.d_a_hat += (size_t)i0 * desc->cin * B * ctx->R * nwords;
+    if (rc.d_share) rc.d_share += (size_t)i0 * desc->cout * B * nwords;
+  }
+  LayerRun r = make_run(ctx, desc, g, imgs, rand ? &rc : nullptr, st);
+  const size_t ctw = (size_t)g.B * 2 * ctx->R * ctx->n;
+  const size_t tin = (size_t)desc->cin * desc->H * desc->W, tout = (size_t)desc->cout * g.oh * g.ow;
+  uint64_t* ct_in = w.ct_in + (size_t)i0 * desc->cin * ctw;
+  uint64_t* ct_out = w.ct_out + (size_t)i0 * desc->cout * ctw;
+  uint32_t* bs = (bob_share ? bob_share : w.bob) + (size_t)i0 * tout;
+  const void* x = in + (size_t)i0 * tin * (in_dtype == ENSEI_IN_U8 ? 1 : 4);
+  const uint64_t* k = key + (size_t)i0 * ks;
+  const bool inj = injected(rand);
+  // Bob's HomShare masks depend only on his randomness: fork them onto the aux stream
+  // so they overlap Alice's encryption; join before the ElementMult consumes them.
+  EG_CUDA(cudaEventRecord(fork, st));
+  EG_CUDA(cudaStreamWaitEvent(aux, fork, 0));
+  LayerRun ra = r;
+  ra.st = aux;
+  share(ra, inj, ct_out, bs, (int)(imgs * desc->cout));
+  EG_CUDA(cudaEventRecord(join, aux));
+  tile(r, TILE_ENC, inj, in_dtype, k, ks, x, ct_in, (int)(imgs * desc->cin));
+  if (bob_prev)
+    tile(r, TILE_HOMREC, false, ENSEI_IN_U32, k, 0, bob_prev + (size_t)i0 * tin, ct_in, (int)(imgs * desc->cin));
+  EG_CUDA(cudaStreamWaitEvent(st, join, 0));
+  mac(r, ct_in, w_eval, ct_out);
+  dec(r, k, ks, ct_out, alice_share ? alice_share + (size_t)i0 * tout : nullptr, bs, out ? out + (size_t)i0 * tout : nullptr,
+      (int)(imgs * desc->cout));
+}
+
 void conv_layer(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uint64_t* key, uint32_t ks,
                 const uint64_t* w_eval, const void* in, int in_dtype, const uint32_t* bob_prev, uint32_t imgs,
                 const ensei_randomness* rand, void* ws, uint32_t* alice_share, uint32_t* bob_share, uint32_t* out,
                 void* stream) {
   require(ctx && desc && key && w_eval && in && ws, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
   Geo g = geometry(ctx, desc);
-  LayerRun r = make_run(ctx, desc, g, imgs, rand, stream);
   Workspace w = carve(ctx, desc, g, imgs, ws, in_dtype, false);
-  uint32_t* bs = bob_share ? bob_share : w.bob;
-  const bool inj = injected(rand);
-  // Bob's HomShare masks depend only on his randomness: fork them onto the aux stream
-  // so they overlap Alice's encryption; join before the ElementMult consumes them.
-  EG_CUDA(cudaEventRecord(ctx->ev_fork, r.st));
-  EG_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
-  LayerRun ra = r;
-  ra.st = ctx->aux;
-  share(ra, inj, w.ct_out, bs, (int)(imgs * desc->cout));
-  EG_CUDA(cudaEventRecord(ctx->ev_join, ctx->aux));
-  tile(r, TILE_ENC, inj, in_dtype, key, ks, in, w.ct_in, (int)(imgs * desc->cin));
-  if (bob_prev) tile(r, TILE_HOMREC, false, ENSEI_IN_U32, key, 0, bob_prev, w.ct_in, (int)(imgs * desc->cin));
-  EG_CUDA(cudaStreamWaitEvent(r.st, ctx->ev_join, 0));
-  mac(r, w.ct_in, w_eval, w.ct_out);
-  dec(r, key, ks, w.ct_out, alice_share, bs, out, (int)(imgs * desc->cout));
+  layer_chain(ctx, desc, g, key, ks, w_eval, static_cast<const uint8_t*>(in), in_dtype, bob_prev, 0, imgs, rand, w,
+              alice_share, bob_share, out, (cudaStream_t)stream, ctx->aux, ctx->ev_fork, ctx->ev_join);
 }
 
 }  // namespace

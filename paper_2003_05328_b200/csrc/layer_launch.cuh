@@ -20,14 +20,28 @@ static void set_smem(K k, size_t smem) {
 }
 
 // ---- tile -> ring (Enc / HomRec / weights / secret) ----
+// thread groups per CTA: the blocks of one tile run concurrently when they fit
+template <int LOGN>
+constexpr bool kTwoGroups = LOGN <= 12;
+inline int groups_for(int logn, int B) { return (B >= 2 && logn <= 12) ? 2 : 1; }
+
+template <int LOGN, int LOGL, int R, int TM, bool INJ, int IN_T, int G>
+static void enc_go_g(const LayerRun& r, const uint64_t* key, uint32_t key_stride, const void* in, uint64_t* out,
+                     int items) {
+  auto k = tile_enc_kernel<LOGN, LOGL, LOGL, R, TM, INJ, IN_T, G>;
+  constexpr size_t smem = tile_enc_smem<LOGN, LOGL, LOGL, G>();
+  set_smem(k, smem);
+  k<<<items, G * ((1 << LOGN) >> kLogE), smem, r.st>>>(r.a, key, key_stride, in, out);
+  check_launch("tile_enc_kernel");
+}
+
 template <int LOGN, int LOGL, int R, int TM, bool INJ, int IN_T>
 static void enc_go(const LayerRun& r, const uint64_t* key, uint32_t key_stride, const void* in, uint64_t* out,
                    int items) {
-  auto k = tile_enc_kernel<LOGN, LOGL, LOGL, R, 0, TM, INJ, IN_T>;
-  constexpr size_t smem = tile_enc_smem<LOGN, LOGL, LOGL, R>();
-  set_smem(k, smem);
-  k<<<items, (1 << LOGN) >> kLogE, smem, r.st>>>(r.a, key, key_stride, in, out);
-  check_launch("tile_enc_kernel");
+  if constexpr (kTwoGroups<LOGN>) {
+    if (groups_for(LOGN, r.a.B) == 2) return enc_go_g<LOGN, LOGL, R, TM, INJ, IN_T, 2>(r, key, key_stride, in, out, items);
+  }
+  enc_go_g<LOGN, LOGL, R, TM, INJ, IN_T, 1>(r, key, key_stride, in, out, items);
 }
 
 template <int LOGN, int LOGL, int R>
@@ -73,13 +87,21 @@ void launch_tile(const LayerRun& r, int tm, bool inj, int in_t, const uint64_t* 
 }
 
 // ---- HomShare masks + Bob share ----
+template <int LOGN, int LOGL, int R, bool INJ, int G>
+static void share_go_g(const LayerRun& r, uint64_t* ct_out, uint32_t* bob_share, int items) {
+  auto k = share_kernel<LOGN, LOGL, LOGL, R, INJ, G>;
+  const size_t smem = share_smem<LOGN, LOGL, LOGL, G>(r.a.B);
+  set_smem(k, smem);
+  k<<<items, G * ((1 << LOGN) >> kLogE), smem, r.st>>>(r.a, ct_out, bob_share);
+  check_launch("share_kernel");
+}
+
 template <int LOGN, int LOGL, int R, bool INJ>
 static void share_go(const LayerRun& r, uint64_t* ct_out, uint32_t* bob_share, int items) {
-  auto k = share_kernel<LOGN, LOGL, LOGL, R, INJ>;
-  constexpr size_t smem = share_smem<LOGN, LOGL, LOGL>();
-  set_smem(k, smem);
-  k<<<items, (1 << LOGN) >> kLogE, smem, r.st>>>(r.a, ct_out, bob_share);
-  check_launch("share_kernel");
+  if constexpr (kTwoGroups<LOGN>) {
+    if (groups_for(LOGN, r.a.B) == 2) return share_go_g<LOGN, LOGL, R, INJ, 2>(r, ct_out, bob_share, items);
+  }
+  share_go_g<LOGN, LOGL, R, INJ, 1>(r, ct_out, bob_share, items);
 }
 
 template <int LOGN, int R, bool INJ>
@@ -111,14 +133,23 @@ void launch_share(const LayerRun& r, bool inj, uint64_t* mask, uint32_t* bob_sha
 }
 
 // ---- decrypt ----
+template <int LOGN, int LOGL, int G>
+static void dec_go_g(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint64_t* ct, uint32_t* alice,
+                     const uint32_t* bob, uint32_t* out, int items) {
+  auto k = dec_kernel<LOGN, LOGL, LOGL, G>;
+  constexpr size_t smem = dec_smem<LOGN, LOGL, LOGL, G>();
+  set_smem(k, smem);
+  k<<<items, G * ((1 << LOGN) >> kLogE), smem, r.st>>>(r.a, key, ks, ct, alice, bob, out);
+  check_launch("dec_kernel");
+}
+
 template <int LOGN, int LOGL>
 static void dec_go(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint64_t* ct, uint32_t* alice,
                    const uint32_t* bob, uint32_t* out, int items) {
-  auto k = dec_kernel<LOGN, LOGL, LOGL>;
-  constexpr size_t smem = share_smem<LOGN, LOGL, LOGL>();
-  set_smem(k, smem);
-  k<<<items, (1 << LOGN) >> kLogE, smem, r.st>>>(r.a, key, ks, ct, alice, bob, out);
-  check_launch("dec_kernel");
+  if constexpr (kTwoGroups<LOGN>) {
+    if (groups_for(LOGN, r.a.B) == 2) return dec_go_g<LOGN, LOGL, 2>(r, key, ks, ct, alice, bob, out, items);
+  }
+  dec_go_g<LOGN, LOGL, 1>(r, key, ks, ct, alice, bob, out, items);
 }
 
 template <int LOGN, int LOGL>

@@ -86,6 +86,7 @@ struct ensei_gpu_ctx {
   ensei_gpu::DeviceTables tab;
   void* table_mem = nullptr;
   bool approx_ok = true;  // every q_i < 2^61: approximate-quotient butterflies (MODE 0)
+  bool kara_ok = true;    // every q_i within the Karatsuba MAC's headroom (layer.cuh)
   // fork/join helpers: Bob's input-independent HomShare work runs concurrently
   // with Alice's encryption on an auxiliary stream (capturable in CUDA graphs)
   cudaStream_t aux = nullptr;

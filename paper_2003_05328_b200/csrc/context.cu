@@ -110,6 +110,13 @@ static void ctx_create(int device, uint32_t n, const uint64_t* qs, uint32_t R, u
     require(q > (1ull << 32), ENSEI_ERR_UNSUPPORTED, "q_i below 2^32 not supported on this path");
     c->q[i] = q;
     if (q >= (1ull << 61)) c->approx_ok = false;
+    {  // Karatsuba MAC headroom: 2^50 + 6 Pm, 2^50 + 60 P2 < 2^64, 1008 (q-1)^2 < 2^128
+      typedef unsigned __int128 u128;
+      const u128 x1 = (q - 1) >> 30, xs = (u128)((1ull << 30) - 1) + x1;
+      const u128 lim64 = ((u128)1 << 64) - ((u128)1 << 50);
+      const u128 qq = (u128)(q - 1) * (q - 1);
+      if (6 * xs * xs >= lim64 || 60 * x1 * x1 >= lim64 || qq > (~(u128)0) / 1008) c->kara_ok = false;
+    }
   }
   // Delta = floor(Q / p) mod q_i.  Q == 1 mod p for every chain here (each q_i == 1 mod p),
   // so Delta = (Q - 1) / p exactly; computed per prime without big integers:
@@ -234,25 +241,25 @@ int ensei_gpu_permute(ensei_gpu_ctx* ctx, int to_natural, uint64_t* d_data, size
 }  // extern "C"
 
 // ------------------------------------------------------------ IMAD peak probe
-// Chains of mad.wide.u32 with 64-bit accumulation (the instruction the modular
-// kernels are built from); 8 independent chains per thread, full occupancy.
+// Issue-slot rate of the integer multiply (fmaheavy) pipe: dependent mad.lo.u32 chains
+// whose operands change every iteration (8 independent chains per thread, full
+// occupancy).  IMAD.WIDE / IMAD.HI occupy two of these slots each (measured ~31/clk/SM
+// vs ~61/clk/SM for IMAD), which is why the roofline counts c_* in IMAD slots.
 namespace ensei_gpu {
 __global__ void imad_probe_kernel(uint64_t* sink, uint32_t seed, int iters) {
   uint32_t a[8], b[8];
-  uint64_t d[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     a[i] = seed * (threadIdx.x + i) + 1;
     b[i] = a[i] ^ 0x9e3779b9u;
-    d[i] = a[i];
   }
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(d[i]) : "r"(a[i]), "r"(b[i]));
+    for (int i = 0; i < 8; ++i) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[i]) : "r"(b[i]), "r"(b[(i + 1) & 7]));
   }
   uint64_t s = 0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) s ^= d[i];
+  for (int i = 0; i < 8; ++i) s ^= a[i];
   if (s == 0x12345) sink[0] = s;
 }
 }  // namespace ensei_gpu

@@ -677,6 +677,257 @@ __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN))
   }
 }
 
+// Karatsuba ElementMult (the production MAC).  Same per-slot product as mac_kernel,
+// three IMAD.WIDE per MAC instead of four: with x = x1 2^30 + x0, y = y1 2^30 + y0,
+//   x y = P0 + 2^30 (Pm - P0 - P2) + 2^60 P2,  P0 = x0 y0, P2 = x1 y1,
+//   Pm = (x0 + x1)(y0 + y1)  (< 2.27 2^60 since x1, y1 < 2^29.01 for q < 2^59.01).
+// Each of S0 = sum P0, Sm = sum Pm, S2 = sum P2 is kept exactly as H 2^50 + L (L a
+// 64-bit accumulator, H a 32-bit word: H < K 2^11.2): products accumulate into L, and
+// L's bits >= 50 move into H every 6 / 12 / 60 channels for Sm / S0 / S2 (headroom
+// after a fold: 2^50 + 6 Pm, 12 P0, 60 P2 all < 2^64).  The epilogue rebuilds the
+// exact u128 sum T = sum x y (< 2^128 while K <= 1008) and reduces it once; longer K
+// flushes T mod q into the output word every 1008 channels and accumulates there.
+// Measured on B200: IMAD.WIDE costs 4 fmaheavy cycles per warp, IADD3 2 ALU cycles, the
+// pipes co-issue, so the fmaheavy floor drops from 20 to 12 cycles per MAC.
+//
+// Work: tiles = (S-slot group) x (MT-row tile) x (NT-col tile), rows/cols fastest so
+// concurrently running CTAs share the slot group's ct and weight words in L2.  The grid
+// is persistent; each CTA walks its tiles' K chunks as one flat sequence with a
+// STAGES-deep cp.async ring, so the next tile's loads overlap this tile's epilogue
+// (small-K layers are otherwise pure load latency).
+constexpr int kKaraMaxK = 1008;
+constexpr uint64_t kKaraLowBits = 50;  // S = H 2^50 + L: L < 2^50 after a fold, H < K 2^11.2
+
+template <int S, int MT, int NT, int KT, int STAGES>
+constexpr size_t mac_kara_smem() {
+  return (size_t)STAGES * KT * (MT + NT) * S * sizeof(uint64_t);
+}
+
+template <int R, int S, int MT, int NT, int KT, int TM, int TN, int STAGES>
+__global__ void __launch_bounds__(S*(MT / TM) * (NT / TN), (512 / (S * (MT / TM) * (NT / TN))) > 1 ? 512 / (S * (MT / TM) * (NT / TN)) : 1)
+    mac_kara_kernel(LayerArgs a, int logn, const uint64_t* __restrict__ ct, const uint64_t* __restrict__ w,
+                    int has_mask, uint64_t* __restrict__ out) {
+  static_assert(KT % 6 == 0 && kKaraMaxK % KT == 0, "K chunk: whole fold blocks dividing 1008");
+  constexpr int NTH = S * (MT / TM) * (NT / TN);
+  constexpr int SV = S / 2;
+  constexpr int STAGE_WORDS = KT * (MT + NT) * S;
+  extern __shared__ __align__(16) uint64_t smac[];
+  const int n = 1 << logn;
+  const int rows = 2 * a.num_images, cols = a.cout, K = a.cin;
+  const int nrt = (rows + MT - 1) / MT, nct = (cols + NT - 1) / NT;
+  const int tiles_per_group = nrt * nct;
+  const int ntiles = (a.B * R * n / S) * tiles_per_group;
+  const int nchunks = (K + KT - 1) / KT;
+  const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int nsteps = my_tiles * nchunks;
+  const int tid = threadIdx.x;
+  const int sl = tid % S, tm = (tid / S) % (MT / TM), tn = tid / (S * (MT / TM));
+  const size_t ctw = (size_t)ct_words<R>(n);
+  const size_t chan_stride = (size_t)a.B * ctw;
+  const size_t w_chan = (size_t)a.B * R * n;
+  constexpr uint64_t M30 = (1ull << 30) - 1;
+  constexpr uint64_t kLowMask = (1ull << kKaraLowBits) - 1;
+
+  struct Tile {
+    int b, r, k0, row0, col0;
+    const uint64_t* a_base;  // ct words of (row0, channel 0, block b, prime r, slot k0)
+    const uint64_t* w_base;  // weight words of (col0, channel 0, pair bp, slot k0)
+  };
+  // tile decode (runtime divisions): once per tile on each side, not per K chunk
+  auto tile_of = [&](int j) {
+    const int t = blockIdx.x + j * gridDim.x;
+    const int g = t / tiles_per_group, rem = t % tiles_per_group;
+    const int s0 = g * S, bp = s0 >> logn;
+    Tile tl;
+    tl.b = bp / R;
+    tl.r = bp % R;
+    tl.k0 = s0 & (n - 1);
+    tl.row0 = (rem % nrt) * MT;
+    tl.col0 = (rem / nrt) * NT;
+    tl.a_base = ct + (size_t)(tl.row0 >> 1) * a.cin * chan_stride + (size_t)tl.b * ctw + (size_t)tl.r * n + tl.k0;
+    tl.w_base = w + (size_t)tl.col0 * a.cin * w_chan + (size_t)bp * n + tl.k0;
+    return tl;
+  };
+  Tile ld = tile_of(0);
+  int ld_j = 0, ld_c = 0;  // next (tile, chunk) to load
+  auto load_step = [&](int step) {
+    if (step < nsteps) {
+      const int kc = ld_c * KT;
+      uint64_t* Ab = smac + (step % STAGES) * STAGE_WORDS;
+      uint64_t* Bb = Ab + KT * MT * S;
+      const uint64_t* as = ld.a_base + (size_t)kc * chan_stride;
+      const uint64_t* ws = ld.w_base + (size_t)kc * w_chan;
+#pragma unroll
+      for (int e = tid; e < KT * MT * SV; e += NTH) {
+        const int v = e % SV, row = (e / SV) % MT, kk = e / (SV * MT);
+        uint64_t* dst = Ab + (kk * MT + row) * S + 2 * v;
+        if (ld.row0 + row < rows && kc + kk < K) {
+          cp_async16(dst, as + (size_t)((row >> 1) * a.cin + kk) * chan_stride + (row & 1) * R * n + 2 * v);
+        } else {
+          dst[0] = 0;
+          dst[1] = 0;
+        }
+      }
+#pragma unroll
+      for (int e = tid; e < KT * NT * SV; e += NTH) {
+        const int v = e % SV, col = (e / SV) % NT, kk = e / (SV * NT);
+        uint64_t* dst = Bb + (kk * NT + col) * S + 2 * v;
+        if (ld.col0 + col < cols && kc + kk < K) {
+          cp_async16(dst, ws + (size_t)(col * a.cin + kk) * w_chan + 2 * v);
+        } else {
+          dst[0] = 0;
+          dst[1] = 0;
+        }
+      }
+      if (++ld_c == nchunks) {
+        ld_c = 0;
+        if (++ld_j < my_tiles) ld = tile_of(ld_j);
+      }
+    }
+    cp_async_commit();  // empty groups keep the wait_group count uniform
+  };
+
+  uint64_t L0[TM][TN], Lm[TM][TN], L2[TM][TN];
+  uint32_t H0[TM][TN], Hm[TM][TN], H2[TM][TN];
+  auto zero_acc = [&]() {
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        L0[i][j] = Lm[i][j] = L2[i][j] = 0;
+        H0[i][j] = Hm[i][j] = H2[i][j] = 0;
+      }
+  };
+  // exact T = sum x y (u128) from the split sums, reduced mod q
+  auto reduce_T = [&](const Field64& f, const PrimeConst& pc, int i, int j) -> uint64_t {
+    typedef unsigned __int128 u128;
+    const u128 s0 = ((u128)H0[i][j] << kKaraLowBits) + L0[i][j];
+    const u128 sm = ((u128)Hm[i][j] << kKaraLowBits) + Lm[i][j];
+    const u128 s2 = ((u128)H2[i][j] << kKaraLowBits) + L2[i][j];
+    const u128 t = s0 + ((sm - s0 - s2) << 30) + (s2 << 60);
+    const uint64_t lo = (uint64_t)t, hi = (uint64_t)(t >> 64);
+    uint64_t x = Bfly<Field64, 0>::corr(f, lo, pc.cred);
+    if (hi) x += f.mul_shoup_approx(hi, pc.c64, pc.c64p);
+    return Bfly<Field64, 0>::fin_ct(f, x, pc.cred);
+  };
+
+#pragma unroll 1
+  for (int st = 0; st < STAGES - 1; ++st) load_step(st);
+  zero_acc();
+  int blocks = 0, kdone = 0, flushes = 0;
+  Tile cm = tile_of(0);
+  int cm_j = 0, cm_c = 0;  // (tile, chunk) being computed
+#pragma unroll 1
+  for (int step = 0; step < nsteps; ++step) {
+    load_step(step + STAGES - 1);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(STAGES - 1) : "memory");
+    __syncthreads();
+    const uint64_t* Ab = smac + (step % STAGES) * STAGE_WORDS;
+    const uint64_t* Bb = Ab + KT * MT * S;
+    const int kmax = min(KT, K - cm_c * KT);
+    // one channel pair: six products per output into the three split sums
+    auto pair = [&](int kk) {
+      uint32_t xl[2][TM], xh[2][TM], xs[2][TM], yl[2][TN], yh[2][TN], ys[2][TN];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          const uint64_t v = Ab[((kk + u) * MT + tm * TM + i) * S + sl];
+          xl[u][i] = (uint32_t)(v & M30);
+          xh[u][i] = (uint32_t)(v >> 30);
+          xs[u][i] = xl[u][i] + xh[u][i];
+        }
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          const uint64_t v = Bb[((kk + u) * NT + tn * TN + j) * S + sl];
+          yl[u][j] = lo32(v);
+          yh[u][j] = hi32(v);
+          ys[u][j] = yl[u][j] + yh[u][j];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+          asm("mad.wide.u32 %0, %3, %4, %0;\n\t"
+              "mad.wide.u32 %1, %5, %6, %1;\n\t"
+              "mad.wide.u32 %2, %7, %8, %2;\n\t"
+              "mad.wide.u32 %0, %9, %10, %0;\n\t"
+              "mad.wide.u32 %1, %11, %12, %1;\n\t"
+              "mad.wide.u32 %2, %13, %14, %2;"
+              : "+l"(L0[i][j]), "+l"(Lm[i][j]), "+l"(L2[i][j])
+              : "r"(xl[0][i]), "r"(yl[0][j]), "r"(xs[0][i]), "r"(ys[0][j]), "r"(xh[0][i]), "r"(yh[0][j]),
+                "r"(xl[1][i]), "r"(yl[1][j]), "r"(xs[1][i]), "r"(ys[1][j]), "r"(xh[1][i]), "r"(yh[1][j]));
+    };
+    int kk = 0;
+#pragma unroll 1
+    for (; kk + 6 <= kmax; kk += 6) {  // Sm headroom: 7 products -> fold every 6 channels
+#pragma unroll
+      for (int u = 0; u < 3; ++u) pair(kk + 2 * u);
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          Hm[i][j] += (uint32_t)(Lm[i][j] >> kKaraLowBits);
+          Lm[i][j] &= kLowMask;
+        }
+      if (++blocks % 2 == 0) {  // S0: 15 products
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) {
+            H0[i][j] += (uint32_t)(L0[i][j] >> kKaraLowBits);
+            L0[i][j] &= kLowMask;
+          }
+        if (blocks == 10) {  // S2: 63 products
+          blocks = 0;
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) {
+              H2[i][j] += (uint32_t)(L2[i][j] >> kKaraLowBits);
+              L2[i][j] &= kLowMask;
+            }
+        }
+      }
+    }
+#pragma unroll 1
+    for (; kk < kmax; kk += 2) pair(kk);  // last chunk only: < 3 pairs, zero-filled odd tail
+    kdone += KT;
+    const bool last = cm_c == nchunks - 1;
+    if (last || kdone == kKaraMaxK) {  // flush: out = (mask | previous partial) + T mod q
+      const PrimeConst pc = a.pc[cm.r];
+      const Field64 f = pc.f;
+      const int k = cm.k0 + sl;
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const int gr = cm.row0 + tm * TM + i;
+        const int img = gr >> 1, comp = gr & 1;
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          const int go = cm.col0 + tn * TN + j;
+          if (gr >= rows || go >= cols) continue;
+          uint64_t x = reduce_T(f, pc, i, j);
+          const size_t oa = ((size_t)img * a.cout + go) * chan_stride + (size_t)cm.b * ctw +
+                            (size_t)(comp * R + cm.r) * n + k;
+          if (flushes > 0 || (comp == 1 && has_mask)) x = f.add(x, out[oa]);  // HomShare mask / partial
+          out[oa] = x;
+        }
+      }
+      zero_acc();
+      blocks = 0;
+      kdone = 0;
+      flushes = last ? 0 : flushes + 1;
+    }
+    if (++cm_c == nchunks) {
+      cm_c = 0;
+      if (++cm_j < my_tiles) cm = tile_of(cm_j);
+    }
+    __syncthreads();  // this stage's buffer is refilled STAGES-1 steps later
+  }
+  cp_async_wait_all();
+}
+
 template <int S, int MT, int NT, int KT>
 constexpr size_t mac_smem() {
   return (size_t)2 * KT * (MT + NT) * S * sizeof(uint64_t);

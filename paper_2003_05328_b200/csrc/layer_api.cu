@@ -2,6 +2,7 @@
 // keys, weight preparation, Alice Enc, Bob eval, Alice Dec, recombination and the
 // whole-layer / host-buffer entry points.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -175,18 +176,55 @@ void mac_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* 
   check_launch("mac_kernel");
 }
 
-void mac(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
-  if (r.a.num_images == 0) return;
+template <int R, int S, int MT, int NT, int KT, int TM, int TN, int STAGES>
+void mac_kara_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
+  const int n = (int)r.ctx->n, rows = 2 * r.a.num_images, cols = r.a.cout;
+  auto k = mac_kara_kernel<R, S, MT, NT, KT, TM, TN, STAGES>;
+  constexpr size_t smem = mac_kara_smem<S, MT, NT, KT, STAGES>();
+  set_smem(k, smem);
+  const long tiles = (long)(r.a.B * R * n / S) * ((rows + MT - 1) / MT) * ((cols + NT - 1) / NT);
+  static int per_sm = -1;  // per instantiation; the launch config never changes
+  if (per_sm < 0) EG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, S * (MT / TM) * (NT / TN), smem));
+  const long grid = std::min<long>(tiles, (long)std::max(per_sm, 1) * r.ctx->sm_count);
+  k<<<(unsigned)grid, S * (MT / TM) * (NT / TN), smem, r.st>>>(r.a, (int)r.ctx->logn, ct, w, 1, out);
+  check_launch("mac_kara_kernel");
+}
+
+static int mac_variant() {
+  static int v = [] {
+    const char* e = getenv("ENSEI_MAC_VARIANT");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
+template <int R>
+void mac_r(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
   const int rows = 2 * r.a.num_images, cols = r.a.cout;
   const bool small = rows <= 16 && cols <= 16;
-  if (r.R == 1) {
-    if (small) return mac_go<1, 16, 16, 16, 16, 2, 4>(r, ct, w, out);
-    return mac_go<1, 8, 32, 32, 16, 4, 4>(r, ct, w, out);
+  switch (r.ctx->kara_ok ? mac_variant() : 0) {
+    case 0:  // four-product kernel (kept for A/B)
+      if (small) return mac_go<R, 16, 16, 16, 16, 2, 4>(r, ct, w, out);
+      return mac_go<R, 8, 32, 32, 16, 4, 4>(r, ct, w, out);
+    case 2:
+      if (small) return mac_kara_go<R, 4, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
+      return mac_kara_go<R, 8, 32, 16, 12, 2, 4, 3>(r, ct, w, out);
+    case 3:
+      if (small) return mac_kara_go<R, 8, 16, 16, 24, 2, 4, 2>(r, ct, w, out);
+      return mac_kara_go<R, 4, 32, 32, 12, 2, 4, 3>(r, ct, w, out);
+    case 4:
+      if (small) return mac_kara_go<R, 2, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
+      return mac_kara_go<R, 4, 32, 32, 12, 2, 4, 3>(r, ct, w, out);
+    default:
+      if (small) return mac_kara_go<R, 8, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
+      return mac_kara_go<R, 8, 32, 16, 24, 2, 4, 2>(r, ct, w, out);
   }
-  if (r.R == 3) {
-    if (small) return mac_go<3, 16, 16, 16, 16, 2, 4>(r, ct, w, out);
-    return mac_go<3, 8, 32, 32, 16, 4, 4>(r, ct, w, out);
-  }
+}
+
+void mac(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
+  if (r.a.num_images == 0) return;
+  if (r.R == 1) return mac_r<1>(r, ct, w, out);
+  if (r.R == 3) return mac_r<3>(r, ct, w, out);
   fail(ENSEI_ERR_UNSUPPORTED, "ElementMult: unsupported prime count");
 }
 

@@ -1,0 +1,79 @@
+"""ElementMult + channel accumulation (REF protocol.cpp:537-607 conv branch: mul_plain
+then add_ct over input channels, ringbfv.cpp:233-263) through ensei_gpu_bob_mac, against
+exact Python-integer sums, on the shapes that exercise the kernel's edges: odd K, K
+spanning several K-chunks and fold blocks, partial row / column tiles, the small-tile
+path, both prime counts, and K past the exact-u128 limit (1008 channels).
+
+ct_out's c1 words carry the HomShare mask on entry (the kernel adds, does not overwrite),
+so the test pre-fills them with random residues."""
+import numpy as np
+import pytest
+import torch
+
+from gpu_util import Q, RNS, dev, to_np, u64
+
+pytestmark = pytest.mark.gpu
+
+M30 = (1 << 30) - 1
+
+
+@pytest.fixture(scope="module")
+def ops():
+    from paper_2003_05328_b200 import ops as _ops
+    return _ops
+
+
+def _pack(v):
+    """Prepared-weight word: (v >> 30) << 32 | (v & (2^30 - 1)) (ensei_gpu.h prepare_weights)."""
+    return ((v >> np.uint64(30)) << np.uint64(32)) | (v & np.uint64(M30))
+
+
+# (n, images, cin, cout, primes): small-tile path (rows, cols <= 16), large tiles with partial
+# row/col tiles, odd K, K = one fold block + tail, K across chunks, K > 1008 (residue carry)
+CASES = [
+    (2048, 1, 1, 1, 1),
+    (2048, 3, 5, 7, 1),
+    (2048, 8, 16, 16, 1),
+    (2048, 3, 13, 36, 1),
+    (2048, 3, 40, 36, 1),
+    (2048, 9, 64, 20, 1),
+    (2048, 2, 1030, 3, 1),
+    (8192, 2, 7, 3, 3),
+    (8192, 20, 30, 17, 3),
+]
+
+
+@pytest.mark.parametrize("n,images,cin,cout,R", CASES)
+def test_bob_mac_exact(ops, n, images, cin, cout, R):
+    q = (Q,) if R == 1 else RNS
+    ctx = ops.Context(n=n, q=q)
+    L = ops.LayerOps(ctx, ops.ConvSpec(16, 16, 3, 3, True, cin, cout))
+    B = L.B
+    rng = np.random.default_rng(n + 7 * cin + cout)
+    qs = np.array(q, dtype=np.uint64).reshape(1, 1, 1, 1, R, 1)
+    ct = (rng.integers(0, 2**63, size=(images, cin, B, 2, R, n), dtype=np.uint64) % qs)
+    w = (rng.integers(0, 2**63, size=(cout, cin, B, R, n), dtype=np.uint64) %
+         np.array(q, dtype=np.uint64).reshape(1, 1, 1, R, 1))
+    mask = (rng.integers(0, 2**63, size=(images, cout, B, R, n), dtype=np.uint64) %
+            np.array(q, dtype=np.uint64).reshape(1, 1, 1, R, 1))
+    out = np.zeros((images, cout, B, 2, R, n), dtype=np.uint64)
+    out[:, :, :, 1] = mask
+    d_out = u64(out)
+    L.bob_mac(u64(ct), u64(_pack(w)), d_out)
+    torch.cuda.synchronize()
+    got = to_np(d_out).view(np.uint64)
+    # exact check on a slot sample (all rows and columns; Python integers)
+    slots = sorted(set([0, 1, n // 2, n - 1] + list(rng.integers(0, n, size=12))))
+    for b in range(B):
+        for r in range(R):
+            qr = q[r]
+            for k in slots:
+                xs = ct[:, :, b, :, r, k].astype(object)        # [img][cin][comp]
+                ys = w[:, :, b, r, k].astype(object)            # [cout][cin]
+                for img in range(images):
+                    for comp in range(2):
+                        acc = (xs[img, :, comp][None, :] * ys).sum(axis=1)
+                        if comp == 1:
+                            acc = acc + mask[img, :, b, r, k].astype(object)
+                        exp = np.array([int(v) % qr for v in acc], dtype=np.uint64)
+                        assert (got[img, :, b, comp, r, k] == exp).all(), (b, r, k, img, comp)

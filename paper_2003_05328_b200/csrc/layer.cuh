@@ -708,6 +708,7 @@ __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN), (512 / (S * (MT / TM)
     mac_kara_kernel(LayerArgs a, int logn, const uint64_t* __restrict__ ct, const uint64_t* __restrict__ w,
                     int has_mask, uint64_t* __restrict__ out) {
   static_assert(KT % 6 == 0 && kKaraMaxK % KT == 0, "K chunk: whole fold blocks dividing 1008");
+  static_assert(TM == 2, "thread rows = the two components of one image");
   constexpr int NTH = S * (MT / TM) * (NT / TN);
   constexpr int SV = S / 2;
   constexpr int STAGE_WORDS = KT * (MT + NT) * S;
@@ -750,30 +751,37 @@ __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN), (512 / (S * (MT / TM)
   };
   Tile ld = tile_of(0);
   int ld_j = 0, ld_c = 0;  // next (tile, chunk) to load
+  // Each thread's 16-byte copies: fixed (row, v) and (col, v), channel kk0 + m*KSTEP, so a
+  // step's addresses are one base pointer plus a per-channel stride (no index decoding).
+  constexpr int A_KSTEP = NTH / (SV * MT), B_KSTEP = NTH / (SV * NT);
+  static_assert(NTH % (SV * MT) == 0 && NTH % (SV * NT) == 0, "copy mapping");
+  const int a_v = tid % SV, a_row = (tid / SV) % MT, a_kk0 = tid / (SV * MT);
+  const int b_col = (tid / SV) % NT, b_kk0 = tid / (SV * NT);
+  const size_t a_off = (size_t)((a_row >> 1) * a.cin + a_kk0) * chan_stride + (a_row & 1) * R * n + 2 * a_v;
+  const size_t b_off = (size_t)(b_col * a.cin + b_kk0) * w_chan + 2 * a_v;
   auto load_step = [&](int step) {
     if (step < nsteps) {
       const int kc = ld_c * KT;
       uint64_t* Ab = smac + (step % STAGES) * STAGE_WORDS;
       uint64_t* Bb = Ab + KT * MT * S;
-      const uint64_t* as = ld.a_base + (size_t)kc * chan_stride;
-      const uint64_t* ws = ld.w_base + (size_t)kc * w_chan;
+      const bool a_ok = ld.row0 + a_row < rows, b_ok = ld.col0 + b_col < cols;
+      const uint64_t* as = ld.a_base + (size_t)kc * chan_stride + a_off;
+      const uint64_t* ws = ld.w_base + (size_t)kc * w_chan + b_off;
 #pragma unroll
-      for (int e = tid; e < KT * MT * SV; e += NTH) {
-        const int v = e % SV, row = (e / SV) % MT, kk = e / (SV * MT);
-        uint64_t* dst = Ab + (kk * MT + row) * S + 2 * v;
-        if (ld.row0 + row < rows && kc + kk < K) {
-          cp_async16(dst, as + (size_t)((row >> 1) * a.cin + kk) * chan_stride + (row & 1) * R * n + 2 * v);
+      for (int kk = a_kk0, m = 0; m < KT / A_KSTEP; ++m, kk += A_KSTEP) {
+        uint64_t* dst = Ab + (kk * MT + a_row) * S + 2 * a_v;
+        if (a_ok && kc + kk < K) {
+          cp_async16(dst, as + (size_t)m * A_KSTEP * chan_stride);
         } else {
           dst[0] = 0;
           dst[1] = 0;
         }
       }
 #pragma unroll
-      for (int e = tid; e < KT * NT * SV; e += NTH) {
-        const int v = e % SV, col = (e / SV) % NT, kk = e / (SV * NT);
-        uint64_t* dst = Bb + (kk * NT + col) * S + 2 * v;
-        if (ld.col0 + col < cols && kc + kk < K) {
-          cp_async16(dst, ws + (size_t)(col * a.cin + kk) * w_chan + 2 * v);
+      for (int kk = b_kk0, m = 0; m < KT / B_KSTEP; ++m, kk += B_KSTEP) {
+        uint64_t* dst = Bb + (kk * NT + b_col) * S + 2 * a_v;
+        if (b_ok && kc + kk < K) {
+          cp_async16(dst, ws + (size_t)m * B_KSTEP * w_chan);
         } else {
           dst[0] = 0;
           dst[1] = 0;
@@ -898,22 +906,25 @@ __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN), (512 / (S * (MT / TM)
     if (last || kdone == kKaraMaxK) {  // flush: out = (mask | previous partial) + T mod q
       const PrimeConst pc = a.pc[cm.r];
       const Field64 f = pc.f;
-      const int k = cm.k0 + sl;
+      // rows row0 + 2 tm + i: image row0/2 + tm, component i (TM == 2)
+      const int img = (cm.row0 >> 1) + tm, go0 = cm.col0 + tn * TN;
+      uint64_t* ob = out + ((size_t)img * a.cout + go0) * chan_stride + (size_t)cm.b * ctw + (size_t)cm.r * n +
+                     cm.k0 + sl;
+      const bool row_ok = 2 * img < rows;
+      uint64_t prev[TM][TN];
 #pragma unroll
-      for (int i = 0; i < TM; ++i) {
-        const int gr = cm.row0 + tm * TM + i;
-        const int img = gr >> 1, comp = gr & 1;
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) {
-          const int go = cm.col0 + tn * TN + j;
-          if (gr >= rows || go >= cols) continue;
-          uint64_t x = reduce_T(f, pc, i, j);
-          const size_t oa = ((size_t)img * a.cout + go) * chan_stride + (size_t)cm.b * ctw +
-                            (size_t)(comp * R + cm.r) * n + k;
-          if (flushes > 0 || (comp == 1 && has_mask)) x = f.add(x, out[oa]);  // HomShare mask / partial
-          out[oa] = x;
+          prev[i][j] = 0;
+          if (row_ok && go0 + j < cols && (flushes > 0 || (i == 1 && has_mask)))
+            prev[i][j] = ob[(size_t)j * chan_stride + (size_t)i * R * n];
         }
-      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+          if (row_ok && go0 + j < cols) ob[(size_t)j * chan_stride + (size_t)i * R * n] = f.add(reduce_T(f, pc, i, j), prev[i][j]);
       zero_acc();
       blocks = 0;
       kdone = 0;

@@ -211,10 +211,10 @@ void mac_r(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* o
       return mac_kara_go<R, 8, 32, 16, 12, 2, 4, 3>(r, ct, w, out);
     case 3:
       if (small) return mac_kara_go<R, 8, 16, 16, 24, 2, 4, 2>(r, ct, w, out);
-      return mac_kara_go<R, 4, 32, 32, 12, 2, 4, 3>(r, ct, w, out);
+      return mac_kara_go<R, 8, 32, 16, 24, 2, 4, 3>(r, ct, w, out);
     case 4:
-      if (small) return mac_kara_go<R, 2, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
-      return mac_kara_go<R, 4, 32, 32, 12, 2, 4, 3>(r, ct, w, out);
+      if (small) return mac_kara_go<R, 4, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
+      return mac_kara_go<R, 16, 16, 16, 24, 2, 4, 2>(r, ct, w, out);
     default:
       if (small) return mac_kara_go<R, 8, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
       return mac_kara_go<R, 8, 32, 16, 24, 2, 4, 2>(r, ct, w, out);

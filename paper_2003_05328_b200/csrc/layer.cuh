@@ -23,6 +23,10 @@
 namespace ensei_gpu {
 
 constexpr int kLogE = 3;  // elements per thread in the ring transforms (E = 8)
+// Tile kernels are latency-bound (one CTA per tile, serial fused stages): capping them
+// at 64 registers lets two CTAs share an SM, so Bob's HomShare CTAs co-reside with
+// Alice's Enc CTAs and each hides the other's latency.
+constexpr int tile_min_blocks(int threads) { return threads >= 1024 ? 1 : 1024 / threads; }
 
 struct LayerArgs {
   // geometry (REF ConvGeometry / LayerPlan)
@@ -122,7 +126,7 @@ enum TileMode { TILE_ENC = 0, TILE_HOMREC = 1, TILE_WEIGHTS = 2 };
 // a^ t^, stores) runs as a separate coalesced loop after the NTT, not inside its
 // unrolled last pass, to keep register pressure low.
 template <int LOGN, int LOGH, int LOGW, int R, int TM, bool INJ, int IN_T, int G>
-__global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE))
+__global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE), tile_min_blocks(G*((1 << LOGN) >> kLogE)))
     tile_enc_kernel(LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride,
                     const void* __restrict__ in, uint64_t* __restrict__ out) {
   constexpr int N = 1 << LOGN, NT = N >> kLogE;
@@ -263,7 +267,7 @@ constexpr size_t tile_enc_smem() {
 // NTT_q(Delta*INTT_p(p - s_B)) go to the c1 words of the output ciphertext (device
 // layout) and Bob's share = crop(IDFT2D(merge(s_B))).
 template <int LOGN, int LOGH, int LOGW, int R, bool INJ, int G>
-__global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE))
+__global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE), tile_min_blocks(G*((1 << LOGN) >> kLogE)))
     share_kernel(LayerArgs a, uint64_t* __restrict__ mask, uint32_t* __restrict__ bob_share) {
   constexpr int N = 1 << LOGN, NT = N >> kLogE;
   constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
@@ -706,7 +710,7 @@ constexpr size_t mac_kara_smem() {
 template <int R, int S, int MT, int NT, int KT, int TM, int TN, int STAGES>
 __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN), (512 / (S * (MT / TM) * (NT / TN))) > 1 ? 512 / (S * (MT / TM) * (NT / TN)) : 1)
     mac_kara_kernel(LayerArgs a, int logn, const uint64_t* __restrict__ ct, const uint64_t* __restrict__ w,
-                    int has_mask, uint64_t* __restrict__ out) {
+                    int has_mask, uint64_t* __restrict__ out, uint32_t zero) {
   static_assert(KT % 6 == 0 && kKaraMaxK % KT == 0, "K chunk: whole fold blocks dividing 1008");
   static_assert(TM == 2, "thread rows = the two components of one image");
   constexpr int NTH = S * (MT / TM) * (NT / TN);
@@ -843,14 +847,14 @@ __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN), (512 / (S * (MT / TM)
           const uint64_t v = Ab[((kk + u) * MT + tm * TM + i) * S + sl];
           xl[u][i] = (uint32_t)(v & M30);
           xh[u][i] = (uint32_t)(v >> 30);
-          xs[u][i] = xl[u][i] + xh[u][i];
+          xs[u][i] = xl[u][i] + xh[u][i] + zero;  // 3-input: an ALU IADD3, not an fmaheavy IMAD
         }
 #pragma unroll
         for (int j = 0; j < TN; ++j) {
           const uint64_t v = Bb[((kk + u) * NT + tn * TN + j) * S + sl];
           yl[u][j] = lo32(v);
           yh[u][j] = hi32(v);
-          ys[u][j] = yl[u][j] + yh[u][j];
+          ys[u][j] = yl[u][j] + yh[u][j] + zero;
         }
       }
 #pragma unroll

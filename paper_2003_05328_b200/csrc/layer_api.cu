@@ -186,7 +186,7 @@ void mac_kara_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint6
   static int per_sm = -1;  // per instantiation; the launch config never changes
   if (per_sm < 0) EG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, S * (MT / TM) * (NT / TN), smem));
   const long grid = std::min<long>(tiles, (long)std::max(per_sm, 1) * r.ctx->sm_count);
-  k<<<(unsigned)grid, S * (MT / TM) * (NT / TN), smem, r.st>>>(r.a, (int)r.ctx->logn, ct, w, 1, out);
+  k<<<(unsigned)grid, S * (MT / TM) * (NT / TN), smem, r.st>>>(r.a, (int)r.ctx->logn, ct, w, 1, out, 0u);
   check_launch("mac_kara_kernel");
 }
 

@@ -38,7 +38,11 @@ sys.path.insert(0, ROOT)
 P = 638977
 Q = 576460803525083137
 METRIC = "oblivious NTT-domain conv/sec (1/2/4/8 B200); NTT modmul/s vs roofline"
-C_Q, C_MAC, C_P = 10, 8, 3  # IMAD per modmul class (min(survey, SASS))
+# IMAD-pipe slots per modmul class, min(SURVEY.md 8(d) constant, our SASS) with
+# IMAD.WIDE = 2 slots (measured: 4 fmaheavy cycles per warp vs 2 for IMAD):
+#   q-Shoup 5 WIDE + 4 IMAD = 14 > 10 -> 10;  Karatsuba MAC 3 WIDE = 6 < 8 -> 6;
+#   p-Shoup 1 WIDE + 2 IMAD = 4 > 3 -> 3.
+C_Q, C_MAC, C_P = 10, 6, 3
 
 
 def parse():
@@ -328,7 +332,7 @@ def main():
             b.synchronize()
             acc.append(a.elapsed_time(b))
         times[name] = statistics.median(acc)
-    imad_peak = lib.ensei_gpu_imad_peak(local)  # mad.wide.u32 ops/s, live probe
+    imad_peak = lib.ensei_gpu_imad_peak(local)  # IMAD-pipe slots/s (mad.lo.u32 chains), live probe
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
@@ -347,7 +351,7 @@ def main():
         "unit": "GIMAD/s" if bound == "imad" else "GB/s",
         "frac": imad_frac if bound == "imad" else hbm_frac,
         "traffic": None,
-        "peak_source": ("live mad.wide.u32 probe (ensei_gpu_imad_peak)" if bound == "imad"
+        "peak_source": ("live mad.lo.u32 probe (ensei_gpu_imad_peak)" if bound == "imad"
                         else "MEASURED_PEAKS.json hbm_gbs (measured)"),
         "imad": {"achieved_GIMAD_s": imad_ach, "peak_GIMAD_s": imad_peak / 1e9, "frac": imad_frac,
                  "imad_per_launch": kd["imad"], "c_q": C_Q, "c_mac": C_MAC, "c_p": C_P},

@@ -857,19 +857,23 @@ __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN), (512 / (S * (MT / TM)
           ys[u][j] = yl[u][j] + yh[u][j] + zero;
         }
       }
+      // k-parity outer: consecutive updates of one accumulator are 3*TM*TN products
+      // apart, so ptxas keeps IMAD.WIDE with the accumulator as addend (2 register
+      // reads per bank, no 3-input IADD3 of pair-aligned words)
 #pragma unroll
-      for (int i = 0; i < TM; ++i)
+      for (int u = 0; u < 2; ++u)
 #pragma unroll
-        for (int j = 0; j < TN; ++j)
-          asm("mad.wide.u32 %0, %3, %4, %0;\n\t"
-              "mad.wide.u32 %1, %5, %6, %1;\n\t"
-              "mad.wide.u32 %2, %7, %8, %2;\n\t"
-              "mad.wide.u32 %0, %9, %10, %0;\n\t"
-              "mad.wide.u32 %1, %11, %12, %1;\n\t"
-              "mad.wide.u32 %2, %13, %14, %2;"
-              : "+l"(L0[i][j]), "+l"(Lm[i][j]), "+l"(L2[i][j])
-              : "r"(xl[0][i]), "r"(yl[0][j]), "r"(xs[0][i]), "r"(ys[0][j]), "r"(xh[0][i]), "r"(yh[0][j]),
-                "r"(xl[1][i]), "r"(yl[1][j]), "r"(xs[1][i]), "r"(ys[1][j]), "r"(xh[1][i]), "r"(yh[1][j]));
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j)
+            asm("{\n\t.reg .u32 l0, h0, l1, h1, l2, h2;\n\t"
+                "mov.b64 {l0, h0}, %0;\n\tmov.b64 {l1, h1}, %1;\n\tmov.b64 {l2, h2}, %2;\n\t"
+                "mad.lo.cc.u32 l0, %3, %4, l0;\n\tmadc.hi.u32 h0, %3, %4, h0;\n\t"
+                "mad.lo.cc.u32 l1, %5, %6, l1;\n\tmadc.hi.u32 h1, %5, %6, h1;\n\t"
+                "mad.lo.cc.u32 l2, %7, %8, l2;\n\tmadc.hi.u32 h2, %7, %8, h2;\n\t"
+                "mov.b64 %0, {l0, h0};\n\tmov.b64 %1, {l1, h1};\n\tmov.b64 %2, {l2, h2};\n\t}"
+                : "+l"(L0[i][j]), "+l"(Lm[i][j]), "+l"(L2[i][j])
+                : "r"(xl[u][i]), "r"(yl[u][j]), "r"(xs[u][i]), "r"(ys[u][j]), "r"(xh[u][i]), "r"(yh[u][j]));
     };
     int kk = 0;
 #pragma unroll 1

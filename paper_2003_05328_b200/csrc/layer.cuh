@@ -105,6 +105,31 @@ struct PhiSrc {
   }
 };
 
+// Same as PhiSrc with c0, c1, t^, t^' staged in shared memory (swizzled u64 layout,
+// 16-byte paired reads).
+struct PhiSrcS {
+  const uint64_t *c0, *c1, *t, *tp;
+  Field64 f;
+  static constexpr bool kVec = true;
+  EG_DEV uint64_t at(int j) const {
+    const int s = sidx<uint64_t>(j);
+    uint64_t x = f.mul_shoup_approx(c0[s], t[s], tp[s]) + c1[s];  // < 5q
+    return hi32(x) > hi32(f.q4) ? x - f.q4 : x;
+  }
+  EG_DEV uint64_t operator()(int j) const { return at(j); }
+  EG_DEV void ld2(int j, uint64_t& x, uint64_t& y) const {
+    const int s = sidx<uint64_t>(j);
+    const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(c0 + s);
+    const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(c1 + s);
+    const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(t + s);
+    const ulonglong2 wp = *reinterpret_cast<const ulonglong2*>(tp + s);
+    x = f.mul_shoup_approx(a.x, w.x, wp.x) + b.x;
+    y = f.mul_shoup_approx(a.y, w.y, wp.y) + b.y;
+    x = hi32(x) > hi32(f.q4) ? x - f.q4 : x;
+    y = hi32(y) > hi32(f.q4) ? y - f.q4 : y;
+  }
+};
+
 // ------------------------------------------------------------ tile -> ring
 
 // Barrier over the NT threads of thread group g (literal ids keep ptxas' barrier
@@ -437,6 +462,15 @@ constexpr size_t dec_rns_smem() {
 // INTT_q -> round(p phi / q) -> decode (NTT_p) -> scatter into the tile; then all
 // threads: IDFT2D -> crop (-> + Bob's share).
 template <int LOGN, int LOGH, int LOGW, int G>
+constexpr size_t dec_smem() {
+  return (((size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4 + 127) & ~(size_t)127) +
+         G * ((((size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4) + 127) & ~(size_t)127);
+}
+
+// STG: the CTA's ciphertext blocks and the key are staged into shared memory with
+// cp.async (swizzled) before the first INTT pass, instead of per-thread dependent global
+// loads inside it (the pass was 30% of the kernel's stall samples at n = 2048).
+template <int LOGN, int LOGH, int LOGW, int G, bool STG>
 __global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE))
     dec_kernel(LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride,
                const uint64_t* __restrict__ ct, uint32_t* __restrict__ alice_share,
@@ -459,9 +493,22 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE))
   const PrimeConst pc = a.pc[0];
   const Field64 f = pc.f;
   const uint64_t cp = pc.cp, h = f.q >> 1;  // floor(p 2^64 / q), floor(q / 2)
+  uint64_t* kst = reinterpret_cast<uint64_t*>(smem_raw + dec_smem<LOGN, LOGH, LOGW, G>());  // [t^][t^'][B][c0][c1]
+  if constexpr (STG) {
+    const uint64_t* cg = ct + (size_t)item * a.B * ct_words<1>(N);
+    const int narr = 2 + 2 * a.B;  // N-word arrays: t^, t^', then c0, c1 per block
+    for (int e = threadIdx.x; e < narr * (N / 2); e += blockDim.x) {
+      const int arr = e / (N / 2), c = e % (N / 2);
+      const uint64_t* g0 = arr < 2 ? kimg + (size_t)arr * N : cg + (size_t)(arr - 2) * N;
+      cp_async16(kst + (size_t)arr * N + sidx<uint64_t>(2 * c), g0 + 2 * c);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+  }
   for (int b = g; b < a.B; b += G) {
     const uint64_t* cb = ct + ((size_t)item * a.B + b) * ct_words<1>(N);
-    PhiSrc src{cb, cb + N, kimg, kimg + N, f};
+    auto run_inv = [&](auto& src) {
     auto dst = [&](int i, uint64_t v) {
       const uint64_t phi = Bfly<Field64, 0>::fin_gs(f, v);
       // exact floor((p phi + floor(q/2)) / q) (REF ringbfv.cpp:224-229): the estimate
@@ -476,6 +523,14 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE))
       pbuf[sidx<uint32_t>(i)] = (uint32_t)(Q % p);
     };
     ntt_inverse<Field64, uint64_t, LOGN, kLogE, 0, false, false>(f, a.twq_inv[0], qbuf, tid, src, dst, bar);
+    };
+    if constexpr (STG) {
+      PhiSrcS src{kst + (size_t)(2 + 2 * b) * N, kst + (size_t)(3 + 2 * b) * N, kst, kst + N, f};
+      run_inv(src);
+    } else {
+      PhiSrc src{cb, cb + N, kimg, kimg + N, f};
+      run_inv(src);
+    }
     bar.sync();
     // decode_slots (NTT_p) -> scatter into the bit-reversed tile
     SmemRW<uint32_t> psrc{pbuf};
@@ -498,11 +553,6 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE))
   }
 }
 
-template <int LOGN, int LOGH, int LOGW, int G>
-constexpr size_t dec_smem() {
-  return (((size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4 + 127) & ~(size_t)127) +
-         G * ((((size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4) + 127) & ~(size_t)127);
-}
 
 // ------------------------------------------------------------ ElementMult
 
@@ -799,23 +849,25 @@ __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN), (512 / (S * (MT / TM)
     cp_async_commit();  // empty groups keep the wait_group count uniform
   };
 
-  uint64_t L0[TM][TN], Lm[TM][TN], L2[TM][TN];
+  // L split into 32-bit halves (not a register pair): the carry-chained multiply-add
+  // then updates the accumulator in place, with no pair-rotation moves
+  uint32_t L0l[TM][TN], L0h[TM][TN], Lml[TM][TN], Lmh[TM][TN], L2l[TM][TN], L2h[TM][TN];
   uint32_t H0[TM][TN], Hm[TM][TN], H2[TM][TN];
   auto zero_acc = [&]() {
 #pragma unroll
     for (int i = 0; i < TM; ++i)
 #pragma unroll
       for (int j = 0; j < TN; ++j) {
-        L0[i][j] = Lm[i][j] = L2[i][j] = 0;
+        L0l[i][j] = L0h[i][j] = Lml[i][j] = Lmh[i][j] = L2l[i][j] = L2h[i][j] = 0;
         H0[i][j] = Hm[i][j] = H2[i][j] = 0;
       }
   };
   // exact T = sum x y (u128) from the split sums, reduced mod q
   auto reduce_T = [&](const Field64& f, const PrimeConst& pc, int i, int j) -> uint64_t {
     typedef unsigned __int128 u128;
-    const u128 s0 = ((u128)H0[i][j] << kKaraLowBits) + L0[i][j];
-    const u128 sm = ((u128)Hm[i][j] << kKaraLowBits) + Lm[i][j];
-    const u128 s2 = ((u128)H2[i][j] << kKaraLowBits) + L2[i][j];
+    const u128 s0 = ((u128)H0[i][j] << kKaraLowBits) + (((uint64_t)L0h[i][j] << 32) | L0l[i][j]);
+    const u128 sm = ((u128)Hm[i][j] << kKaraLowBits) + (((uint64_t)Lmh[i][j] << 32) | Lml[i][j]);
+    const u128 s2 = ((u128)H2[i][j] << kKaraLowBits) + (((uint64_t)L2h[i][j] << 32) | L2l[i][j]);
     const u128 t = s0 + ((sm - s0 - s2) << 30) + (s2 << 60);
     const uint64_t lo = (uint64_t)t, hi = (uint64_t)(t >> 64);
     uint64_t x = Bfly<Field64, 0>::corr(f, lo, pc.cred);
@@ -866,13 +918,10 @@ __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN), (512 / (S * (MT / TM)
         for (int i = 0; i < TM; ++i)
 #pragma unroll
           for (int j = 0; j < TN; ++j)
-            asm("{\n\t.reg .u32 l0, h0, l1, h1, l2, h2;\n\t"
-                "mov.b64 {l0, h0}, %0;\n\tmov.b64 {l1, h1}, %1;\n\tmov.b64 {l2, h2}, %2;\n\t"
-                "mad.lo.cc.u32 l0, %3, %4, l0;\n\tmadc.hi.u32 h0, %3, %4, h0;\n\t"
-                "mad.lo.cc.u32 l1, %5, %6, l1;\n\tmadc.hi.u32 h1, %5, %6, h1;\n\t"
-                "mad.lo.cc.u32 l2, %7, %8, l2;\n\tmadc.hi.u32 h2, %7, %8, h2;\n\t"
-                "mov.b64 %0, {l0, h0};\n\tmov.b64 %1, {l1, h1};\n\tmov.b64 %2, {l2, h2};\n\t}"
-                : "+l"(L0[i][j]), "+l"(Lm[i][j]), "+l"(L2[i][j])
+            asm("mad.lo.cc.u32 %0, %6, %7, %0;\n\tmadc.hi.u32 %1, %6, %7, %1;\n\t"
+                "mad.lo.cc.u32 %2, %8, %9, %2;\n\tmadc.hi.u32 %3, %8, %9, %3;\n\t"
+                "mad.lo.cc.u32 %4, %10, %11, %4;\n\tmadc.hi.u32 %5, %10, %11, %5;"
+                : "+r"(L0l[i][j]), "+r"(L0h[i][j]), "+r"(Lml[i][j]), "+r"(Lmh[i][j]), "+r"(L2l[i][j]), "+r"(L2h[i][j])
                 : "r"(xl[u][i]), "r"(yl[u][j]), "r"(xs[u][i]), "r"(ys[u][j]), "r"(xh[u][i]), "r"(yh[u][j]));
     };
     int kk = 0;
@@ -884,16 +933,16 @@ __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN), (512 / (S * (MT / TM)
       for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) {
-          Hm[i][j] += (uint32_t)(Lm[i][j] >> kKaraLowBits);
-          Lm[i][j] &= kLowMask;
+          Hm[i][j] += Lmh[i][j] >> (kKaraLowBits - 32);
+          Lmh[i][j] &= (uint32_t)(kLowMask >> 32);
         }
       if (++blocks % 2 == 0) {  // S0: 15 products
 #pragma unroll
         for (int i = 0; i < TM; ++i)
 #pragma unroll
           for (int j = 0; j < TN; ++j) {
-            H0[i][j] += (uint32_t)(L0[i][j] >> kKaraLowBits);
-            L0[i][j] &= kLowMask;
+            H0[i][j] += L0h[i][j] >> (kKaraLowBits - 32);
+            L0h[i][j] &= (uint32_t)(kLowMask >> 32);
           }
         if (blocks == 10) {  // S2: 63 products
           blocks = 0;
@@ -901,8 +950,8 @@ __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN), (512 / (S * (MT / TM)
           for (int i = 0; i < TM; ++i)
 #pragma unroll
             for (int j = 0; j < TN; ++j) {
-              H2[i][j] += (uint32_t)(L2[i][j] >> kKaraLowBits);
-              L2[i][j] &= kLowMask;
+              H2[i][j] += L2h[i][j] >> (kKaraLowBits - 32);
+              L2h[i][j] &= (uint32_t)(kLowMask >> 32);
             }
         }
       }

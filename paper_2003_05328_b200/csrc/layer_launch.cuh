@@ -136,10 +136,17 @@ void launch_share(const LayerRun& r, bool inj, uint64_t* mask, uint32_t* bob_sha
 template <int LOGN, int LOGL, int G>
 static void dec_go_g(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint64_t* ct, uint32_t* alice,
                      const uint32_t* bob, uint32_t* out, int items) {
-  auto k = dec_kernel<LOGN, LOGL, LOGL, G>;
-  constexpr size_t smem = dec_smem<LOGN, LOGL, LOGL, G>();
-  set_smem(k, smem);
-  k<<<items, G * ((1 << LOGN) >> kLogE), smem, r.st>>>(r.a, key, ks, ct, alice, bob, out);
+  constexpr size_t base = dec_smem<LOGN, LOGL, LOGL, G>();
+  const size_t staged = base + (size_t)(2 + 2 * r.a.B) * (1 << LOGN) * 8;  // + t^, t^', c0/c1 per block
+  if (staged <= 227 * 1024) {
+    auto k = dec_kernel<LOGN, LOGL, LOGL, G, true>;
+    set_smem(k, staged);
+    k<<<items, G * ((1 << LOGN) >> kLogE), staged, r.st>>>(r.a, key, ks, ct, alice, bob, out);
+  } else {
+    auto k = dec_kernel<LOGN, LOGL, LOGL, G, false>;
+    set_smem(k, base);
+    k<<<items, G * ((1 << LOGN) >> kLogE), base, r.st>>>(r.a, key, ks, ct, alice, bob, out);
+  }
   check_launch("dec_kernel");
 }
 

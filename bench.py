@@ -45,6 +45,22 @@ METRIC = "oblivious NTT-domain conv/sec (1/2/4/8 B200); NTT modmul/s vs roofline
 C_Q, C_MAC, C_P = 10, 6, 3
 
 
+NCU_KERNELS = {"enc": "tile_enc_kernel", "share": "share_kernel", "mac": "mac_kara_kernel", "dec": "dec_kernel"}
+
+
+def ncu_traffic(cfg, name):
+    """DRAM bytes (read + write) per launch of kernel `name` from the committed ncu --set full
+    capture of this workload (profiles/*_ncu_traffic.json, written by tools/ncu_traffic.py);
+    None when no capture is committed."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_traffic.json")))
+    if not files:
+        return None
+    d = json.load(open(files[-1])).get(cfg, {})
+    rec = d.get(NCU_KERNELS.get(name, name))
+    return None if rec is None else rec["dram_bytes"]
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -350,13 +366,17 @@ def main():
         "peak": imad_peak / 1e9 if bound == "imad" else hbm_peak,
         "unit": "GIMAD/s" if bound == "imad" else "GB/s",
         "frac": imad_frac if bound == "imad" else hbm_frac,
-        "traffic": None,
+        "traffic": ncu_traffic("config1", dom),
         "peak_source": ("live mad.lo.u32 probe (ensei_gpu_imad_peak)" if bound == "imad"
                         else "MEASURED_PEAKS.json hbm_gbs (measured)"),
         "imad": {"achieved_GIMAD_s": imad_ach, "peak_GIMAD_s": imad_peak / 1e9, "frac": imad_frac,
                  "imad_per_launch": kd["imad"], "c_q": C_Q, "c_mac": C_MAC, "c_p": C_P},
         "hbm": {"achieved_GB_s": hbm_ach, "peak_GB_s": hbm_peak, "frac": hbm_frac, "bytes_per_launch": kd["bytes"]},
         "kernel_ms": times,
+        "per_kernel": {k: {"ms": times[k],
+                           "imad_frac": kcount[k]["imad"] / (times[k] * 1e-3) / imad_peak,
+                           "hbm_frac": kcount[k]["bytes"] / (times[k] * 1e-3) / 1e9 / hbm_peak}
+                       for k in times},
     }
     total_modmul = sum(v["modmul"] for v in kcount.values())
 

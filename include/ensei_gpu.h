@@ -231,10 +231,13 @@ int ensei_gpu_conv_layer(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const 
                          const ensei_randomness* rand, void* d_workspace, uint32_t* d_alice_share,
                          uint32_t* d_bob_share, uint32_t* d_out, void* stream);
 
-/* Same with HOST buffers (pinned recommended): copies h_in to the device,
- * runs the layer, copies the reconstructed output (and, if non-NULL, both
- * shares) back, synchronously on `stream`.  d_workspace must also hold the
- * staging input/output (ensei_gpu_conv_host_workspace_bytes()). */
+/* Same with HOST buffers, synchronous on `stream`.  Pinned (page-locked) buffers
+ * are read / written by the kernels in place across the host link (zero-copy:
+ * the transfers overlap the layer); pageable buffers are staged through
+ * d_workspace, which must hold the staging input/output
+ * (ensei_gpu_conv_host_workspace_bytes()).  The launch sequence is captured
+ * into a CUDA graph on first use and replayed while every argument is
+ * unchanged. */
 size_t ensei_gpu_conv_host_workspace_bytes(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
                                            uint32_t num_images, int in_dtype);
 int ensei_gpu_conv_layer_host(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
@@ -245,7 +248,7 @@ int ensei_gpu_conv_layer_host(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
 /* ------------------------------------------------------------ utilities */
 /* number of this library's kernels launched so far in the process */
 uint64_t ensei_gpu_launch_count(void);
-/* IMAD-pipe peak probe: returns mad.wide.u32 ops/s measured on `device` */
+/* IMAD-pipe peak probe: returns IMAD slots/s (dependent mad.lo.u32 chains) measured on `device` */
 double ensei_gpu_imad_peak(int device);
 
 #ifdef __cplusplus

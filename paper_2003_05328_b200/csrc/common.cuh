@@ -1,6 +1,7 @@
 // common.cuh -- context layout, error plumbing and launch bookkeeping shared by the
 // kernels and the C ABI (include/ensei_gpu.h).
 #pragma once
+#include <vector>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -91,5 +92,12 @@ struct ensei_gpu_ctx {
   // with Alice's encryption on an auxiliary stream (capturable in CUDA graphs)
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // ensei_gpu_conv_layer_host: H2D + layer + D2H captured once into a CUDA graph and
+  // replayed while every argument is unchanged (key = the arguments' bytes).
+  cudaStream_t host_st = nullptr;  // capture/replay stream when the caller passes the legacy stream
+  cudaEvent_t host_ev = nullptr;
+  cudaGraphExec_t host_graph = nullptr;
+  uint64_t host_graph_kernels = 0;  // kernels per replay (for ensei_gpu_launch_count)
+  std::vector<uint8_t> host_graph_key;
 
 };

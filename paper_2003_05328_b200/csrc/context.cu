@@ -179,6 +179,9 @@ void ensei_gpu_ctx_destroy(ensei_gpu_ctx* ctx) {
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->host_graph) cudaGraphExecDestroy(ctx->host_graph);
+  if (ctx->host_st) cudaStreamDestroy(ctx->host_st);
+  if (ctx->host_ev) cudaEventDestroy(ctx->host_ev);
   delete ctx;
 }
 

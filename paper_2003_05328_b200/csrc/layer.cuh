@@ -822,7 +822,8 @@ __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN), (512 / (S * (MT / TM)
       const uint64_t* as = ld.a_base + (size_t)kc * chan_stride + a_off;
       const uint64_t* ws = ld.w_base + (size_t)kc * w_chan + b_off;
 #pragma unroll
-      for (int kk = a_kk0, m = 0; m < KT / A_KSTEP; ++m, kk += A_KSTEP) {
+      for (int kk = a_kk0, m = 0; m < (KT + A_KSTEP - 1) / A_KSTEP; ++m, kk += A_KSTEP) {
+        if (kk >= KT) break;  // KT need not be a multiple of the copy stride
         uint64_t* dst = Ab + (kk * MT + a_row) * S + 2 * a_v;
         if (a_ok && kc + kk < K) {
           cp_async16(dst, as + (size_t)m * A_KSTEP * chan_stride);
@@ -832,7 +833,8 @@ __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN), (512 / (S * (MT / TM)
         }
       }
 #pragma unroll
-      for (int kk = b_kk0, m = 0; m < KT / B_KSTEP; ++m, kk += B_KSTEP) {
+      for (int kk = b_kk0, m = 0; m < (KT + B_KSTEP - 1) / B_KSTEP; ++m, kk += B_KSTEP) {
+        if (kk >= KT) break;
         uint64_t* dst = Bb + (kk * NT + b_col) * S + 2 * a_v;
         if (b_ok && kc + kk < K) {
           cp_async16(dst, ws + (size_t)m * B_KSTEP * w_chan);

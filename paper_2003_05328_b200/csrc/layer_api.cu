@@ -211,10 +211,13 @@ void mac_r(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* o
       return mac_kara_go<R, 8, 32, 16, 12, 2, 4, 3>(r, ct, w, out);
     case 3:
       if (small) return mac_kara_go<R, 8, 16, 16, 24, 2, 4, 2>(r, ct, w, out);
-      return mac_kara_go<R, 8, 32, 16, 24, 2, 4, 3>(r, ct, w, out);
+      return mac_kara_go<R, 8, 16, 16, 24, 2, 2, 2>(r, ct, w, out);
     case 4:
       if (small) return mac_kara_go<R, 4, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
-      return mac_kara_go<R, 16, 16, 16, 24, 2, 4, 2>(r, ct, w, out);
+      return mac_kara_go<R, 4, 32, 16, 24, 2, 2, 2>(r, ct, w, out);
+    case 5:
+      if (small) return mac_kara_go<R, 4, 16, 16, 12, 2, 2, 3>(r, ct, w, out);
+      return mac_kara_go<R, 4, 32, 32, 24, 2, 2, 2>(r, ct, w, out);
     default:
       if (small) return mac_kara_go<R, 8, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
       return mac_kara_go<R, 8, 32, 16, 24, 2, 4, 2>(r, ct, w, out);
@@ -526,16 +529,89 @@ int ensei_gpu_conv_layer_host(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, c
                               const uint64_t* d_w_eval, const void* h_in, int in_dtype, uint32_t num_images,
                               const ensei_randomness* rand, void* d_workspace, uint32_t* h_out, void* stream) {
   return guarded([&] {
-    require(ctx && desc && h_in && h_out && d_workspace, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    require(ctx && desc && h_in && h_out && d_workspace && rand, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
     Geo g = geometry(ctx, desc);
     Workspace w = carve(ctx, desc, g, num_images, d_workspace, in_dtype, true);
-    cudaStream_t st = (cudaStream_t)stream;
     const size_t nin = (size_t)num_images * desc->cin * desc->H * desc->W * (in_dtype == ENSEI_IN_U8 ? 1 : 4);
     const size_t nout = (size_t)num_images * desc->cout * g.oh * g.ow * sizeof(uint32_t);
-    EG_CUDA(cudaMemcpyAsync(w.stage_in, h_in, nin, cudaMemcpyHostToDevice, st));
-    conv_layer(ctx, desc, d_key, 0, d_w_eval, w.stage_in, in_dtype, nullptr, num_images, rand, d_workspace, nullptr,
-               nullptr, w.stage_out, stream);
-    EG_CUDA(cudaMemcpyAsync(h_out, w.stage_out, nout, cudaMemcpyDeviceToHost, st));
+    cudaStream_t user = (cudaStream_t)stream;
+    // the legacy stream cannot be captured: run on the context's own stream, ordered after
+    // the caller's prior work by an event
+    if (!ctx->host_st) {
+      EG_CUDA(cudaStreamCreateWithFlags(&ctx->host_st, cudaStreamNonBlocking));
+      EG_CUDA(cudaEventCreateWithFlags(&ctx->host_ev, cudaEventDisableTiming));
+    }
+    cudaStream_t st = user ? user : ctx->host_st;
+    if (!user) {
+      EG_CUDA(cudaEventRecord(ctx->host_ev, 0));
+      EG_CUDA(cudaStreamWaitEvent(st, ctx->host_ev, 0));
+    }
+    // Pinned (page-locked) host buffers are device-addressable: Enc then reads the pixels
+    // and Dec writes the outputs across the host link directly (zero-copy), so the
+    // transfers overlap the kernels instead of being two serial memcpys with their own
+    // fixed latency.  Pageable buffers go through the workspace staging copies.
+    auto mapped = [](const void* h) -> void* {
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+      }
+      return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+    };
+    const void* din = mapped(h_in);
+    uint32_t* dout = static_cast<uint32_t*>(mapped(h_out));
+    auto enqueue = [&] {
+      if (!din) EG_CUDA(cudaMemcpyAsync(w.stage_in, h_in, nin, cudaMemcpyHostToDevice, st));
+      conv_layer(ctx, desc, d_key, 0, d_w_eval, din ? din : w.stage_in, in_dtype, nullptr, num_images, rand,
+                 d_workspace, nullptr, nullptr, dout ? dout : w.stage_out, st);
+      if (!dout) EG_CUDA(cudaMemcpyAsync(h_out, w.stage_out, nout, cudaMemcpyDeviceToHost, st));
+    };
+    // graph key: every argument that shapes the launches (pointers, sizes, randomness)
+    std::vector<uint8_t> key;
+    auto put = [&](const void* p, size_t n) {
+      const uint8_t* b = static_cast<const uint8_t*>(p);
+      key.insert(key.end(), b, b + n);
+    };
+    put(desc, sizeof(*desc));
+    put(rand, sizeof(*rand));
+    const void* ptrs[] = {d_key, d_w_eval, h_in, d_workspace, h_out, st};
+    put(ptrs, sizeof(ptrs));
+    put(&in_dtype, sizeof(in_dtype));
+    put(&num_images, sizeof(num_images));
+    if (!(ctx->host_graph && key == ctx->host_graph_key)) {
+      if (ctx->host_graph) {
+        cudaGraphExecDestroy(ctx->host_graph);
+        ctx->host_graph = nullptr;
+      }
+      ctx->host_graph_key.clear();
+      cudaGraph_t graph = nullptr;
+      bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      const uint64_t before = g_launches.load();
+      if (ok) {
+        try {
+          enqueue();
+        } catch (...) {
+          cudaStreamEndCapture(st, &graph);
+          if (graph) cudaGraphDestroy(graph);
+          throw;
+        }
+        ctx->host_graph_kernels = g_launches.load() - before;
+        g_launches.fetch_sub(ctx->host_graph_kernels);  // captured, not launched: counted at replay
+        ok = cudaStreamEndCapture(st, &graph) == cudaSuccess && graph;
+        ok = ok && cudaGraphInstantiate(&ctx->host_graph, graph, 0) == cudaSuccess;
+        if (graph) cudaGraphDestroy(graph);
+      }
+      if (!ok) {  // not capturable (e.g. pageable host memory): plain launches
+        cudaGetLastError();
+        ctx->host_graph = nullptr;
+        enqueue();
+        EG_CUDA(cudaStreamSynchronize(st));
+        return;
+      }
+      ctx->host_graph_key = key;
+    }
+    EG_CUDA(cudaGraphLaunch(ctx->host_graph, st));
+    count_launch(ctx->host_graph_kernels);
     EG_CUDA(cudaStreamSynchronize(st));
   });
 }

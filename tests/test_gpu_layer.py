@@ -162,8 +162,20 @@ def test_host_buffer_entry_equals_device_path(ops):
     we = L.prepare_weights(w.to(dev()))
     d = L.forward(key, we, imgs.to(dev()), ops.Randomness(seed=2))
     h_out = torch.empty((2, 4, 16, 16), dtype=torch.int32).pin_memory()
-    L.forward_host(key, we, imgs.pin_memory(), ops.Randomness(seed=2), L.workspace(2, host=True), h_out)
+    h_in, ws = imgs.pin_memory(), L.workspace(2, host=True)
+    L.forward_host(key, we, h_in, ops.Randomness(seed=2), ws, h_out)
     assert torch.equal(h_out, d.cpu())
+    # same arguments: the cached CUDA graph replays and reads the host buffer's new contents
+    imgs2 = torch.randint(0, 256, (2, 4, 16, 16), dtype=torch.uint8, generator=g)
+    h_in.copy_(imgs2)
+    L.forward_host(key, we, h_in, ops.Randomness(seed=2), ws, h_out)
+    assert torch.equal(h_out, L.forward(key, we, imgs2.to(dev()), ops.Randomness(seed=2)).cpu())
+    # changed randomness -> re-captured graph; pageable buffers -> uncaptured fallback
+    L.forward_host(key, we, h_in, ops.Randomness(seed=3), ws, h_out)
+    assert torch.equal(h_out, L.forward(key, we, imgs2.to(dev()), ops.Randomness(seed=3)).cpu())
+    out_pageable = torch.empty((2, 4, 16, 16), dtype=torch.int32)
+    L.forward_host(key, we, imgs2.clone(), ops.Randomness(seed=3), ws, out_pageable)
+    assert torch.equal(out_pageable, h_out)
 
 
 def test_pooled_relu_stack_vs_oracle(ops):

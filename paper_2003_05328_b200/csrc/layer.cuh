@@ -22,7 +22,11 @@
 
 namespace ensei_gpu {
 
-constexpr int kLogE = 3;  // elements per thread in the ring transforms (E = 8)
+// log2(coefficients per thread) in the ring transforms of the tile kernels (8 per thread,
+// n/8 threads per ring polynomial, radix-8 register passes).  4 per thread at n = 2048
+// (twice the threads per tile, 6 passes instead of 4) was measured slower: config 1
+// 78.6 -> 86.5 us per step, config 3 -9 %.
+__host__ __device__ constexpr int tile_loge(int) { return 3; }
 // Tile kernels are latency-bound (one CTA per tile, serial fused stages): capping them
 // at 64 registers lets two CTAs share an SM, so Bob's HomShare CTAs co-reside with
 // Alice's Enc CTAs and each hides the other's latency.
@@ -151,10 +155,10 @@ enum TileMode { TILE_ENC = 0, TILE_HOMREC = 1, TILE_WEIGHTS = 2 };
 // a^ t^, stores) runs as a separate coalesced loop after the NTT, not inside its
 // unrolled last pass, to keep register pressure low.
 template <int LOGN, int LOGH, int LOGW, int R, int TM, bool INJ, int IN_T, int G>
-__global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE), tile_min_blocks(G*((1 << LOGN) >> kLogE)))
+__global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_blocks(G*((1 << LOGN) >> tile_loge(LOGN))))
     tile_enc_kernel(LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride,
                     const void* __restrict__ in, uint64_t* __restrict__ out) {
-  constexpr int N = 1 << LOGN, NT = N >> kLogE;
+  constexpr int N = 1 << LOGN, NT = N >> tile_loge(LOGN);
   constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
   constexpr size_t GROUP_BYTES = (size_t)N * 8 + ssize<uint32_t>(N) * 4 + N;
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -220,7 +224,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE), tile_min_blocks(G*((
       auto src = [&](int j) { return gather_slot<LOGN, LOGH, LOGW>(S, b, j, a.G); };
       SmemRW<uint32_t> dst_raw{pbuf};
       auto dst = [&](int i, uint32_t v) { dst_raw(i, Bfly<Field32, 0>::fin_gs(pf, v)); };
-      ntt_inverse<Field32, uint32_t, LOGN, kLogE, 0, false, false>(pf, a.twp_inv, pbuf, tid, src, dst, bar);
+      ntt_inverse<Field32, uint32_t, LOGN, tile_loge(LOGN), 0, false, false>(pf, a.twp_inv, pbuf, tid, src, dst, bar);
     }
     bar.sync();
 #pragma unroll 1
@@ -243,7 +247,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE), tile_min_blocks(G*((
       };
       // 5. NTT_q in place (lazy values stay in qbuf), then the epilogue
       SmemRW<uint64_t> qs{qbuf};
-      ntt_forward<Field64, uint64_t, LOGN, kLogE, 0, false, false>(f, a.twq_fwd[r], qbuf, tid, src, qs, bar,
+      ntt_forward<Field64, uint64_t, LOGN, tile_loge(LOGN), 0, false, false>(f, a.twq_fwd[r], qbuf, tid, src, qs, bar,
                                                                    pc.cred);
       bar.sync();
       if constexpr (TM == TILE_WEIGHTS) {
@@ -292,9 +296,9 @@ constexpr size_t tile_enc_smem() {
 // NTT_q(Delta*INTT_p(p - s_B)) go to the c1 words of the output ciphertext (device
 // layout) and Bob's share = crop(IDFT2D(merge(s_B))).
 template <int LOGN, int LOGH, int LOGW, int R, bool INJ, int G>
-__global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE), tile_min_blocks(G*((1 << LOGN) >> kLogE)))
+__global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_blocks(G*((1 << LOGN) >> tile_loge(LOGN))))
     share_kernel(LayerArgs a, uint64_t* __restrict__ mask, uint32_t* __restrict__ bob_share) {
-  constexpr int N = 1 << LOGN, NT = N >> kLogE;
+  constexpr int N = 1 << LOGN, NT = N >> tile_loge(LOGN);
   constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
   constexpr size_t GROUP_BYTES = (size_t)N * 8 + ssize<uint32_t>(N) * 4;
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -334,7 +338,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE), tile_min_blocks(G*((
     };
     SmemRW<uint32_t> dst_raw{pbuf};
     auto dst = [&](int i, uint32_t v) { dst_raw(i, Bfly<Field32, 0>::fin_gs(pf, v)); };
-    ntt_inverse<Field32, uint32_t, LOGN, kLogE, 0, false, false>(pf, a.twp_inv, pbuf, tid, src, dst, bar);
+    ntt_inverse<Field32, uint32_t, LOGN, tile_loge(LOGN), 0, false, false>(pf, a.twp_inv, pbuf, tid, src, dst, bar);
     bar.sync();
 #pragma unroll 1
     for (int r = 0; r < R; ++r) {
@@ -344,7 +348,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE), tile_min_blocks(G*((
       // mask lands where c1 of the output ciphertext (img, o, b) lives
       uint64_t* mo = mask + ((size_t)item * a.B + b) * ct_words<R>(N) + (size_t)(R + r) * N;
       GlobalOut64Fwd outw{mo, f, pc.cred};
-      ntt_forward<Field64, uint64_t, LOGN, kLogE, 0, false, false>(f, a.twq_fwd[r], qbuf, tid, qsrc, outw, bar,
+      ntt_forward<Field64, uint64_t, LOGN, tile_loge(LOGN), 0, false, false>(f, a.twq_fwd[r], qbuf, tid, qsrc, outw, bar,
                                                                    pc.cred);
       bar.sync();
     }
@@ -379,11 +383,11 @@ constexpr size_t share_smem(int B) {
 // extension: REF has no RNS; pinned by the oracle's exact
 // multi-limb CRT rounding (eo_crt_round).
 template <int LOGN, int LOGH, int LOGW, int R>
-__global__ void __launch_bounds__((1 << LOGN) >> kLogE)
+__global__ void __launch_bounds__((1 << LOGN) >> tile_loge(LOGN))
     dec_rns_kernel(LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride,
                    const uint64_t* __restrict__ ct, uint32_t* __restrict__ alice_share,
                    const uint32_t* __restrict__ bob_share, uint32_t* __restrict__ outp) {
-  constexpr int N = 1 << LOGN, NT = N >> kLogE;
+  constexpr int N = 1 << LOGN, NT = N >> tile_loge(LOGN);
   constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
@@ -424,7 +428,7 @@ __global__ void __launch_bounds__((1 << LOGN) >> kLogE)
         pbuf[sidx<uint32_t>(i)] = acc >= p ? acc - p : acc;
         facc[i] += (double)rem * pc.inv_q;
       };
-      ntt_inverse<Field64, uint64_t, LOGN, kLogE, 0, false, false>(f, a.twq_inv[r], qbuf, tid, src, dst, bar);
+      ntt_inverse<Field64, uint64_t, LOGN, tile_loge(LOGN), 0, false, false>(f, a.twq_inv[r], qbuf, tid, src, dst, bar);
       __syncthreads();
     }
     for (int i = tid; i < N; i += NT) {
@@ -434,7 +438,7 @@ __global__ void __launch_bounds__((1 << LOGN) >> kLogE)
     __syncthreads();
     SmemRW<uint32_t> psrc{pbuf};
     auto pdst = [&](int j, uint32_t v) { scatter_slot<LOGN, LOGH, LOGW>(S, b, j, a.G, reduce_lazy(pf, v, a.pp.cred)); };
-    ntt_forward<Field32, uint32_t, LOGN, kLogE, 0, false, false>(pf, a.twp_fwd, pbuf, tid, psrc, pdst, bar);
+    ntt_forward<Field32, uint32_t, LOGN, tile_loge(LOGN), 0, false, false>(pf, a.twp_fwd, pbuf, tid, psrc, pdst, bar);
     __syncthreads();
   }
   tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, S, LS);
@@ -471,11 +475,11 @@ constexpr size_t dec_smem() {
 // cp.async (swizzled) before the first INTT pass, instead of per-thread dependent global
 // loads inside it (the pass was 30% of the kernel's stall samples at n = 2048).
 template <int LOGN, int LOGH, int LOGW, int G, bool STG>
-__global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE))
+__global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)))
     dec_kernel(LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride,
                const uint64_t* __restrict__ ct, uint32_t* __restrict__ alice_share,
                const uint32_t* __restrict__ bob_share, uint32_t* __restrict__ outp) {
-  constexpr int N = 1 << LOGN, NT = N >> kLogE;
+  constexpr int N = 1 << LOGN, NT = N >> tile_loge(LOGN);
   constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
   constexpr size_t GROUP_BYTES = (size_t)N * 8 + ssize<uint32_t>(N) * 4;
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -522,7 +526,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE))
       }
       pbuf[sidx<uint32_t>(i)] = (uint32_t)(Q % p);
     };
-    ntt_inverse<Field64, uint64_t, LOGN, kLogE, 0, false, false>(f, a.twq_inv[0], qbuf, tid, src, dst, bar);
+    ntt_inverse<Field64, uint64_t, LOGN, tile_loge(LOGN), 0, false, false>(f, a.twq_inv[0], qbuf, tid, src, dst, bar);
     };
     if constexpr (STG) {
       PhiSrcS src{kst + (size_t)(2 + 2 * b) * N, kst + (size_t)(3 + 2 * b) * N, kst, kst + N, f};
@@ -535,7 +539,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> kLogE))
     // decode_slots (NTT_p) -> scatter into the bit-reversed tile
     SmemRW<uint32_t> psrc{pbuf};
     auto pdst = [&](int j, uint32_t v) { scatter_slot<LOGN, LOGH, LOGW>(S, b, j, a.G, reduce_lazy(pf, v, a.pp.cred)); };
-    ntt_forward<Field32, uint32_t, LOGN, kLogE, 0, false, false>(pf, a.twp_fwd, pbuf, tid, psrc, pdst, bar);
+    ntt_forward<Field32, uint32_t, LOGN, tile_loge(LOGN), 0, false, false>(pf, a.twp_fwd, pbuf, tid, psrc, pdst, bar);
     bar.sync();
   }
   __syncthreads();

@@ -31,7 +31,7 @@ static void enc_go_g(const LayerRun& r, const uint64_t* key, uint32_t key_stride
   auto k = tile_enc_kernel<LOGN, LOGL, LOGL, R, TM, INJ, IN_T, G>;
   constexpr size_t smem = tile_enc_smem<LOGN, LOGL, LOGL, G>();
   set_smem(k, smem);
-  k<<<items, G * ((1 << LOGN) >> kLogE), smem, r.st>>>(r.a, key, key_stride, in, out);
+  k<<<items, G * ((1 << LOGN) >> tile_loge(LOGN)), smem, r.st>>>(r.a, key, key_stride, in, out);
   check_launch("tile_enc_kernel");
 }
 
@@ -92,7 +92,7 @@ static void share_go_g(const LayerRun& r, uint64_t* ct_out, uint32_t* bob_share,
   auto k = share_kernel<LOGN, LOGL, LOGL, R, INJ, G>;
   const size_t smem = share_smem<LOGN, LOGL, LOGL, G>(r.a.B);
   set_smem(k, smem);
-  k<<<items, G * ((1 << LOGN) >> kLogE), smem, r.st>>>(r.a, ct_out, bob_share);
+  k<<<items, G * ((1 << LOGN) >> tile_loge(LOGN)), smem, r.st>>>(r.a, ct_out, bob_share);
   check_launch("share_kernel");
 }
 
@@ -141,11 +141,11 @@ static void dec_go_g(const LayerRun& r, const uint64_t* key, uint32_t ks, const 
   if (staged <= 227 * 1024) {
     auto k = dec_kernel<LOGN, LOGL, LOGL, G, true>;
     set_smem(k, staged);
-    k<<<items, G * ((1 << LOGN) >> kLogE), staged, r.st>>>(r.a, key, ks, ct, alice, bob, out);
+    k<<<items, G * ((1 << LOGN) >> tile_loge(LOGN)), staged, r.st>>>(r.a, key, ks, ct, alice, bob, out);
   } else {
     auto k = dec_kernel<LOGN, LOGL, LOGL, G, false>;
     set_smem(k, base);
-    k<<<items, G * ((1 << LOGN) >> kLogE), base, r.st>>>(r.a, key, ks, ct, alice, bob, out);
+    k<<<items, G * ((1 << LOGN) >> tile_loge(LOGN)), base, r.st>>>(r.a, key, ks, ct, alice, bob, out);
   }
   check_launch("dec_kernel");
 }
@@ -165,7 +165,7 @@ static void dec_rns_go(const LayerRun& r, const uint64_t* key, uint32_t ks, cons
   auto k = dec_rns_kernel<LOGN, LOGL, LOGL, 3>;
   constexpr size_t smem = dec_rns_smem<LOGN, LOGL, LOGL>();
   set_smem(k, smem);
-  k<<<items, (1 << LOGN) >> kLogE, smem, r.st>>>(r.a, key, ks, ct, alice, bob, out);
+  k<<<items, (1 << LOGN) >> tile_loge(LOGN), smem, r.st>>>(r.a, key, ks, ct, alice, bob, out);
   check_launch("dec_rns_kernel");
 }
 
@@ -197,9 +197,9 @@ void launch_dec(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint6
 
 // ---- secret key: t -> (t_eval, Shoup companion) per prime, device layout ----
 template <int LOGN>
-__global__ void __launch_bounds__((1 << LOGN) >> kLogE)
+__global__ void __launch_bounds__((1 << LOGN) >> tile_loge(LOGN))
     secret_kernel(LayerArgs a, const int64_t* t_in, int64_t* t_out, uint64_t* key, int sample) {
-  constexpr int N = 1 << LOGN, NT = N >> kLogE;
+  constexpr int N = 1 << LOGN, NT = N >> tile_loge(LOGN);
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
   const int r = blockIdx.x;
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__((1 << LOGN) >> kLogE)
     kr[j] = x;
     kr[N + j] = (uint64_t)(((unsigned __int128)x << 64) / f.q);
   };
-  ntt_forward<Field64, uint64_t, LOGN, kLogE, 0, false, false>(f, a.twq_fwd[r], qbuf, threadIdx.x, src, dst, bar,
+  ntt_forward<Field64, uint64_t, LOGN, tile_loge(LOGN), 0, false, false>(f, a.twq_fwd[r], qbuf, threadIdx.x, src, dst, bar,
                                                                pc.cred);
 }
 
@@ -231,7 +231,7 @@ void launch_secret(const LayerRun& r, const int64_t* t_in, int64_t* t_out, uint6
   auto k = secret_kernel<LOGN>;
   constexpr size_t smem = (size_t)(1 << LOGN) * 8;
   set_smem(k, smem);
-  k<<<r.R, (1 << LOGN) >> kLogE, smem, r.st>>>(r.a, t_in, t_out, key, sample ? 1 : 0);
+  k<<<r.R, (1 << LOGN) >> tile_loge(LOGN), smem, r.st>>>(r.a, t_in, t_out, key, sample ? 1 : 0);
   check_launch("secret_kernel");
 }
 

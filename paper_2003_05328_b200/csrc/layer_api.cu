@@ -198,30 +198,22 @@ static int mac_variant() {
   return v;
 }
 
+// Tile choice (measured on B200, configs 1/3/4): 8-slot x 32-row x 16-col tiles with 24-channel
+// chunks and 2 stages for the large shapes; 8 x 16 x 16 with 12-channel chunks, 3 stages when
+// rows and cols fit 16.  Alternatives measured slower: 4 outputs per thread (no register-pair
+// moves but one more shared load per MAC), 12-channel chunks with 3 stages, 4-slot tiles.
+// ENSEI_MAC_VARIANT=0 forces the 4-product kernel (A/B); it is also the fallback for primes
+// outside the Karatsuba headroom (kara_ok).
 template <int R>
 void mac_r(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
   const int rows = 2 * r.a.num_images, cols = r.a.cout;
   const bool small = rows <= 16 && cols <= 16;
-  switch (r.ctx->kara_ok ? mac_variant() : 0) {
-    case 0:  // four-product kernel (kept for A/B)
-      if (small) return mac_go<R, 16, 16, 16, 16, 2, 4>(r, ct, w, out);
-      return mac_go<R, 8, 32, 32, 16, 4, 4>(r, ct, w, out);
-    case 2:
-      if (small) return mac_kara_go<R, 4, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
-      return mac_kara_go<R, 8, 32, 16, 12, 2, 4, 3>(r, ct, w, out);
-    case 3:
-      if (small) return mac_kara_go<R, 8, 16, 16, 24, 2, 4, 2>(r, ct, w, out);
-      return mac_kara_go<R, 8, 16, 16, 24, 2, 2, 2>(r, ct, w, out);
-    case 4:
-      if (small) return mac_kara_go<R, 4, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
-      return mac_kara_go<R, 4, 32, 16, 24, 2, 2, 2>(r, ct, w, out);
-    case 5:
-      if (small) return mac_kara_go<R, 4, 16, 16, 12, 2, 2, 3>(r, ct, w, out);
-      return mac_kara_go<R, 4, 32, 32, 24, 2, 2, 2>(r, ct, w, out);
-    default:
-      if (small) return mac_kara_go<R, 8, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
-      return mac_kara_go<R, 8, 32, 16, 24, 2, 4, 2>(r, ct, w, out);
+  if (!r.ctx->kara_ok || mac_variant() == 0) {
+    if (small) return mac_go<R, 16, 16, 16, 16, 2, 4>(r, ct, w, out);
+    return mac_go<R, 8, 32, 32, 16, 4, 4>(r, ct, w, out);
   }
+  if (small) return mac_kara_go<R, 8, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
+  return mac_kara_go<R, 8, 32, 16, 24, 2, 4, 2>(r, ct, w, out);
 }
 
 void mac(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {

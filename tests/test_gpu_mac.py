@@ -77,3 +77,17 @@ def test_bob_mac_exact(ops, n, images, cin, cout, R):
                             acc = acc + mask[img, :, b, r, k].astype(object)
                         exp = np.array([int(v) % qr for v in acc], dtype=np.uint64)
                         assert (got[img, :, b, comp, r, k] == exp).all(), (b, r, k, img, comp)
+
+
+def test_bob_mac_four_product_fallback():
+    """The 4-product kernel (fallback for primes outside the Karatsuba headroom) on the same
+    edge shapes; selected in a fresh process by ENSEI_MAC_VARIANT=0 (read once per process)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, ENSEI_MAC_VARIANT="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", os.path.join(here, "test_gpu_mac.py"),
+                        "-k", "test_bob_mac_exact"], env=env, capture_output=True, text=True, timeout=900,
+                       cwd=os.path.dirname(here))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

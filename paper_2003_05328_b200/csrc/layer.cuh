@@ -1002,6 +1002,55 @@ __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN), (512 / (S * (MT / TM)
   cp_async_wait_all();
 }
 
+// ElementMult for tiny channel counts (config 0's 1 -> 1 layer): the tile GEMM would leave
+// most of its 16-column tiles and its 12/24-channel K chunks empty and pay the u128
+// epilogue per single product.  One thread per (image, block, prime, slot) computes every
+// (out channel, component) output of that slot directly: exact u128 sum of cin products
+// (cin (q-1)^2 < 2^128), one reduction, + the HomShare mask on c1.  Consecutive threads
+// touch consecutive slots (coalesced); the kernel is HBM-bound.
+template <int R>
+__global__ void __launch_bounds__(256)
+    mac_direct_kernel(LayerArgs a, int logn, const uint64_t* __restrict__ ct, const uint64_t* __restrict__ w,
+                      int has_mask, uint64_t* __restrict__ out) {
+  typedef unsigned __int128 u128;
+  const int n = 1 << logn;
+  const size_t slots = (size_t)a.B * R * n;  // per image: (block, prime, slot)
+  const size_t total = (size_t)a.num_images * slots;
+  const size_t ctw = (size_t)ct_words<R>(n);
+  const size_t chan_stride = (size_t)a.B * ctw;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+    const size_t img = t / slots, rem = t % slots;
+    const int bp = (int)(rem >> logn), sl = (int)(rem & (n - 1));
+    const int b = bp / R, r = bp % R;
+    const PrimeConst pc = a.pc[r];
+    const Field64 f = pc.f;
+    const uint64_t* xb = ct + img * a.cin * chan_stride + (size_t)b * ctw + (size_t)r * n + sl;
+    const uint64_t* wb = w + (size_t)bp * n + sl;
+    uint64_t* ob = out + img * a.cout * chan_stride + (size_t)b * ctw + (size_t)r * n + sl;
+    for (int o = 0; o < a.cout; ++o) {
+      u128 T0 = 0, T1 = 0;
+      for (int c = 0; c < a.cin; ++c) {
+        const uint64_t v = wb[((size_t)o * a.cin + c) * a.B * R * n];
+        const uint64_t y = (v & 0x3FFFFFFFull) | ((v >> 32) << 30);  // unpack the MAC limb format
+        T0 += (u128)xb[(size_t)c * chan_stride] * y;
+        T1 += (u128)xb[(size_t)c * chan_stride + (size_t)R * n] * y;
+      }
+      uint64_t res[2];
+      const u128 T[2] = {T0, T1};
+#pragma unroll
+      for (int comp = 0; comp < 2; ++comp) {
+        uint64_t x = Bfly<Field64, 0>::corr(f, (uint64_t)T[comp], pc.cred);
+        const uint64_t hi = (uint64_t)(T[comp] >> 64);
+        if (hi) x += f.mul_shoup_approx(hi, pc.c64, pc.c64p);
+        res[comp] = Bfly<Field64, 0>::fin_ct(f, x, pc.cred);
+      }
+      uint64_t* oo = ob + (size_t)o * chan_stride;
+      oo[0] = res[0];
+      oo[(size_t)R * n] = has_mask ? f.add(res[1], oo[(size_t)R * n]) : res[1];
+    }
+  }
+}
+
 template <int S, int MT, int NT, int KT>
 constexpr size_t mac_smem() {
   return (size_t)2 * KT * (MT + NT) * S * sizeof(uint64_t);

@@ -198,16 +198,26 @@ static int mac_variant() {
   return v;
 }
 
-// Tile choice (measured on B200, configs 1/3/4): 8-slot x 32-row x 16-col tiles with 24-channel
+// Tile choice (measured on B200, configs 1/3/4; cout <= 2 and cin <= 4 use mac_direct_kernel): 8-slot x 32-row x 16-col tiles with 24-channel
 // chunks and 2 stages for the large shapes; 8 x 16 x 16 with 12-channel chunks, 3 stages when
 // rows and cols fit 16.  Alternatives measured slower: 4 outputs per thread (no register-pair
 // moves but one more shared load per MAC), 12-channel chunks with 3 stages, 4-slot tiles.
 // ENSEI_MAC_VARIANT=0 forces the 4-product kernel (A/B); it is also the fallback for primes
 // outside the Karatsuba headroom (kara_ok).
 template <int R>
+void mac_direct_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
+  const size_t total = (size_t)r.a.num_images * r.a.B * R * r.ctx->n;
+  const long grid = std::min<long>((long)((total + 255) / 256), (long)r.ctx->sm_count * 8);
+  mac_direct_kernel<R><<<(unsigned)grid, 256, 0, r.st>>>(r.a, (int)r.ctx->logn, ct, w, 1, out);
+  check_launch("mac_direct_kernel");
+}
+
+template <int R>
 void mac_r(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
   const int rows = 2 * r.a.num_images, cols = r.a.cout;
   const bool small = rows <= 16 && cols <= 16;
+  // tiny channel counts (config 0: 1 -> 1): direct per-slot kernel (exact while cin <= 1008)
+  if (r.a.cout <= 2 && r.a.cin <= 4) return mac_direct_go<R>(r, ct, w, out);
   if (!r.ctx->kara_ok || mac_variant() == 0) {
     if (small) return mac_go<R, 16, 16, 16, 16, 2, 4>(r, ct, w, out);
     return mac_go<R, 8, 32, 32, 16, 4, 4>(r, ct, w, out);

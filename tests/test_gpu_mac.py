@@ -28,10 +28,13 @@ def _pack(v):
     return ((v >> np.uint64(30)) << np.uint64(32)) | (v & np.uint64(M30))
 
 
-# (n, images, cin, cout, primes): small-tile path (rows, cols <= 16), large tiles with partial
-# row/col tiles, odd K, K = one fold block + tail, K across chunks, K > 1008 (residue carry)
+# (n, images, cin, cout, primes): direct kernel for tiny channel counts, small-tile path (rows,
+# cols <= 16), large tiles with partial row/col tiles, odd K, K = one fold block + tail, K across
+# chunks, K > 1008 (residue carry)
 CASES = [
-    (2048, 1, 1, 1, 1),
+    (2048, 1, 1, 1, 1),           # direct per-slot kernel (cout <= 2, cin <= 4): config 0's 1 -> 1
+    (2048, 5, 4, 2, 1),           # direct kernel, several channels
+    (8192, 3, 3, 1, 3),           # direct kernel, three primes
     (2048, 3, 5, 7, 1),
     (2048, 8, 16, 16, 1),
     (2048, 3, 13, 36, 1),

@@ -198,7 +198,7 @@ static int mac_variant() {
   return v;
 }
 
-// Tile choice (measured on B200, configs 1/3/4; cout <= 2 and cin <= 4 use mac_direct_kernel): 8-slot x 32-row x 16-col tiles with 24-channel
+// Tile choice (measured on B200, configs 1/3/4; cout <= 2 and cin <= 4 use mac_direct_kernel): 8-slot x 32-row x 16-col tiles with 36-channel
 // chunks and 2 stages for the large shapes; 8 x 16 x 16 with 12-channel chunks, 3 stages when
 // rows and cols fit 16.  Alternatives measured slower: 4 outputs per thread (no register-pair
 // moves but one more shared load per MAC), 12-channel chunks with 3 stages, 4-slot tiles.
@@ -223,7 +223,7 @@ void mac_r(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* o
     return mac_go<R, 8, 32, 32, 16, 4, 4>(r, ct, w, out);
   }
   if (small) return mac_kara_go<R, 8, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
-  return mac_kara_go<R, 8, 32, 16, 24, 2, 4, 2>(r, ct, w, out);
+  return mac_kara_go<R, 8, 32, 16, 36, 2, 4, 2>(r, ct, w, out);
 }
 
 void mac(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {

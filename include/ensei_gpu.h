@@ -245,6 +245,82 @@ int ensei_gpu_conv_layer_host(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
                               int in_dtype, uint32_t num_images, const ensei_randomness* rand,
                               void* d_workspace, uint32_t* h_out, void* stream);
 
+/* ---------------------------------------------------------- wire framing */
+/* REF wire format (wire.hpp:17-80, wire.cpp:44-144, protocol.cpp:83-150):
+ *   frame  = "ENSE" | 0x01 | type (1) | payload length (8, LE) | payload
+ *   ciphertext-blocks payload (encode_ct_blocks) = layer (4) | channels (4) |
+ *            blocks (4) | per [channel][block]: domain tag (1) | n (8) |
+ *            c0 (n x 8) | c1 (n x 8), natural slot order
+ *   shares payload (encode_shares) = layer (4) | channels (4) | rows (4) |
+ *            cols (4) | channels x rows x cols residues (8 each)
+ * all little-endian.  The frames are built / parsed by kernels straight from / into
+ * the device layouts above, so a frame never takes a host-side serialisation pass;
+ * `frames` may be device memory or page-locked host memory (read / written in place
+ * across the host link), never pageable memory.  Batched: `num_frames` frames (one
+ * per image session) at a fixed byte stride. */
+#define ENSEI_MSG_HELLO 0x01
+#define ENSEI_MSG_CIPHERTEXT_BLOCKS 0x02
+#define ENSEI_MSG_ALICE_SHARE_CIPHERTEXTS 0x03
+#define ENSEI_MSG_ACTIVATION_SHARE_UP 0x04
+#define ENSEI_MSG_ACTIVATION_SHARE_DOWN 0x05
+#define ENSEI_MSG_DONE 0x06
+#define ENSEI_MSG_ERROR 0x07
+#define ENSEI_DOMAIN_COEFFICIENT 0 /* REF RingDomain::Coefficient (ringbfv.hpp:10) */
+#define ENSEI_DOMAIN_EVALUATION 1  /* REF RingDomain::Evaluation */
+
+/* whole-frame sizes (header included) */
+size_t ensei_gpu_wire_ct_frame_bytes(uint32_t n, uint32_t channels, uint32_t blocks);
+size_t ensei_gpu_wire_share_frame_bytes(uint32_t channels, uint32_t rows, uint32_t cols);
+
+/* encode_frame(encode_ct_blocks(type, layer, cts)) (REF protocol.cpp:83-97,
+ * wire.cpp:44-55,112-117) for num_frames messages of channels x blocks ciphertexts
+ * (single prime).  d_ct[frame][channel][block][2][n]: with domain =
+ * ENSEI_DOMAIN_EVALUATION the polynomials are in device layout (bit-reversed) and
+ * are written in REF's natural slot order; with ENSEI_DOMAIN_COEFFICIENT they are
+ * coefficient-domain polynomials in natural order (REF Baseline-mode ciphertexts,
+ * e.g. after ensei_gpu_negacyclic inverse) and are written as they are. */
+int ensei_gpu_wire_encode_ct_blocks(ensei_gpu_ctx* ctx, uint32_t msg_type, uint32_t layer,
+                                    uint32_t channels, uint32_t blocks, uint32_t domain,
+                                    const uint64_t* d_ct, uint32_t num_frames, uint8_t* frames,
+                                    size_t frame_stride, void* stream);
+
+/* decode_frame + recv_expect + decode_ct_blocks (REF wire.cpp:57-79,119-144,
+ * protocol.cpp:55-65,99-117) of num_frames frames of frame_len bytes each, into
+ * d_ct[frame][channel][block][2][n] in device layout (evaluation domain).  Records
+ * tagged Coefficient (REF Baseline mode) are moved to the evaluation domain on the
+ * way in (REF BobSession's to_evaluation_domain, protocol.cpp:562-566, ringbfv.cpp:
+ * 308-324); *coeff_records (nullable) = how many there were (REF counts 2 ct_ntt
+ * each).  Synchronous on `stream`.  Errors exactly as REF: MalformedPayload (header,
+ * domain tag, ring dimension, coefficient >= q, truncated / trailing bytes),
+ * ProtocolOrderViolation (Error frame from the peer, unexpected type, layout
+ * mismatch); the first violation in REF's read order wins.  layer_out[num_frames]
+ * (nullable, host) receives each frame's layer field. */
+int ensei_gpu_wire_decode_ct_blocks(ensei_gpu_ctx* ctx, const uint8_t* frames, size_t frame_len,
+                                    size_t frame_stride, uint32_t num_frames, uint32_t expect_type,
+                                    uint32_t expect_channels, uint32_t expect_blocks,
+                                    uint32_t* layer_out, uint64_t* d_ct, uint32_t* coeff_records,
+                                    void* stream);
+
+/* encode_frame(encode_shares(type, layer, mats)) (REF protocol.cpp:119-132):
+ * d_shares[frame][channels][rows][cols] uint32 residues -> u64 LE on the wire. */
+int ensei_gpu_wire_encode_shares(ensei_gpu_ctx* ctx, uint32_t msg_type, uint32_t layer,
+                                 uint32_t channels, uint32_t rows, uint32_t cols,
+                                 const uint32_t* d_shares, uint32_t num_frames, uint8_t* frames,
+                                 size_t frame_stride, void* stream);
+
+/* decode_frame + recv_expect + decode_shares (REF protocol.cpp:134-150): values
+ * must be < max_value (<= 2^32; REF passes p_a) else MalformedPayload("share value
+ * out of range").  Synchronous on `stream`. */
+int ensei_gpu_wire_decode_shares(ensei_gpu_ctx* ctx, const uint8_t* frames, size_t frame_len,
+                                 size_t frame_stride, uint32_t num_frames, uint32_t expect_type,
+                                 uint32_t expect_channels, uint32_t expect_rows,
+                                 uint32_t expect_cols, uint64_t max_value, uint32_t* layer_out,
+                                 uint32_t* d_shares, void* stream);
+
+/* Host helper: REF fnv1a (wire.cpp:409-416), the transcript hash RecordingTransport
+ * chains over every encoded frame (wire.cpp:336-352).  `data` is host memory. */
+uint64_t ensei_gpu_fnv1a(const uint8_t* data, size_t len, uint64_t seed);
+
 /* ------------------------------------------------------------ utilities */
 /* number of this library's kernels launched so far in the process */
 uint64_t ensei_gpu_launch_count(void);

@@ -97,7 +97,7 @@ ProtoArgs make_proto(uint64_t p, uint64_t q, uint32_t n, double sigma, int freq_
       LayerWeights bank(d[5], std::vector<Mat>(d[4], Mat(d[1], d[2])));
       for (auto& row : bank)
         for (Mat& m : row)
-          for (auto& v : m.data) v = weights[woff++];
+          for (auto& v : m.data) v = weights ? weights[woff++] : 0;
       a.weights.push_back(std::move(bank));
     } else {
       s.kind = LayerKind::Activation;
@@ -107,7 +107,7 @@ ProtoArgs make_proto(uint64_t p, uint64_t q, uint32_t n, double sigma, int freq_
   }
   for (uint32_t c = 0; c < cin0; ++c) {
     Mat m(H, W);
-    for (size_t i = 0; i < (size_t)H * W; ++i) m.data[i] = image[(size_t)c * H * W + i];
+    for (size_t i = 0; i < (size_t)H * W; ++i) m.data[i] = image ? image[(size_t)c * H * W + i] : 0;
     a.image.push_back(std::move(m));
   }
   return a;
@@ -478,6 +478,119 @@ double ref_bench_negacyclic(uint64_t q, uint32_t n, uint64_t* data, size_t count
     for (auto& th : pool) th.join();
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   } catch (const std::exception& e) { fail(e); return -1.0; }
+}
+
+// ---------------------------------------------------------------- wire framing
+// REF's message layouts through its PUBLIC wire API (ByteWriter / write_ciphertext /
+// encode_frame, decode_frame / ByteReader / read_ciphertext, wire.cpp:44-144); the
+// payload walk is the one of the file-local encode_ct_blocks / decode_ct_blocks /
+// encode_shares / decode_shares and recv_expect (protocol.cpp:55-150).
+static int wire_code(const std::exception& e) {
+  g_err = e.what();
+  if (dynamic_cast<const MalformedPayload*>(&e)) return 14;
+  if (dynamic_cast<const ProtocolOrderViolation*>(&e)) return 12;
+  return -1;
+}
+
+static Frame expect_frame(const uint8_t* bytes, size_t len, uint32_t expect) {
+  Frame f = decode_frame(std::vector<uint8_t>(bytes, bytes + len));
+  if (f.type == MsgType::Error)
+    throw ProtocolOrderViolation("peer aborted: " + std::string(f.payload.begin(), f.payload.end()));
+  if (f.type != static_cast<MsgType>(expect))
+    throw ProtocolOrderViolation(std::string("expected ") + msg_type_name(static_cast<MsgType>(expect)) +
+                                 ", got " + msg_type_name(f.type));
+  return f;
+}
+
+int ref_wire_ct_frame(uint32_t type, uint32_t layer, uint32_t n, uint32_t channels, uint32_t blocks, int tag,
+                      const uint64_t* cts, uint8_t* out, size_t cap, size_t* len) {
+  try {
+    ByteWriter w;
+    w.put_u32(layer);
+    w.put_u32(channels);
+    w.put_u32(channels ? blocks : 0);
+    for (size_t r = 0; r < (size_t)channels * blocks; ++r) {
+      Ciphertext ct;
+      ct.c0.domain = ct.c1.domain = static_cast<RingDomain>(tag);
+      ct.c0.coeffs.assign(cts + 2 * r * n, cts + (2 * r + 1) * n);
+      ct.c1.coeffs.assign(cts + (2 * r + 1) * n, cts + (2 * r + 2) * n);
+      write_ciphertext(w, ct);
+    }
+    Frame f;
+    f.type = static_cast<MsgType>(type);
+    f.payload = std::move(w.buf);
+    std::vector<uint8_t> b = encode_frame(f);
+    *len = b.size();
+    if (b.size() > cap) return -2;
+    std::memcpy(out, b.data(), b.size());
+    return 0;
+  } catch (const std::exception& e) { return wire_code(e); }
+}
+
+int ref_wire_ct_decode(const uint8_t* bytes, size_t len, uint32_t expect, uint64_t p, uint64_t q, uint32_t n,
+                       uint32_t channels, uint32_t blocks, uint32_t* layer, uint64_t* cts, uint8_t* tags) {
+  try {
+    RlweParams prm = make_rlwe_params(n, q, p, 4.0);
+    Frame f = expect_frame(bytes, len, expect);
+    ByteReader r(f.payload);
+    *layer = r.get_u32();
+    uint32_t ch = r.get_u32(), bl = r.get_u32();
+    if (ch != channels || bl != blocks) throw ProtocolOrderViolation("ciphertext block layout mismatch");
+    for (size_t k = 0; k < (size_t)ch * bl; ++k) {
+      Ciphertext ct = read_ciphertext(r, prm);
+      tags[k] = static_cast<uint8_t>(ct.domain());
+      std::memcpy(cts + 2 * k * n, ct.c0.coeffs.data(), 8ull * n);
+      std::memcpy(cts + (2 * k + 1) * n, ct.c1.coeffs.data(), 8ull * n);
+    }
+    r.expect_end();
+    return 0;
+  } catch (const std::exception& e) { return wire_code(e); }
+}
+
+int ref_wire_share_frame(uint32_t type, uint32_t layer, uint32_t channels, uint32_t rows, uint32_t cols,
+                         const uint64_t* v, uint8_t* out, size_t cap, size_t* len) {
+  try {
+    ByteWriter w;
+    w.put_u32(layer);
+    w.put_u32(channels);
+    w.put_u32(channels ? rows : 0);
+    w.put_u32(channels ? cols : 0);
+    for (size_t i = 0; i < (size_t)channels * rows * cols; ++i) w.put_u64(v[i]);
+    Frame f;
+    f.type = static_cast<MsgType>(type);
+    f.payload = std::move(w.buf);
+    std::vector<uint8_t> b = encode_frame(f);
+    *len = b.size();
+    if (b.size() > cap) return -2;
+    std::memcpy(out, b.data(), b.size());
+    return 0;
+  } catch (const std::exception& e) { return wire_code(e); }
+}
+
+int ref_wire_share_decode(const uint8_t* bytes, size_t len, uint32_t expect, uint32_t channels, uint32_t rows,
+                          uint32_t cols, uint64_t max_value, uint32_t* layer, uint64_t* v) {
+  try {
+    Frame f = expect_frame(bytes, len, expect);
+    ByteReader r(f.payload);
+    *layer = r.get_u32();
+    uint32_t ch = r.get_u32(), ro = r.get_u32(), co = r.get_u32();
+    if (ch != channels || ro != rows || co != cols) throw ProtocolOrderViolation("share layout mismatch");
+    for (size_t i = 0; i < (size_t)ch * ro * co; ++i) {
+      uint64_t x = r.get_u64();
+      if (x >= max_value) throw MalformedPayload("share value out of range");
+      v[i] = x;
+    }
+    r.expect_end();
+    return 0;
+  } catch (const std::exception& e) { return wire_code(e); }
+}
+
+uint64_t ref_config_digest(uint64_t p, uint64_t q, uint32_t n, double sigma, int freq_direct, uint64_t seed,
+                           uint32_t H, uint32_t W, uint32_t nlayers, const int32_t* desc) {
+  try {
+    ProtoArgs a = make_proto(p, q, n, sigma, freq_direct, seed, H, W, nlayers, desc, nullptr, nullptr);
+    return config_digest(a.cfg);
+  } catch (const std::exception& e) { fail(e); return 0; }
 }
 
 }  // extern "C"

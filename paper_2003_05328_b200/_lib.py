@@ -100,6 +100,13 @@ def lib():
             "ensei_gpu_conv_host_workspace_bytes": (sz, [vp, C.POINTER(ConvDesc), u32, i32]),
             "ensei_gpu_conv_layer_host": (i32, [vp, C.POINTER(ConvDesc), vp, vp, vp, i32, u32,
                                                 C.POINTER(Randomness), vp, vp, vp]),
+            "ensei_gpu_wire_ct_frame_bytes": (sz, [u32, u32, u32]),
+            "ensei_gpu_wire_share_frame_bytes": (sz, [u32, u32, u32]),
+            "ensei_gpu_wire_encode_ct_blocks": (i32, [vp, u32, u32, u32, u32, u32, vp, u32, vp, sz, vp]),
+            "ensei_gpu_wire_decode_ct_blocks": (i32, [vp, vp, sz, sz, u32, u32, u32, u32, vp, vp, vp, vp]),
+            "ensei_gpu_wire_encode_shares": (i32, [vp, u32, u32, u32, u32, u32, vp, u32, vp, sz, vp]),
+            "ensei_gpu_wire_decode_shares": (i32, [vp, vp, sz, sz, u32, u32, u32, u32, u32, u64, vp, vp, vp]),
+            "ensei_gpu_fnv1a": (u64, [vp, sz, u64]),
             "ensei_gpu_launch_count": (u64, []),
             "ensei_gpu_imad_peak": (C.c_double, [i32]),
         }

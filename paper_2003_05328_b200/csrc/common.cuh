@@ -99,5 +99,9 @@ struct ensei_gpu_ctx {
   cudaGraphExec_t host_graph = nullptr;
   uint64_t host_graph_kernels = 0;  // kernels per replay (for ensei_gpu_launch_count)
   std::vector<uint8_t> host_graph_key;
+  // wire decoding (wire.cu): mapped pinned status block [first-error key, domain flags,
+  // per-record domain tags], grown on demand; read by the host after the decode kernels
+  uint8_t* wire_status = nullptr;
+  size_t wire_status_cap = 0;
 
 };

@@ -97,27 +97,220 @@ class Session:
                 if keep_trace:
                     trace.append({"ct_in": ct, "ct_out": ct_out, "alice": alice, "bob": bob})
             else:
-                imgs, ch = alice.shape[0], alice.shape[1]
-                oh, ow = (h // 2, w // 2) if s.pool2 else (h, w)
-                na = torch.empty((imgs, ch, oh, ow), dtype=torch.int32, device=ctx.device)
-                nb = torch.empty_like(na)
-                flag = torch.zeros(1, dtype=torch.int32, device=ctx.device)
-                rs = r.struct()
-                check(lib().ensei_gpu_activation(ctx.h, s.fn, int(s.pool2), ch, h, w, imgs, ops._ptr(alice),
-                                                 ops._ptr(bob), C.byref(rs), ops._ptr(na), ops._ptr(nb),
-                                                 ops._ptr(flag), ops._stream()))
-                if s.fn == 1 and int(flag.item()):
-                    raise RangeOverflow("square activation exceeds p_a/2")
-                alice, bob = na, nb
-                h, w = oh, ow
+                alice, bob, h, w = self.activation(s, alice, bob, h, w, r)
                 if li + 1 == len(self.schedule):
                     out = self._recombine(alice, bob)
         if out is None:
             out = self._recombine(alice, bob)
         return (out, trace) if keep_trace else out
 
+    def activation(self, s: Act, alice: torch.Tensor, bob: torch.Tensor, h: int, w: int, r: ops.Randomness):
+        """trusted_activation (REF protocol.cpp:237-268) on the device; returns the fresh
+        shares (Alice's, Bob's) and the new spatial size."""
+        ctx = self.ctx
+        imgs, ch = alice.shape[0], alice.shape[1]
+        oh, ow = (h // 2, w // 2) if s.pool2 else (h, w)
+        na = torch.empty((imgs, ch, oh, ow), dtype=torch.int32, device=ctx.device)
+        nb = torch.empty_like(na)
+        flag = torch.zeros(1, dtype=torch.int32, device=ctx.device)
+        rs = r.struct()
+        check(lib().ensei_gpu_activation(ctx.h, s.fn, int(s.pool2), ch, h, w, imgs, ops._ptr(alice),
+                                         ops._ptr(bob), C.byref(rs), ops._ptr(na), ops._ptr(nb),
+                                         ops._ptr(flag), ops._stream()))
+        if s.fn == 1 and int(flag.item()):
+            raise RangeOverflow("square activation exceeds p_a/2")
+        return na, nb, oh, ow
+
     def _recombine(self, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
         out = torch.empty_like(a)
         check(lib().ensei_gpu_recombine(self.ctx.h, ops._ptr(a), ops._ptr(b), a.numel(), ops._ptr(out),
                                         ops._stream()))
         return out
+
+
+# --------------------------------------------------------------------------- wire
+# The two parties as REF runs them (AliceSession::run / BobSession::run,
+# protocol.cpp:276-640): every conv and activation step exchanges REF-format frames
+# (paper_2003_05328_b200/wire.py) over a Transport, one transport per image session.
+# Ciphertext / share frames are built and parsed by the wire kernels; the counters
+# are REF's logical TransformCounters (counters.hpp:17-31) for one session.
+
+@dataclass
+class PartyResult:
+    """REF PartyResult (protocol.hpp): output (Alice), counters, transcripts."""
+    output: Optional[torch.Tensor]
+    counters: dict
+    transcripts: list
+
+
+def _counters():
+    return {"ct_ntt": 0, "ring_ntt": 0, "image_ntt": 0, "hadamard": 0}
+
+
+def _sync():
+    torch.cuda.current_stream().synchronize()
+
+
+def _hello(transports, digest: int, first: bool):
+    from . import wire as Wr
+    import struct
+    if first:
+        for t in transports:
+            t.send_frame(Wr.hello_frame(digest))
+    peers = [struct.unpack("<Q", Wr.expect_host(t.recv_frame(), Wr.HELLO))[0] for t in transports]
+    if not first:
+        for t in transports:
+            t.send_frame(Wr.hello_frame(digest))
+    if any(d != digest for d in peers):
+        for t in transports:
+            try:
+                t.send_frame(Wr.error_frame("configuration digest mismatch"))
+            except Exception:
+                pass
+        raise Wr.ProtocolOrderViolation("configuration digest mismatch")
+
+
+def run_alice(sess: Session, key: torch.Tensor, x: torch.Tensor, rands: Sequence[ops.Randomness],
+              transports, digest: int, freq_direct: bool = True, key_stride: int = 0) -> PartyResult:
+    """AliceSession::run (REF protocol.cpp:358-437) for x.shape[0] image sessions."""
+    from . import wire as Wr
+    ctx, n = sess.ctx, sess.ctx.n
+    from ._lib import LAYOUT_BITREV
+    T = [Wr.RecordingTransport(t) for t in transports]
+    _hello(T, digest, first=True)
+    cnt = _counters()
+    alice, bob = x, None
+    h, w = sess.H, sess.W
+    out = None
+    for li, s in enumerate(sess.schedule):
+        r = rands[li]
+        if isinstance(s, Conv):
+            lo = sess.layers[li]
+            B = lo.B
+            ct = lo.alice_encrypt(key, alice.contiguous(), r, key_stride=key_stride)
+            cnt["image_ntt"] += s.cin
+            cnt["ring_ntt"] += s.cin * B * (2 if freq_direct else 3)
+            if not freq_direct:  # REF encrypt (Baseline): coefficient-domain ciphertexts
+                ctx.negacyclic(ct.view(-1, n), 0, inverse=True, layout=LAYOUT_BITREV)
+            frames = Wr.encode_ct_blocks(ctx, Wr.CIPHERTEXT_BLOCKS, li, ct,
+                                         Wr.EVALUATION if freq_direct else Wr.COEFFICIENT)
+            _sync()
+            for i, t in enumerate(T):
+                t.send_frame(frames[i])
+            got = Wr.gather_frames([t.recv_frame() for t in T])
+            ct_out, _, ncoef = Wr.decode_ct_blocks(ctx, got, Wr.ALICE_SHARE_CIPHERTEXTS, s.cout, B)
+            alice = lo.alice_decrypt(key, ct_out, key_stride=key_stride)
+            cnt["ring_ntt"] += s.cout * B * 2 + ncoef // max(len(T), 1)  # Coefficient decrypt: +1 forward
+            cnt["image_ntt"] += s.cout
+            h, w = lo.geom.oh, lo.geom.ow
+        else:
+            got = Wr.gather_frames([t.recv_frame() for t in T])
+            bob, _ = Wr.decode_shares(ctx, got, Wr.ACTIVATION_SHARE_UP, alice.shape[1], h, w, ctx.p)
+            alice, nb, h, w = sess.activation(s, alice, bob, h, w, r)
+            if li + 1 == len(sess.schedule):
+                out = sess._recombine(alice, nb)
+            else:
+                frames = Wr.encode_shares(ctx, Wr.ACTIVATION_SHARE_DOWN, li, nb)
+                _sync()
+                for i, t in enumerate(T):
+                    t.send_frame(frames[i])
+    if isinstance(sess.schedule[-1], Conv):  # Bob uploads his share of the last conv
+        got = Wr.gather_frames([t.recv_frame() for t in T])
+        bob, _ = Wr.decode_shares(ctx, got, Wr.ACTIVATION_SHARE_UP, alice.shape[1], h, w, ctx.p)
+        out = sess._recombine(alice, bob)
+    for t in T:
+        t.send_frame(Wr.done_frame())
+    for t in T:
+        Wr.expect_host(t.recv_frame(), Wr.DONE)
+    return PartyResult(out, cnt, [t.transcript for t in T])
+
+
+def run_bob(sess: Session, rands: Sequence[ops.Randomness], transports, digest: int) -> PartyResult:
+    """BobSession::run (REF protocol.cpp:521-640) for len(transports) image sessions."""
+    from . import wire as Wr
+    ctx = sess.ctx
+    T = [Wr.RecordingTransport(t) for t in transports]
+    _hello(T, digest, first=False)
+    cnt = _counters()
+    mine = None
+    li_last = len(sess.schedule) - 1
+    for li, s in enumerate(sess.schedule):
+        r = rands[li]
+        if isinstance(s, Conv):
+            lo = sess.layers[li]
+            B = lo.B
+            got = Wr.gather_frames([t.recv_frame() for t in T])
+            ct, _, ncoef = Wr.decode_ct_blocks(ctx, got, Wr.CIPHERTEXT_BLOCKS, s.cin, B)
+            per = ncoef // max(len(T), 1)  # to_evaluation_domain: 2 ring transforms, ct_ntt += 2
+            cnt["ct_ntt"] += 2 * per
+            cnt["ring_ntt"] += 2 * per
+            if mine is not None:  # HomRec (REF protocol.cpp:543-557)
+                cnt["image_ntt"] += s.cin
+                cnt["ring_ntt"] += 2 * s.cin * B
+            ct_out, mine = lo.bob_eval(ct, sess.w_eval[li], r, bob_prev=mine)
+            cnt["hadamard"] += s.cin * s.cout * B
+            cnt["ring_ntt"] += 2 * s.cout * B
+            cnt["image_ntt"] += s.cout
+            frames = Wr.encode_ct_blocks(ctx, Wr.ALICE_SHARE_CIPHERTEXTS, li, ct_out, Wr.EVALUATION)
+            _sync()
+            for i, t in enumerate(T):
+                t.send_frame(frames[i])
+        else:
+            frames = Wr.encode_shares(ctx, Wr.ACTIVATION_SHARE_UP, li, mine)
+            _sync()
+            for i, t in enumerate(T):
+                t.send_frame(frames[i])
+            if li != li_last:
+                got = Wr.gather_frames([t.recv_frame() for t in T])
+                mine, _ = Wr.decode_shares(ctx, got, Wr.ACTIVATION_SHARE_DOWN, mine.shape[1], mine.shape[2],
+                                           mine.shape[3], ctx.p)
+    if isinstance(sess.schedule[-1], Conv):
+        frames = Wr.encode_shares(ctx, Wr.ACTIVATION_SHARE_UP, li_last, mine)
+        _sync()
+        for i, t in enumerate(T):
+            t.send_frame(frames[i])
+    for t in T:
+        Wr.expect_host(t.recv_frame(), Wr.DONE)
+    for t in T:
+        t.send_frame(Wr.done_frame())
+    return PartyResult(None, cnt, [t.transcript for t in T])
+
+
+def run_inproc(sess: Session, key: torch.Tensor, x: torch.Tensor, rand: Callable[[int], ops.Randomness],
+               seed: int, freq_direct: bool = True, key_stride: int = 0, sigma: float = 4.0):
+    """REF run_inproc (protocol.cpp:670-692): Bob on a thread, Alice on the caller, one
+    in-process transport pair per image session.  Returns (alice, bob) PartyResults."""
+    import threading
+    from . import wire as Wr
+    rands = [rand(li) for li in range(len(sess.schedule))]  # REF Rng consumption is per party, in layer order
+    ctx = sess.ctx
+    digest = Wr.config_digest(ctx.n, ctx.q[0], ctx.p, seed, sess.H, sess.W, sess.schedule, freq_direct, sigma)
+    pairs = [Wr.make_inproc_pair() for _ in range(x.shape[0])]
+    res, err = {}, {}
+    dev = torch.cuda.current_device()
+
+    def bob():
+        try:
+            torch.cuda.set_device(dev)
+            res["bob"] = run_bob(sess, rands, [p[1] for p in pairs], digest)
+        except BaseException as e:  # noqa: BLE001 -- re-raised on the caller
+            err["bob"] = e
+        finally:
+            for p in pairs:
+                p[1].close()
+
+    th = threading.Thread(target=bob, daemon=True)
+    th.start()
+    try:
+        res["alice"] = run_alice(sess, key, x, rands, [p[0] for p in pairs], digest, freq_direct, key_stride)
+    except BaseException as e:  # noqa: BLE001
+        err["alice"] = e
+    finally:
+        for p in pairs:
+            p[0].close()
+    th.join()
+    if "alice" in err:
+        raise err["alice"]
+    if "bob" in err:
+        raise err["bob"]
+    return res["alice"], res["bob"]

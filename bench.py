@@ -431,6 +431,43 @@ def main():
             del buf, c2
         torch.cuda.empty_cache()
 
+    # ---- wire framing side measurement: the step's AliceShareCiphertexts frames
+    # (imgs x 16 channels x 2 blocks records, REF wire layout) built from / parsed into
+    # the device layout, device-resident frames (HBM roofline) and page-locked host frames.
+    wire = None
+    if rank == 0:
+        from paper_2003_05328_b200 import wire as Wr
+        fb = Wr.ct_frame_bytes(2048, 16, g.blocks)
+        ct_out.copy_((ct_out.view(torch.int64).abs() % Q).view(torch.uint64))
+        fr_dev = torch.empty((imgs, fb), dtype=torch.uint8, device=dev)
+        fr_host = Wr.pinned_frames(imgs, fb)
+        ct_back = torch.empty_like(ct_out)
+        wire = {"frame_bytes": fb, "frames": imgs}
+        for name, fn in (("encode_device", lambda: Wr.encode_ct_blocks(ctx, Wr.ALICE_SHARE_CIPHERTEXTS, 0, ct_out,
+                                                                         out=fr_dev)),
+                         ("decode_device", lambda: Wr.decode_ct_blocks(ctx, fr_dev, Wr.ALICE_SHARE_CIPHERTEXTS, 16,
+                                                                         g.blocks, out=ct_back)),
+                         ("encode_pinned_host", lambda: Wr.encode_ct_blocks(ctx, Wr.ALICE_SHARE_CIPHERTEXTS, 0,
+                                                                              ct_out, out=fr_host)),
+                         ("decode_pinned_host", lambda: Wr.decode_ct_blocks(ctx, fr_host, Wr.ALICE_SHARE_CIPHERTEXTS,
+                                                                              16, g.blocks, out=ct_back))):
+            for _ in range(3):
+                fn()
+            acc = []
+            for _ in range(10):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                b.synchronize()
+                acc.append(a.elapsed_time(b))
+            ms = statistics.median(acc)
+            nbytes = imgs * fb + ct_out.numel() * 8  # read one side, write the other
+            wire[name] = {"ms": ms, "GB_s": nbytes / (ms / 1e3) / 1e9,
+                          "hbm_frac": nbytes / (ms / 1e3) / 1e9 / hbm_peak if "device" in name else None}
+        assert torch.equal(ct_back, ct_out)
+
     # ---- CPU baseline (reference, bounded sample, rank 0)
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -460,6 +497,7 @@ def main():
             "roofline": roofline,
             "modmul_per_s": total_modmul * world * args.steps / (total_ms / 1e3),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk, "ntt_config2": ntt,
+            "wire": wire,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -245,6 +245,43 @@ int ensei_gpu_conv_layer_host(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
                               int in_dtype, uint32_t num_images, const ensei_randomness* rand,
                               void* d_workspace, uint32_t* h_out, void* stream);
 
+/* ------------------------------------------------------------ parameters */
+/* REF PrecisionProfile (params.hpp:11-17) */
+typedef struct {
+  int32_t input_bits, filter_bits, f_h, f_w;
+} ensei_precision_profile;
+
+#define ENSEI_CHAIN_UNIFIED 0     /* REF ChainMode::Unified */
+#define ENSEI_CHAIN_SPLIT_PAPER 1 /* REF ChainMode::SplitPaper */
+
+/* REF ParamSet (params.hpp:27-34): ModulusChain + RlweParams moduli.  num_q = 1 is
+ * REF's single-prime q; num_q > 1 is the RNS extension (q = product of q[0..num_q)). */
+typedef struct {
+  uint64_t p_n, p_a, p_e;
+  uint32_t n, num_q;
+  uint64_t q[ENSEI_MAX_PRIMES];
+  double sigma;
+  double log2_q_min; /* derive_q's requirement (REF params.cpp:49-60), log2 */
+  uint32_t mode, insecure;
+  ensei_precision_profile profile;
+} ensei_param_set;
+
+/* min_pntt (REF params.cpp:79-89); ENSEI_ERR_RANGE_VIOLATION as REF */
+int ensei_gpu_min_pntt(const ensei_precision_profile* profile, uint64_t* out);
+
+/* build_params (REF params.cpp:91-117) + derive_q.  max_primes = 1 reproduces REF
+ * exactly (ENSEI_ERR_SEARCH_EXHAUSTED when q would reach 2^62, e.g. >= ~100-way channel
+ * accumulation at n = 2048); max_primes > 1 switches to an RNS chain of the smallest
+ * primes >= 2^59 that are == 1 (mod 2n p_e) when -- and only when -- REF's single
+ * prime runs out (min_primes forces at least that many RNS primes). */
+int ensei_gpu_build_params(const ensei_precision_profile* profile, uint32_t n, uint32_t mode,
+                           uint64_t accum_channels, uint64_t p_n_floor, double sigma,
+                           uint32_t max_primes, uint32_t min_primes, ensei_param_set* out);
+
+/* preset_params (REF params.cpp:119-144): "binary", "medium", "high", "toy" */
+int ensei_gpu_preset_params(const char* name, uint64_t accum_channels, uint32_t max_primes,
+                            ensei_param_set* out);
+
 /* ---------------------------------------------------------- wire framing */
 /* REF wire format (wire.hpp:17-80, wire.cpp:44-144, protocol.cpp:83-150):
  *   frame  = "ENSE" | 0x01 | type (1) | payload length (8, LE) | payload

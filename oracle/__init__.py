@@ -150,6 +150,10 @@ def ref():
             "ref_wire_share_frame": (C.c_int, [U32, U32, U32, U32, U32, u64p, vp, C.c_size_t,
                                                C.POINTER(C.c_size_t)]),
             "ref_wire_share_decode": (C.c_int, [vp, C.c_size_t, U32, U32, U32, U32, U64, C.POINTER(U32), u64p]),
+            "ref_min_pntt": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(U64)]),
+            "ref_build_params": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, U32, C.c_int, U64, U64, C.c_double,
+                                           u64p]),
+            "ref_preset_params": (C.c_int, [C.c_char_p, U64, u64p]),
             "ref_config_digest": (U64, [U64, U64, U32, C.c_double, C.c_int, U64, U32, U32, U32, i32p]),
         }
         for name, (res, args) in sig.items():

@@ -593,4 +593,45 @@ uint64_t ref_config_digest(uint64_t p, uint64_t q, uint32_t n, double sigma, int
   } catch (const std::exception& e) { fail(e); return 0; }
 }
 
+// ------------------------------------------------------------------ parameters
+static int param_code(const std::exception& e) {
+  g_err = e.what();
+  if (dynamic_cast<const SearchExhausted*>(&e)) return 3;
+  if (dynamic_cast<const RangeViolation*>(&e)) return 11;
+  if (dynamic_cast<const ChainViolation*>(&e)) return 9;
+  return 1;
+}
+
+static void put_params(const ParamSet& ps, uint64_t* out) {
+  out[0] = ps.chain.p_n.modulus();
+  out[1] = ps.chain.p_a.modulus();
+  out[2] = ps.chain.p_e.modulus();
+  out[3] = ps.rlwe.q.modulus();
+  out[4] = ps.rlwe.n;
+  out[5] = ps.insecure ? 1 : 0;
+}
+
+int ref_min_pntt(int ib, int fb, int fh, int fw, uint64_t* out) {
+  try {
+    *out = min_pntt(PrecisionProfile{ib, fb, fh, fw});
+    return 0;
+  } catch (const std::exception& e) { return param_code(e); }
+}
+
+int ref_build_params(int ib, int fb, int fh, int fw, uint32_t n, int split, uint64_t accum, uint64_t floor_,
+                     double sigma, uint64_t* out) {
+  try {
+    put_params(build_params(PrecisionProfile{ib, fb, fh, fw}, n, split ? ChainMode::SplitPaper : ChainMode::Unified,
+                            accum, floor_, sigma), out);
+    return 0;
+  } catch (const std::exception& e) { return param_code(e); }
+}
+
+int ref_preset_params(const char* name, uint64_t accum, uint64_t* out) {
+  try {
+    put_params(preset_params(name, accum), out);
+    return 0;
+  } catch (const std::exception& e) { return param_code(e); }
+}
+
 }  // extern "C"

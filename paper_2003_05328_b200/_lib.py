@@ -60,6 +60,17 @@ class Randomness(C.Structure):
                 ("d_noise", C.c_void_p), ("d_a_hat", C.c_void_p), ("d_share", C.c_void_p)]
 
 
+class PrecisionProfile(C.Structure):
+    _fields_ = [("input_bits", C.c_int32), ("filter_bits", C.c_int32), ("f_h", C.c_int32), ("f_w", C.c_int32)]
+
+
+class ParamSet(C.Structure):
+    _fields_ = [("p_n", C.c_uint64), ("p_a", C.c_uint64), ("p_e", C.c_uint64), ("n", C.c_uint32),
+                ("num_q", C.c_uint32), ("q", C.c_uint64 * ENSEI_MAX_PRIMES), ("sigma", C.c_double),
+                ("log2_q_min", C.c_double), ("mode", C.c_uint32), ("insecure", C.c_uint32),
+                ("profile", PrecisionProfile)]
+
+
 _lib = None
 
 
@@ -107,6 +118,10 @@ def lib():
             "ensei_gpu_wire_encode_shares": (i32, [vp, u32, u32, u32, u32, u32, vp, u32, vp, sz, vp]),
             "ensei_gpu_wire_decode_shares": (i32, [vp, vp, sz, sz, u32, u32, u32, u32, u32, u64, vp, vp, vp]),
             "ensei_gpu_fnv1a": (u64, [vp, sz, u64]),
+            "ensei_gpu_min_pntt": (i32, [C.POINTER(PrecisionProfile), C.POINTER(u64)]),
+            "ensei_gpu_build_params": (i32, [C.POINTER(PrecisionProfile), u32, u32, u64, u64, C.c_double, u32, u32,
+                                             C.POINTER(ParamSet)]),
+            "ensei_gpu_preset_params": (i32, [C.c_char_p, u64, u32, C.POINTER(ParamSet)]),
             "ensei_gpu_launch_count": (u64, []),
             "ensei_gpu_imad_peak": (C.c_double, [i32]),
         }

@@ -8,6 +8,7 @@ and streams; every operation runs in libensei_gpu.so kernels.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 from dataclasses import dataclass
 
 import torch
@@ -40,6 +41,7 @@ def mix64(x: int) -> int:
     return x ^ (x >> 31)
 
 
+@functools.lru_cache(maxsize=256)
 def fork_seed(seed: int, salt: int) -> int:
     """Rng(seed).fork(salt) seed derivation (REF modfield.cpp:221-223)."""
     return mix64(seed ^ mix64(salt))
@@ -134,6 +136,10 @@ class Randomness:
         self.noise, self.a_hat, self.share = noise, a_hat, share
 
     def struct(self) -> Randomness_:
+        # cached per field values: a hot host-entry loop re-passes the same randomness
+        k = (self.seed, self.layer, self.image_base, self.cbd_k, _tid(self.noise), _tid(self.a_hat), _tid(self.share))
+        if getattr(self, "_key", None) == k:
+            return self._struct
         inj = self.noise is not None or self.a_hat is not None or self.share is not None
         r = Randomness_()
         r.mode = RAND_INJECTED if inj else RAND_PHILOX
@@ -143,7 +149,12 @@ class Randomness:
         r.d_noise = None if self.noise is None else self.noise.data_ptr()
         r.d_a_hat = None if self.a_hat is None else self.a_hat.data_ptr()
         r.d_share = None if self.share is None else self.share.data_ptr()
+        self._key, self._struct = k, r
         return r
+
+
+def _tid(t):
+    return None if t is None else (id(t), t.data_ptr())
 
 
 Randomness_ = _lib.Randomness
@@ -241,13 +252,19 @@ class LayerOps:
         return (out, a, b) if want_shares else out
 
     def forward_host(self, key, w_eval, h_x: torch.Tensor, rand: Randomness, ws, h_out: torch.Tensor, stream=None):
-        """Host-buffer entry point (pinned h_x / h_out): H2D, layer, D2H, synchronous."""
-        images = h_x.shape[0]
-        in_t = IN_U8 if h_x.dtype == torch.uint8 else IN_U32
+        """Host-buffer entry point (pinned h_x / h_out): H2D, layer, D2H, synchronous.
+        The marshalled ctypes arguments are cached while the buffers are unchanged."""
         r = rand.struct()
-        check(lib().ensei_gpu_conv_layer_host(self.ctx.h, C.byref(self.d), _ptr(key), _ptr(w_eval),
-                                              C.c_void_p(h_x.data_ptr()), in_t, images, C.byref(r), _ptr(ws),
-                                              C.c_void_p(h_out.data_ptr()), _stream(stream)))
+        st = (stream if stream is not None else torch.cuda.current_stream()).cuda_stream
+        k = (key.data_ptr(), w_eval.data_ptr(), h_x.data_ptr(), h_x.dtype, h_x.shape[0], id(r), ws.data_ptr(),
+             h_out.data_ptr(), st)
+        if getattr(self, "_host_key", None) != k:
+            in_t = IN_U8 if h_x.dtype == torch.uint8 else IN_U32
+            self._host_args = (self.ctx.h, C.byref(self.d), _ptr(key), _ptr(w_eval), C.c_void_p(h_x.data_ptr()),
+                               in_t, h_x.shape[0], C.byref(r), _ptr(ws), C.c_void_p(h_out.data_ptr()),
+                               C.c_void_p(st))
+            self._host_key = k
+        check(lib().ensei_gpu_conv_layer_host(*self._host_args))
         return h_out
 
 

@@ -245,6 +245,20 @@ int ensei_gpu_conv_layer_host(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
                               int in_dtype, uint32_t num_images, const ensei_randomness* rand,
                               void* d_workspace, uint32_t* h_out, void* stream);
 
+/* --------------------------------------------------- reference randomness */
+/* REF Rng (modfield.hpp:104-130, modfield.cpp:198-223) on the host: mt19937_64,
+ * fork(salt) = Rng(mix64(seed ^ mix64(salt))) (AliceSession salt 0xA11CE, BobSession
+ * 0xB0B, protocol.cpp:285,454), masked-rejection uniform_below, 6-sigma-tail discrete
+ * Gaussian.  Feeding its draws, in REF's consumption order, through
+ * ensei_randomness's injected pointers reproduces the reference bit for bit. */
+typedef struct ensei_ref_rng ensei_ref_rng;
+int ensei_gpu_ref_rng_create(uint64_t seed, int use_fork, uint64_t salt, ensei_ref_rng** out);
+void ensei_gpu_ref_rng_destroy(ensei_ref_rng* rng);
+int ensei_gpu_ref_rng_next_u64(ensei_ref_rng* rng, uint64_t* h_out, size_t count);
+int ensei_gpu_ref_rng_uniform_below(ensei_ref_rng* rng, uint64_t bound, uint64_t* h_out,
+                                    size_t count);
+int ensei_gpu_ref_rng_gaussian(ensei_ref_rng* rng, double sigma, int64_t* h_out, size_t count);
+
 /* ------------------------------------------------------------ parameters */
 /* REF PrecisionProfile (params.hpp:11-17) */
 typedef struct {

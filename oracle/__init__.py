@@ -154,6 +154,7 @@ def ref():
             "ref_build_params": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, U32, C.c_int, U64, U64, C.c_double,
                                            u64p]),
             "ref_preset_params": (C.c_int, [C.c_char_p, U64, u64p]),
+            "ref_random_weights": (C.c_int, [U32, i32p, C.c_int64, U64, C.c_int, U64, i64p]),
             "ref_config_digest": (U64, [U64, U64, U32, C.c_double, C.c_int, U64, U32, U32, U32, i32p]),
         }
         for name, (res, args) in sig.items():

@@ -634,4 +634,20 @@ int ref_preset_params(const char* name, uint64_t accum, uint64_t* out) {
   } catch (const std::exception& e) { return param_code(e); }
 }
 
+// REF random_weights (protocol.cpp:752-767) with Rng(seed) or Rng(seed).fork(salt)
+int ref_random_weights(uint32_t nlayers, const int32_t* desc, int64_t magnitude, uint64_t seed, int use_fork,
+                       uint64_t salt, int64_t* out) {
+  try {
+    ProtoArgs a = make_proto(638977, 576460803525083137ull, 2048, 4.0, 1, 0, 8, 8, nlayers, desc, nullptr, nullptr);
+    Rng r = use_fork ? Rng(seed).fork(salt) : Rng(seed);
+    NetworkWeights w = random_weights(a.cfg.schedule, magnitude, r);
+    size_t k = 0;
+    for (auto& bank : w)
+      for (auto& row : bank)
+        for (Mat& m : row)
+          for (int64_t v : m.data) out[k++] = v;
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
 }  // extern "C"

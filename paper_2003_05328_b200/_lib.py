@@ -118,6 +118,11 @@ def lib():
             "ensei_gpu_wire_encode_shares": (i32, [vp, u32, u32, u32, u32, u32, vp, u32, vp, sz, vp]),
             "ensei_gpu_wire_decode_shares": (i32, [vp, vp, sz, sz, u32, u32, u32, u32, u32, u64, vp, vp, vp]),
             "ensei_gpu_fnv1a": (u64, [vp, sz, u64]),
+            "ensei_gpu_ref_rng_create": (i32, [u64, i32, u64, C.POINTER(vp)]),
+            "ensei_gpu_ref_rng_destroy": (None, [vp]),
+            "ensei_gpu_ref_rng_next_u64": (i32, [vp, vp, sz]),
+            "ensei_gpu_ref_rng_uniform_below": (i32, [vp, u64, vp, sz]),
+            "ensei_gpu_ref_rng_gaussian": (i32, [vp, C.c_double, vp, sz]),
             "ensei_gpu_min_pntt": (i32, [C.POINTER(PrecisionProfile), C.POINTER(u64)]),
             "ensei_gpu_build_params": (i32, [C.POINTER(PrecisionProfile), u32, u32, u64, u64, C.c_double, u32, u32,
                                              C.POINTER(ParamSet)]),

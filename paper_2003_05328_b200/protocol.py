@@ -151,17 +151,20 @@ def _sync():
     torch.cuda.current_stream().synchronize()
 
 
-def _hello(transports, digest: int, first: bool):
+def _hello(transports, digest, first: bool):
+    """Hello exchange (REF AliceSession/BobSession::hello, protocol.cpp:292-308, 504-519);
+    `digest` is one config digest per session (or one for all)."""
     from . import wire as Wr
     import struct
+    ds = list(digest) if isinstance(digest, (list, tuple)) else [digest] * len(transports)
     if first:
-        for t in transports:
-            t.send_frame(Wr.hello_frame(digest))
+        for t, d in zip(transports, ds):
+            t.send_frame(Wr.hello_frame(d))
     peers = [struct.unpack("<Q", Wr.expect_host(t.recv_frame(), Wr.HELLO))[0] for t in transports]
     if not first:
-        for t in transports:
-            t.send_frame(Wr.hello_frame(digest))
-    if any(d != digest for d in peers):
+        for t, d in zip(transports, ds):
+            t.send_frame(Wr.hello_frame(d))
+    if any(p != d for p, d in zip(peers, ds)):
         for t in transports:
             try:
                 t.send_frame(Wr.error_frame("configuration digest mismatch"))
@@ -277,14 +280,17 @@ def run_bob(sess: Session, rands: Sequence[ops.Randomness], transports, digest: 
 
 
 def run_inproc(sess: Session, key: torch.Tensor, x: torch.Tensor, rand: Callable[[int], ops.Randomness],
-               seed: int, freq_direct: bool = True, key_stride: int = 0, sigma: float = 4.0):
+               seed, freq_direct: bool = True, key_stride: int = 0, sigma: float = 4.0):
     """REF run_inproc (protocol.cpp:670-692): Bob on a thread, Alice on the caller, one
-    in-process transport pair per image session.  Returns (alice, bob) PartyResults."""
+    in-process transport pair per image session.  `seed` is the sessions' config seed
+    (one int, or one per image: it enters the Hello digest).  Returns (alice, bob)."""
     import threading
     from . import wire as Wr
     rands = [rand(li) for li in range(len(sess.schedule))]  # REF Rng consumption is per party, in layer order
     ctx = sess.ctx
-    digest = Wr.config_digest(ctx.n, ctx.q[0], ctx.p, seed, sess.H, sess.W, sess.schedule, freq_direct, sigma)
+    seeds = list(seed) if isinstance(seed, (list, tuple)) else [seed] * x.shape[0]
+    digest = [Wr.config_digest(ctx.n, ctx.q[0], ctx.p, s, sess.H, sess.W, sess.schedule, freq_direct, sigma)
+              for s in seeds]
     pairs = [Wr.make_inproc_pair() for _ in range(x.shape[0])]
     res, err = {}, {}
     dev = torch.cuda.current_device()

@@ -306,3 +306,79 @@ def test_wire_session_batched_philox(W, ops):
     assert (to_np(alice.output) == to_np(direct)).all()
     hs = {t.content_hash_sent for t in alice.transcripts}
     assert len(hs) == 4  # four distinct sessions
+
+
+def _ref_run(seed, H, Wd, desc, img, ws, mode=1, n=2048):
+    hashes = np.zeros(6, np.uint64)
+    h, w, ch = H, Wd, desc[0][4]
+    for d in desc:
+        if d[0] == 0:
+            h, w, ch = (h if d[3] else h - d[1] + 1), (w if d[3] else w - d[2] + 1), d[5]
+    out = np.zeros(ch * h * w, np.uint64)
+    O.ref_check(O.ref().ref_run_protocol(P, Q, n, 4.0, mode, seed, H, Wd, len(desc),
+                                         np.array(desc, np.int32).reshape(-1), img.reshape(-1).astype(np.int64),
+                                         np.concatenate([x.reshape(-1) for x in ws]).astype(np.int64), out,
+                                         hashes.ctypes.data, None, 0, None, None, None, None))
+    return out, hashes
+
+
+@pytest.mark.parametrize("idx", [1, 2])
+def test_product_parity_mode_from_json_schedule(W, ops, golden, idx):
+    """Product-only REF-compatible run: a JSON schedule (schedule.py), REF's fixture draws
+    and per-party streams from the product's RefRng (refrand.py), frames over transports:
+    the transcripts equal the reference's golden ones -- no oracle code on this path."""
+    import json
+    from paper_2003_05328_b200 import protocol as GP
+    from paper_2003_05328_b200 import refrand as RR
+    from paper_2003_05328_b200 import schedule as S
+    case = golden["proto"][idx]
+    layers = [{"kind": "conv", "filter_h": d[1], "filter_w": d[2], "conv_type": "same" if d[3] else "valid",
+               "channels_in": d[4], "channels_out": d[5]} if d[0] == 0 else {"kind": "activation",
+                                                                                "fn": S.FN_NAME[d[6]]}
+              for d in case["desc"]]
+    sf = S.parse_schedule(json.dumps({"layers": layers}))
+    H, Wd, n = case["H"], case["W"], case["n"]
+    g = RR.RefRng(case["seed"], 0xDA7A)
+    cin = sf.schedule[0].cin
+    img = g.uniform_below(256, cin * H * Wd).astype(np.int64).reshape(cin, H, Wd)
+    ws = [(g.uniform_below(256, s.cout * s.cin * s.fh * s.fw).astype(np.int64) - 128).reshape(s.cout, s.cin, s.fh,
+                                                                                               s.fw)
+          for s in sf.schedule if isinstance(s, GP.Conv)]
+    ctx = ctx_for(ops, n)
+    sess = GP.Session(ctx, sf.schedule, H, Wd, [torch.from_numpy(w.astype(np.int32)) for w in ws])
+    sr = RR.SessionRandomness(ctx, [case["seed"]])
+    key = sr.keys()[0]
+    x = torch.from_numpy(img.astype(np.int32)[None]).to(dev())
+    alice, bob = GP.run_inproc(sess, key, x, sr.for_session(sess), seed=case["seed"], freq_direct=bool(case["mode"]))
+    ta = alice.transcripts[0]
+    assert "%016x" % ta.content_hash_sent == case["alice_sent"]
+    assert "%016x" % ta.content_hash_recv == case["alice_recv"]
+    assert fnv(to_np(alice.output).astype(np.uint64).reshape(-1)) == case["out_fnv"]
+
+
+def test_product_parity_mode_batched_sessions(W, ops):
+    """Three image sessions with their own seeds and keys in one batched run (key_stride):
+    every session's transcripts and output equal an independent reference run."""
+    from paper_2003_05328_b200 import protocol as GP
+    from paper_2003_05328_b200 import refrand as RR
+    desc = [[0, 3, 3, 1, 2, 3, 0], [1, 0, 0, 0, 0, 0, 1], [0, 1, 1, 0, 3, 2, 0]]
+    sched = [GP.Conv(3, 3, True, 2, 3), GP.Act(1), GP.Conv(1, 1, False, 3, 2)]
+    H = Wd = 8
+    ctx = ctx_for(ops, 2048)
+    rng = np.random.default_rng(77)
+    imgs = rng.integers(0, 4, size=(3, 2, H, Wd)).astype(np.int64)  # small: keeps Square in range
+    ws = [rng.integers(-2, 3, size=(3, 2, 3, 3)).astype(np.int64), rng.integers(-2, 3, size=(2, 3, 1, 1))]
+    seeds = [101, 5, 999]
+    sess = GP.Session(ctx, sched, H, Wd, [torch.from_numpy(w.astype(np.int32)) for w in ws])
+    sr = RR.SessionRandomness(ctx, seeds)
+    keys = sr.keys()
+    x = torch.from_numpy(imgs.astype(np.int32)).to(dev())
+    alice, bob = GP.run_inproc(sess, keys, x, sr.for_session(sess), seed=seeds, key_stride=keys.shape[1])
+    out = to_np(alice.output).astype(np.uint64)
+    for i, s in enumerate(seeds):
+        ref_out, h = _ref_run(s, H, Wd, desc, imgs[i], ws)
+        assert (out[i].reshape(-1) == ref_out).all(), i
+        assert alice.transcripts[i].content_hash_sent == int(h[0]) and alice.transcripts[i].content_hash_recv == int(h[1])
+        assert bob.transcripts[i].content_hash_sent == int(h[2]) and bob.transcripts[i].content_hash_recv == int(h[3])
+        assert alice.transcripts[i].total_bytes("sent") == int(h[4])
+        assert bob.transcripts[i].total_bytes("sent") == int(h[5])

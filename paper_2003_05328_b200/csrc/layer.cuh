@@ -756,6 +756,60 @@ __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN))
 constexpr int kKaraMaxK = 1008;
 constexpr uint64_t kKaraLowBits = 50;  // S = H 2^50 + L: L < 2^50 after a fold, H < K 2^11.2
 
+// T = S0 + 2^30 (Sm - S0 - S2) + 2^60 S2 (exact, < 2^128 while K <= 1008) from the split
+// sums S = H 2^50 + L (L = lh:ll), as four 32-bit limbs with explicit carry chains --
+// S0, Sm, S2 and D = Sm - S0 - S2 take three limbs (< 2^82), the shifts are funnel
+// shifts -- then T mod q = corr(T_lo) + Shoup(T_hi, 2^64 mod q), made canonical.
+// ~60 instructions; the generic u128 expression compiled to ~115.
+EG_DEV uint64_t kara_T_mod(const Field64& f, const PrimeConst& pc, uint32_t l0l, uint32_t l0h, uint32_t h0,
+                           uint32_t lml, uint32_t lmh, uint32_t hm, uint32_t l2l, uint32_t l2h, uint32_t h2) {
+  uint32_t t0, t1, t2, t3;
+  asm("{\n\t"
+      ".reg .u32 a1, a2, m1, m2, b1, b2, d0, d1, d2, e0, e1, e2, e3, f1, f2, f3, u;\n\t"
+      // S0 = [%4, a1, a2], Sm = [%7, m1, m2], S2 = [%10, b1, b2]: H 2^50 = limb1 += H << 18, limb2 += H >> 14
+      "shl.b32 u, %5, 18;\n\t"
+      "add.cc.u32 a1, %6, u;\n\t"
+      "shr.b32 u, %5, 14;\n\t"
+      "addc.u32 a2, u, 0;\n\t"
+      "shl.b32 u, %8, 18;\n\t"
+      "add.cc.u32 m1, %9, u;\n\t"
+      "shr.b32 u, %8, 14;\n\t"
+      "addc.u32 m2, u, 0;\n\t"
+      "shl.b32 u, %11, 18;\n\t"
+      "add.cc.u32 b1, %12, u;\n\t"
+      "shr.b32 u, %11, 14;\n\t"
+      "addc.u32 b2, u, 0;\n\t"
+      // D = Sm - S0 - S2 (>= 0: the cross terms x0 y1 + x1 y0)
+      "sub.cc.u32 d0, %7, %4;\n\t"
+      "subc.cc.u32 d1, m1, a1;\n\t"
+      "subc.u32 d2, m2, a2;\n\t"
+      "sub.cc.u32 d0, d0, %10;\n\t"
+      "subc.cc.u32 d1, d1, b1;\n\t"
+      "subc.u32 d2, d2, b2;\n\t"
+      // E = D << 30 (D < 2^71), F = S2 << 60 (S2 < 2^68)
+      "shl.b32 e0, d0, 30;\n\t"
+      "shf.l.clamp.b32 e1, d0, d1, 30;\n\t"
+      "shf.l.clamp.b32 e2, d1, d2, 30;\n\t"
+      "shr.b32 e3, d2, 2;\n\t"
+      "shl.b32 f1, %10, 28;\n\t"
+      "shf.l.clamp.b32 f2, %10, b1, 28;\n\t"
+      "shf.l.clamp.b32 f3, b1, b2, 28;\n\t"
+      // T = S0 + E + F
+      "add.cc.u32 %0, %4, e0;\n\t"
+      "addc.cc.u32 %1, a1, e1;\n\t"
+      "addc.cc.u32 %2, a2, e2;\n\t"
+      "addc.u32 %3, e3, 0;\n\t"
+      "add.cc.u32 %1, %1, f1;\n\t"
+      "addc.cc.u32 %2, %2, f2;\n\t"
+      "addc.u32 %3, %3, f3;\n\t"
+      "}"
+      : "=r"(t0), "=r"(t1), "=r"(t2), "=r"(t3)
+      : "r"(l0l), "r"(h0), "r"(l0h), "r"(lml), "r"(hm), "r"(lmh), "r"(l2l), "r"(h2), "r"(l2h));
+  const uint64_t lo = ((uint64_t)t1 << 32) | t0, hi = ((uint64_t)t3 << 32) | t2;
+  const uint64_t x = Bfly<Field64, 0>::corr(f, lo, pc.cred) + f.mul_shoup_approx(hi, pc.c64, pc.c64p);  // < 7q
+  return Bfly<Field64, 0>::fin_ct(f, x, pc.cred);
+}
+
 template <int S, int MT, int NT, int KT, int STAGES>
 constexpr size_t mac_kara_smem() {
   return (size_t)STAGES * KT * (MT + NT) * S * sizeof(uint64_t);
@@ -868,17 +922,10 @@ __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN), (512 / (S * (MT / TM)
         H0[i][j] = Hm[i][j] = H2[i][j] = 0;
       }
   };
-  // exact T = sum x y (u128) from the split sums, reduced mod q
+  // exact T = sum x y from the split sums, reduced mod q (kara_T_mod: 32-bit limb chains)
   auto reduce_T = [&](const Field64& f, const PrimeConst& pc, int i, int j) -> uint64_t {
-    typedef unsigned __int128 u128;
-    const u128 s0 = ((u128)H0[i][j] << kKaraLowBits) + (((uint64_t)L0h[i][j] << 32) | L0l[i][j]);
-    const u128 sm = ((u128)Hm[i][j] << kKaraLowBits) + (((uint64_t)Lmh[i][j] << 32) | Lml[i][j]);
-    const u128 s2 = ((u128)H2[i][j] << kKaraLowBits) + (((uint64_t)L2h[i][j] << 32) | L2l[i][j]);
-    const u128 t = s0 + ((sm - s0 - s2) << 30) + (s2 << 60);
-    const uint64_t lo = (uint64_t)t, hi = (uint64_t)(t >> 64);
-    uint64_t x = Bfly<Field64, 0>::corr(f, lo, pc.cred);
-    if (hi) x += f.mul_shoup_approx(hi, pc.c64, pc.c64p);
-    return Bfly<Field64, 0>::fin_ct(f, x, pc.cred);
+    return kara_T_mod(f, pc, L0l[i][j], L0h[i][j], H0[i][j], Lml[i][j], Lmh[i][j], Hm[i][j], L2l[i][j], L2h[i][j],
+                      H2[i][j]);
   };
 
 #pragma unroll 1

@@ -251,6 +251,25 @@ class LayerOps:
                                          _ptr(out), _stream(stream)))
         return (out, a, b) if want_shares else out
 
+    def host_call(self, key, w_eval, h_x: torch.Tensor, rand: Randomness, ws, h_out: torch.Tensor, stream=None):
+        """A prepared host-buffer layer call: every argument marshalled once; calling the
+        returned function runs the layer (H2D, Enc, Bob, Dec, D2H, synchronous) again on
+        the same buffers -- the serving loop's form of forward_host."""
+        r = rand.struct()
+        st = (stream if stream is not None else torch.cuda.current_stream()).cuda_stream
+        in_t = IN_U8 if h_x.dtype == torch.uint8 else IN_U32
+        args = (self.ctx.h, C.byref(self.d), _ptr(key), _ptr(w_eval), C.c_void_p(h_x.data_ptr()), in_t, h_x.shape[0],
+                C.byref(r), _ptr(ws), C.c_void_p(h_out.data_ptr()), C.c_void_p(st))
+        fn = lib().ensei_gpu_conv_layer_host
+        keep = (key, w_eval, h_x, rand, r, ws, h_out)  # buffers stay alive with the call
+
+        def call():
+            rc = fn(*args)
+            if rc:
+                check(rc)
+            return keep[6]
+        return call
+
     def forward_host(self, key, w_eval, h_x: torch.Tensor, rand: Randomness, ws, h_out: torch.Tensor, stream=None):
         """Host-buffer entry point (pinned h_x / h_out): H2D, layer, D2H, synchronous.
         The marshalled ctypes arguments are cached while the buffers are unchanged."""

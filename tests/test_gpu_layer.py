@@ -176,6 +176,12 @@ def test_host_buffer_entry_equals_device_path(ops):
     out_pageable = torch.empty((2, 4, 16, 16), dtype=torch.int32)
     L.forward_host(key, we, imgs2.clone(), ops.Randomness(seed=3), ws, out_pageable)
     assert torch.equal(out_pageable, h_out)
+    # prepared call (the bench's e2e form): same results, re-reads the input buffer each call
+    call = L.host_call(key, we, h_in, ops.Randomness(seed=2), ws, h_out)
+    h_in.copy_(imgs)
+    assert torch.equal(call(), d.cpu())
+    h_in.copy_(imgs2)
+    assert torch.equal(call(), L.forward(key, we, imgs2.to(dev()), ops.Randomness(seed=2)).cpu())
 
 
 def test_pooled_relu_stack_vs_oracle(ops):

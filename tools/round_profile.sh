@@ -18,17 +18,17 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 # full captures: one launch of each config-1 layer kernel (after warm-up) and the config-4 MAC
 timeout 900 ncu --set full --import-source on --clock-control none \
   -k regex:"tile_enc_kernel|share_kernel|mac_kara_kernel|dec_kernel" --launch-skip 8 -c 4 \
-  -o $O/full_c1 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-graph > $O/ncu_full_c1.log 2>&1; echo "ncu full c1 rc=$?" >> $O/status
+  -o /tmp/full_c1 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-graph > $O/ncu_full_c1.log 2>&1; echo "ncu full c1 rc=$?" >> $O/status
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:mac_kara --launch-skip 2 -c 1 \
-  -o $O/full_c4_mac python bench.py --config 4 --steps 1 --warmup 3 --no-cpu-baseline --no-graph > $O/ncu_full_c4.log 2>&1; echo "ncu full c4 rc=$?" >> $O/status
+  -o /tmp/full_c4_mac python bench.py --config 4 --steps 1 --warmup 3 --no-cpu-baseline --no-graph > $O/ncu_full_c4.log 2>&1; echo "ncu full c4 rc=$?" >> $O/status
 # export the captures as CSV (raw metrics + SASS source with per-instruction counters), drop the .ncu-rep
 for r in full_c1 full_c4_mac; do
-  if [ -f $O/$r.ncu-rep ]; then
-    ncu -i $O/$r.ncu-rep --page raw --csv > $O/${r}_raw.csv 2>/dev/null
-    ncu -i $O/$r.ncu-rep --page details --csv > $O/${r}_details.csv 2>/dev/null
-    python tools/ncu_traffic.py $O/$r.ncu-rep $( [ $r = full_c1 ] && echo config1 || echo config4 ) $O/ncu_traffic.json > /dev/null 2>&1
-    ncu -i $O/$r.ncu-rep --page source --csv --print-source sass > $O/${r}_sass.csv 2>/dev/null
-    rm -f $O/$r.ncu-rep
+  if [ -f /tmp/$r.ncu-rep ]; then
+    ncu -i /tmp/$r.ncu-rep --page raw --csv > $O/${r}_raw.csv 2>/dev/null
+    ncu -i /tmp/$r.ncu-rep --page details --csv > $O/${r}_details.csv 2>/dev/null
+    python tools/ncu_traffic.py /tmp/$r.ncu-rep $( [ $r = full_c1 ] && echo config1 || echo config4 ) $O/ncu_traffic.json > /dev/null 2>&1
+    ncu -i /tmp/$r.ncu-rep --page source --csv --print-source sass > $O/${r}_sass.csv 2>/dev/null
+    rm -f /tmp/$r.ncu-rep
   fi
 done
 cat $O/status

@@ -1009,8 +1009,11 @@ __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN), (512 / (S * (MT / TM)
         }
       }
     }
-#pragma unroll 1
-    for (; kk < kmax; kk += 2) pair(kk);  // last chunk only: < 3 pairs, zero-filled odd tail
+    // last chunk only: < 3 pairs, zero-filled odd tail; straight-line (a rolled loop here
+    // rotates every accumulator pair through IMAD.MOV at each back edge)
+    if (kk < kmax) pair(kk);
+    if (kk + 2 < kmax) pair(kk + 2);
+    if (kk + 4 < kmax) pair(kk + 4);
     kdone += KT;
     const bool last = cm_c == nchunks - 1;
     if (last || kdone == kKaraMaxK) {  // flush: out = (mask | previous partial) + T mod q

@@ -148,16 +148,63 @@ struct GroupBar {
 
 enum TileMode { TILE_ENC = 0, TILE_HOMREC = 1, TILE_WEIGHTS = 2 };
 
+// Twiddle staging (TWS): a tile kernel walks three read-only tables -- the n-point
+// negacyclic table over q, the one over p and the 64-point cyclic table of its 2D
+// transform.  Read through L1 they were the top stall reason of the latency-bound tile
+// kernels (long_scoreboard on the IMADs consuming twiddles, ~20% of Enc/Dec samples).
+// With TWS one thread issues TMA bulk copies into shared memory at kernel start (one
+// mbarrier), overlapping the CTA's first loads; every thread waits on the barrier before
+// the first transform.  TWS = 1 stages the q table only (32 KB at n = 2048: Enc and
+// HomShare CTAs still co-reside), TWS = 2 all three (49 KB: Dec).  n = 2048 only.
+// Layout: q [N] x 16 B | p [N] x 8 B | cyclic [128] x 8 B.
+template <int LOGN, int TWS>
+__host__ __device__ constexpr size_t tw_stage_bytes() {
+  return TWS == 0 ? 0 : TWS == 1 ? (size_t)(1 << LOGN) * 16 : (size_t)(1 << LOGN) * 24 + 128 * 8;
+}
+struct TwStage {
+  const TwPair<uint64_t>* q;
+  const TwPair<uint32_t>* p;
+  const TwPair<uint32_t>* c;
+};
+template <int LOGN, int TWS>
+EG_DEV TwStage tw_stage_issue(uint8_t* dst, uint64_t* bar, const TwPair<uint64_t>* q, const TwPair<uint32_t>* p,
+                              const TwPair<uint32_t>* c) {
+  constexpr uint32_t N = 1u << LOGN;
+  TwStage s{reinterpret_cast<const TwPair<uint64_t>*>(dst), p, c};
+  if constexpr (TWS == 2) {
+    s.p = reinterpret_cast<const TwPair<uint32_t>*>(dst + N * 16);
+    s.c = reinterpret_cast<const TwPair<uint32_t>*>(dst + N * 24);
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, (uint32_t)tw_stage_bytes<LOGN, TWS>());
+    for (uint32_t off = 0; off < N * 16; off += 32768u)
+      tma_bulk_g2s(dst + off, reinterpret_cast<const uint8_t*>(q) + off, min(32768u, N * 16 - off), bar);
+    if constexpr (TWS == 2) {
+      tma_bulk_g2s(dst + N * 16, p, N * 8, bar);
+      tma_bulk_g2s(dst + N * 24, c, 128 * 8, bar);
+    }
+  }
+  return s;
+}
+
 // One CTA per (image, channel) [ENC / HOMREC] or (out, in) filter [WEIGHTS], G thread
 // groups of NT = n/8 threads; group g handles blocks b = g, g+G, ... concurrently.
 // Shared: tile S (u32) + per group a ring buffer over p (u32), one over q (u64) and the
 // block's Enc noise (int8, drawn two per Philox call).  The q-side epilogue (a^ draw,
 // a^ t^, stores) runs as a separate coalesced loop after the NTT, not inside its
 // unrolled last pass, to keep register pressure low.
-template <int LOGN, int LOGH, int LOGW, int R, int TM, bool INJ, int IN_T, int G>
+template <int LOGN, int LOGH, int LOGW, int G>
+constexpr size_t tile_enc_smem() {
+  return (((size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4 + 127) & ~(size_t)127) +
+         G * ((((size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4 + (1 << LOGN)) + 127) & ~(size_t)127);
+}
+
+template <int LOGN, int LOGH, int LOGW, int R, int TM, bool INJ, int IN_T, int G, int TWS = 0>
 __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_blocks(G*((1 << LOGN) >> tile_loge(LOGN))))
     tile_enc_kernel(LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride,
                     const void* __restrict__ in, uint64_t* __restrict__ out) {
+  static_assert(!TWS || R == 1, "twiddle staging: single prime");
   constexpr int N = 1 << LOGN, NT = N >> tile_loge(LOGN);
   constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
   constexpr size_t GROUP_BYTES = (size_t)N * 8 + ssize<uint32_t>(N) * 4 + N;
@@ -176,6 +223,11 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
   const int ch = item % a.cin;
   const int img = item / a.cin;  // image (or output channel for WEIGHTS)
   const int th = TM == TILE_WEIGHTS ? a.fh : a.H, tw = TM == TILE_WEIGHTS ? a.fw : a.W;
+  __shared__ uint64_t tw_bar;
+  TwStage tws{a.twq_fwd[0], a.twp_inv, a.twc_fwd};
+  if constexpr (TWS)
+    tws = tw_stage_issue<LOGN, TWS>(smem_raw + tile_enc_smem<LOGN, LOGH, LOGW, G>(), &tw_bar, a.twq_fwd[0], a.twp_inv,
+                               a.twc_fwd);
 
   // 1. pad into the tile (REF pad_image / pad_residues, ntt.cpp:155-185)
   for (int i = threadIdx.x; i < Lh * Lw; i += blockDim.x) {
@@ -196,8 +248,9 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
     S[r * LS + c] = v;
   }
   __syncthreads();
+  if constexpr (TWS) mbar_wait(&tw_bar, 0);
   // 2. DFT2D (rows then columns; output bit-reversed in both dims)
-  tile_transform_2d<false, LOGH, LOGW>(pf, a.pp.cred, a.twc_fwd, S, LS);
+  tile_transform_2d<false, LOGH, LOGW>(pf, a.pp.cred, tws.c, S, LS);
 
   const uint64_t* kimg = key + (size_t)(TM == TILE_ENC ? img : 0) * key_stride;
   const int gimg = a.image_base + img;
@@ -224,7 +277,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
       auto src = [&](int j) { return gather_slot<LOGN, LOGH, LOGW>(S, b, j, a.G); };
       SmemRW<uint32_t> dst_raw{pbuf};
       auto dst = [&](int i, uint32_t v) { dst_raw(i, Bfly<Field32, 0>::fin_gs(pf, v)); };
-      ntt_inverse<Field32, uint32_t, LOGN, tile_loge(LOGN), 0, false, false>(pf, a.twp_inv, pbuf, tid, src, dst, bar);
+      ntt_inverse<Field32, uint32_t, LOGN, tile_loge(LOGN), 0, false, false>(pf, tws.p, pbuf, tid, src, dst, bar);
     }
     bar.sync();
 #pragma unroll 1
@@ -247,8 +300,8 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
       };
       // 5. NTT_q in place (lazy values stay in qbuf), then the epilogue
       SmemRW<uint64_t> qs{qbuf};
-      ntt_forward<Field64, uint64_t, LOGN, tile_loge(LOGN), 0, false, false>(f, a.twq_fwd[r], qbuf, tid, src, qs, bar,
-                                                                   pc.cred);
+      ntt_forward<Field64, uint64_t, LOGN, tile_loge(LOGN), 0, false, false>(f, TWS ? tws.q : a.twq_fwd[r], qbuf, tid,
+                                                                         src, qs, bar, pc.cred);
       bar.sync();
       if constexpr (TM == TILE_WEIGHTS) {
         uint64_t* ob = out + ((((size_t)img * a.cin + ch) * a.B + b) * R + r) * N;
@@ -283,11 +336,6 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
   }
 }
 
-template <int LOGN, int LOGH, int LOGW, int G>
-constexpr size_t tile_enc_smem() {
-  return (((size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4 + 127) & ~(size_t)127) +
-         G * ((((size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4 + (1 << LOGN)) + 127) & ~(size_t)127);
-}
 
 // ------------------------------------------------------- HomShare + Bob share
 
@@ -295,9 +343,16 @@ constexpr size_t tile_enc_smem() {
 // drawn once (two per Philox call) into shared memory; masks
 // NTT_q(Delta*INTT_p(p - s_B)) go to the c1 words of the output ciphertext (device
 // layout) and Bob's share = crop(IDFT2D(merge(s_B))).
-template <int LOGN, int LOGH, int LOGW, int R, bool INJ, int G>
+template <int LOGN, int LOGH, int LOGW, int G>
+constexpr size_t share_smem(int B) {
+  return (((size_t)(1 << LOGH) * ((1 << LOGW) + 1) + 31) & ~(size_t)31) * 4 + (size_t)B * (1 << LOGN) * 4 +
+         G * ((((size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4) + 127) & ~(size_t)127);
+}
+
+template <int LOGN, int LOGH, int LOGW, int R, bool INJ, int G, int TWS = 0>
 __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_blocks(G*((1 << LOGN) >> tile_loge(LOGN))))
     share_kernel(LayerArgs a, uint64_t* __restrict__ mask, uint32_t* __restrict__ bob_share) {
+  static_assert(!TWS || R == 1, "twiddle staging: single prime");
   constexpr int N = 1 << LOGN, NT = N >> tile_loge(LOGN);
   constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
   constexpr size_t GROUP_BYTES = (size_t)N * 8 + ssize<uint32_t>(N) * 4;
@@ -314,6 +369,11 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
   const int item = blockIdx.x;  // img * cout + o
   const int o = item % a.cout, img = item / a.cout;
   const int gimg = a.image_base + img;
+  __shared__ uint64_t tw_bar;
+  TwStage tws{a.twq_fwd[0], a.twp_inv, a.twc_inv};
+  if constexpr (TWS)  // tables after the working buffers
+    tws = tw_stage_issue<LOGN, TWS>(smem_raw + share_smem<LOGN, LOGH, LOGW, G>(a.B), &tw_bar, a.twq_fwd[0], a.twp_inv,
+                                    a.twc_inv);
   // 1. s_B for all blocks (natural slot order)
   for (int e = threadIdx.x; e < a.B * N / 2; e += blockDim.x) {
     const int b = e / (N / 2), i2 = e % (N / 2);
@@ -331,6 +391,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
     sbuf[b * N + 2 * i2 + 1] = s1;
   }
   __syncthreads();
+  if constexpr (TWS) mbar_wait(&tw_bar, 0);
   for (int b = g; b < a.B; b += G) {
     auto src = [&](int j) {
       const uint32_t s = sbuf[b * N + brev(j, LOGN)];
@@ -338,7 +399,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
     };
     SmemRW<uint32_t> dst_raw{pbuf};
     auto dst = [&](int i, uint32_t v) { dst_raw(i, Bfly<Field32, 0>::fin_gs(pf, v)); };
-    ntt_inverse<Field32, uint32_t, LOGN, tile_loge(LOGN), 0, false, false>(pf, a.twp_inv, pbuf, tid, src, dst, bar);
+    ntt_inverse<Field32, uint32_t, LOGN, tile_loge(LOGN), 0, false, false>(pf, tws.p, pbuf, tid, src, dst, bar);
     bar.sync();
 #pragma unroll 1
     for (int r = 0; r < R; ++r) {
@@ -348,8 +409,8 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
       // mask lands where c1 of the output ciphertext (img, o, b) lives
       uint64_t* mo = mask + ((size_t)item * a.B + b) * ct_words<R>(N) + (size_t)(R + r) * N;
       GlobalOut64Fwd outw{mo, f, pc.cred};
-      ntt_forward<Field64, uint64_t, LOGN, tile_loge(LOGN), 0, false, false>(f, a.twq_fwd[r], qbuf, tid, qsrc, outw, bar,
-                                                                   pc.cred);
+      ntt_forward<Field64, uint64_t, LOGN, tile_loge(LOGN), 0, false, false>(f, TWS ? tws.q : a.twq_fwd[r], qbuf, tid,
+                                                                         qsrc, outw, bar, pc.cred);
       bar.sync();
     }
   }
@@ -360,7 +421,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
     S[brev(r, LOGH) * LS + brev(c, LOGW)] = sbuf[i];  // natural grid position i = r*Lw + c
   }
   __syncthreads();
-  tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, S, LS);
+  tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, tws.c, S, LS);
   uint32_t* bs = bob_share + (size_t)item * a.oh * a.ow;
   for (int i = threadIdx.x; i < a.oh * a.ow; i += blockDim.x) {
     const int r = i / a.ow, c = i % a.ow;
@@ -368,11 +429,6 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
   }
 }
 
-template <int LOGN, int LOGH, int LOGW, int G>
-constexpr size_t share_smem(int B) {
-  return (((size_t)(1 << LOGH) * ((1 << LOGW) + 1) + 31) & ~(size_t)31) * 4 + (size_t)B * (1 << LOGN) * 4 +
-         G * ((((size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4) + 127) & ~(size_t)127);
-}
 
 // RNS decryption (config 4): per prime r, phi_r = INTT_{q_r}(c0 t^ + c1), y_r = phi_r *
 // (Q/q_r)^-1 mod q_r; with phi = sum_r y_r Q/q_r - kQ,  p phi / Q = sum_r y_r p / q_r - kp,
@@ -474,7 +530,7 @@ constexpr size_t dec_smem() {
 // STG: the CTA's ciphertext blocks and the key are staged into shared memory with
 // cp.async (swizzled) before the first INTT pass, instead of per-thread dependent global
 // loads inside it (the pass was 30% of the kernel's stall samples at n = 2048).
-template <int LOGN, int LOGH, int LOGW, int G, bool STG>
+template <int LOGN, int LOGH, int LOGW, int G, bool STG, int TWS = 0>
 __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)))
     dec_kernel(LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride,
                const uint64_t* __restrict__ ct, uint32_t* __restrict__ alice_share,
@@ -498,6 +554,11 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)))
   const Field64 f = pc.f;
   const uint64_t cp = pc.cp, h = f.q >> 1;  // floor(p 2^64 / q), floor(q / 2)
   uint64_t* kst = reinterpret_cast<uint64_t*>(smem_raw + dec_smem<LOGN, LOGH, LOGW, G>());  // [t^][t^'][B][c0][c1]
+  __shared__ uint64_t tw_bar;
+  TwStage tws{a.twq_inv[0], a.twp_fwd, a.twc_inv};
+  if constexpr (TWS)  // tables after the staged arrays
+    tws = tw_stage_issue<LOGN, TWS>(reinterpret_cast<uint8_t*>(kst + (STG ? (size_t)(2 + 2 * a.B) * N : 0)), &tw_bar,
+                               a.twq_inv[0], a.twp_fwd, a.twc_inv);
   if constexpr (STG) {
     const uint64_t* cg = ct + (size_t)item * a.B * ct_words<1>(N);
     const int narr = 2 + 2 * a.B;  // N-word arrays: t^, t^', then c0, c1 per block
@@ -508,8 +569,9 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)))
     }
     cp_async_commit();
     cp_async_wait_all();
-    __syncthreads();
   }
+  __syncthreads();
+  if constexpr (TWS) mbar_wait(&tw_bar, 0);
   for (int b = g; b < a.B; b += G) {
     const uint64_t* cb = ct + ((size_t)item * a.B + b) * ct_words<1>(N);
     auto run_inv = [&](auto& src) {
@@ -526,7 +588,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)))
       }
       pbuf[sidx<uint32_t>(i)] = (uint32_t)(Q % p);
     };
-    ntt_inverse<Field64, uint64_t, LOGN, tile_loge(LOGN), 0, false, false>(f, a.twq_inv[0], qbuf, tid, src, dst, bar);
+    ntt_inverse<Field64, uint64_t, LOGN, tile_loge(LOGN), 0, false, false>(f, tws.q, qbuf, tid, src, dst, bar);
     };
     if constexpr (STG) {
       PhiSrcS src{kst + (size_t)(2 + 2 * b) * N, kst + (size_t)(3 + 2 * b) * N, kst, kst + N, f};
@@ -539,12 +601,12 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)))
     // decode_slots (NTT_p) -> scatter into the bit-reversed tile
     SmemRW<uint32_t> psrc{pbuf};
     auto pdst = [&](int j, uint32_t v) { scatter_slot<LOGN, LOGH, LOGW>(S, b, j, a.G, reduce_lazy(pf, v, a.pp.cred)); };
-    ntt_forward<Field32, uint32_t, LOGN, tile_loge(LOGN), 0, false, false>(pf, a.twp_fwd, pbuf, tid, psrc, pdst, bar);
+    ntt_forward<Field32, uint32_t, LOGN, tile_loge(LOGN), 0, false, false>(pf, tws.p, pbuf, tid, psrc, pdst, bar);
     bar.sync();
   }
   __syncthreads();
   // IDFT2D + crop (+ recombine with Bob's share)
-  tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, S, LS);
+  tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, tws.c, S, LS);
   const size_t base = (size_t)item * a.oh * a.ow;
   for (int i = threadIdx.x; i < a.oh * a.ow; i += blockDim.x) {
     const int r = i / a.ow, c = i % a.ow;

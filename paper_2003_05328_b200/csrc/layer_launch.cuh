@@ -25,14 +25,27 @@ template <int LOGN>
 constexpr bool kTwoGroups = LOGN <= 12;
 inline int groups_for(int logn, int B) { return (B >= 2 && logn <= 12) ? 2 : 1; }
 
-template <int LOGN, int LOGL, int R, int TM, bool INJ, int IN_T, int G>
-static void enc_go_g(const LayerRun& r, const uint64_t* key, uint32_t key_stride, const void* in, uint64_t* out,
+template <int LOGN, int LOGL, int R, int TM, bool INJ, int IN_T, int G, int TWS>
+static void enc_go_t(const LayerRun& r, const uint64_t* key, uint32_t key_stride, const void* in, uint64_t* out,
                      int items) {
-  auto k = tile_enc_kernel<LOGN, LOGL, LOGL, R, TM, INJ, IN_T, G>;
-  constexpr size_t smem = tile_enc_smem<LOGN, LOGL, LOGL, G>();
+  auto k = tile_enc_kernel<LOGN, LOGL, LOGL, R, TM, INJ, IN_T, G, TWS>;
+  constexpr size_t smem = tile_enc_smem<LOGN, LOGL, LOGL, G>() + tw_stage_bytes<LOGN, TWS>();
   set_smem(k, smem);
   k<<<items, G * ((1 << LOGN) >> tile_loge(LOGN)), smem, r.st>>>(r.a, key, key_stride, in, out);
   check_launch("tile_enc_kernel");
+}
+
+// Twiddle staging (layer.cuh, TWS) at n = 2048 for single-wave launches: the q table
+// (32 KB) costs occupancy once CTAs queue behind each other, but is free when the launch
+// has at most one tile per SM (Enc + HomShare CTAs still co-reside).
+template <int LOGN, int LOGL, int R, int TM, bool INJ, int IN_T, int G>
+static void enc_go_g(const LayerRun& r, const uint64_t* key, uint32_t key_stride, const void* in, uint64_t* out,
+                     int items) {
+  if constexpr (LOGN == 11 && R == 1 && TM != TILE_WEIGHTS) {
+    if (items <= r.ctx->sm_count)
+      return enc_go_t<LOGN, LOGL, R, TM, INJ, IN_T, G, 1>(r, key, key_stride, in, out, items);
+  }
+  enc_go_t<LOGN, LOGL, R, TM, INJ, IN_T, G, 0>(r, key, key_stride, in, out, items);
 }
 
 template <int LOGN, int LOGL, int R, int TM, bool INJ, int IN_T>
@@ -87,13 +100,21 @@ void launch_tile(const LayerRun& r, int tm, bool inj, int in_t, const uint64_t* 
 }
 
 // ---- HomShare masks + Bob share ----
-template <int LOGN, int LOGL, int R, bool INJ, int G>
-static void share_go_g(const LayerRun& r, uint64_t* ct_out, uint32_t* bob_share, int items) {
-  auto k = share_kernel<LOGN, LOGL, LOGL, R, INJ, G>;
-  const size_t smem = share_smem<LOGN, LOGL, LOGL, G>(r.a.B);
+template <int LOGN, int LOGL, int R, bool INJ, int G, int TWS>
+static void share_go_t(const LayerRun& r, uint64_t* ct_out, uint32_t* bob_share, int items) {
+  auto k = share_kernel<LOGN, LOGL, LOGL, R, INJ, G, TWS>;
+  const size_t smem = share_smem<LOGN, LOGL, LOGL, G>(r.a.B) + tw_stage_bytes<LOGN, TWS>();
   set_smem(k, smem);
   k<<<items, G * ((1 << LOGN) >> tile_loge(LOGN)), smem, r.st>>>(r.a, ct_out, bob_share);
   check_launch("share_kernel");
+}
+
+template <int LOGN, int LOGL, int R, bool INJ, int G>
+static void share_go_g(const LayerRun& r, uint64_t* ct_out, uint32_t* bob_share, int items) {
+  if constexpr (LOGN == 11 && R == 1) {  // q-table staging for single-wave launches (as Enc)
+    if (items <= r.ctx->sm_count) return share_go_t<LOGN, LOGL, R, INJ, G, 1>(r, ct_out, bob_share, items);
+  }
+  share_go_t<LOGN, LOGL, R, INJ, G, 0>(r, ct_out, bob_share, items);
 }
 
 template <int LOGN, int LOGL, int R, bool INJ>
@@ -138,7 +159,12 @@ static void dec_go_g(const LayerRun& r, const uint64_t* key, uint32_t ks, const 
                      const uint32_t* bob, uint32_t* out, int items) {
   constexpr size_t base = dec_smem<LOGN, LOGL, LOGL, G>();
   const size_t staged = base + (size_t)(2 + 2 * r.a.B) * (1 << LOGN) * 8;  // + t^, t^', c0/c1 per block
-  if (staged <= 227 * 1024) {
+  constexpr size_t twb = tw_stage_bytes<LOGN, 2>();
+  if (LOGN == 11 && items <= r.ctx->sm_count && staged + twb <= 227 * 1024) {  // + staged twiddles (TWS)
+    auto k = dec_kernel<LOGN, LOGL, LOGL, G, true, LOGN == 11 ? 2 : 0>;
+    set_smem(k, staged + twb);
+    k<<<items, G * ((1 << LOGN) >> tile_loge(LOGN)), staged + twb, r.st>>>(r.a, key, ks, ct, alice, bob, out);
+  } else if (staged <= 227 * 1024) {
     auto k = dec_kernel<LOGN, LOGL, LOGL, G, true>;
     set_smem(k, staged);
     k<<<items, G * ((1 << LOGN) >> tile_loge(LOGN)), staged, r.st>>>(r.a, key, ks, ct, alice, bob, out);

@@ -194,10 +194,13 @@ EG_DEV TwStage tw_stage_issue(uint8_t* dst, uint64_t* bar, const TwPair<uint64_t
 // block's Enc noise (int8, drawn two per Philox call).  The q-side epilogue (a^ draw,
 // a^ t^, stores) runs as a separate coalesced loop after the NTT, not inside its
 // unrolled last pass, to keep register pressure low.
-template <int LOGN, int LOGH, int LOGW, int G>
+// ALIAS (the fully staged single-prime variant): the p-side ring buffer lives inside
+// the q-side one -- the q transform's first pass loads all of it before its first store.
+template <int LOGN, int LOGH, int LOGW, int G, bool ALIAS = false>
 constexpr size_t tile_enc_smem() {
   return (((size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4 + 127) & ~(size_t)127) +
-         G * ((((size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4 + (1 << LOGN)) + 127) & ~(size_t)127);
+         G * ((((size_t)(1 << LOGN) * 8 + (ALIAS ? 0 : ssize<uint32_t>(1 << LOGN) * 4) + (1 << LOGN)) + 127) &
+              ~(size_t)127);
 }
 
 template <int LOGN, int LOGH, int LOGW, int R, int TM, bool INJ, int IN_T, int G, int TWS = 0>
@@ -207,14 +210,16 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
   static_assert(!TWS || R == 1, "twiddle staging: single prime");
   constexpr int N = 1 << LOGN, NT = N >> tile_loge(LOGN);
   constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
-  constexpr size_t GROUP_BYTES = (size_t)N * 8 + ssize<uint32_t>(N) * 4 + N;
+  constexpr bool ALIAS = TWS == 2;
+  static_assert(!ALIAS || R == 1, "aliased p buffer: one q transform per block");
+  constexpr size_t GROUP_BYTES = (size_t)N * 8 + (ALIAS ? 0 : ssize<uint32_t>(N) * 4) + N;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);
   const int g = threadIdx.x / NT, tid = threadIdx.x % NT;
   uint8_t* gbase = smem_raw + (((size_t)Lh * LS * 4 + 127) & ~(size_t)127) + g * ((GROUP_BYTES + 127) & ~(size_t)127);
   uint64_t* qbuf = reinterpret_cast<uint64_t*>(gbase);
-  uint32_t* pbuf = reinterpret_cast<uint32_t*>(qbuf + N);
-  int8_t* ebuf = reinterpret_cast<int8_t*>(pbuf + ssize<uint32_t>(N));
+  uint32_t* pbuf = ALIAS ? reinterpret_cast<uint32_t*>(qbuf) : reinterpret_cast<uint32_t*>(qbuf + N);
+  int8_t* ebuf = ALIAS ? reinterpret_cast<int8_t*>(qbuf + N) : reinterpret_cast<int8_t*>(pbuf + ssize<uint32_t>(N));
   const GroupBar bar{g, NT};
   const Field32 pf = a.pp.f;
   const uint32_t p = pf.q;
@@ -226,7 +231,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
   __shared__ uint64_t tw_bar;
   TwStage tws{a.twq_fwd[0], a.twp_inv, a.twc_fwd};
   if constexpr (TWS)
-    tws = tw_stage_issue<LOGN, TWS>(smem_raw + tile_enc_smem<LOGN, LOGH, LOGW, G>(), &tw_bar, a.twq_fwd[0], a.twp_inv,
+    tws = tw_stage_issue<LOGN, TWS>(smem_raw + tile_enc_smem<LOGN, LOGH, LOGW, G, ALIAS>(), &tw_bar, a.twq_fwd[0], a.twp_inv,
                                a.twc_fwd);
 
   // 1. pad into the tile (REF pad_image / pad_residues, ntt.cpp:155-185)
@@ -300,7 +305,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
       };
       // 5. NTT_q in place (lazy values stay in qbuf), then the epilogue
       SmemRW<uint64_t> qs{qbuf};
-      ntt_forward<Field64, uint64_t, LOGN, tile_loge(LOGN), 0, false, false>(f, TWS ? tws.q : a.twq_fwd[r], qbuf, tid,
+      ntt_forward<Field64, uint64_t, LOGN, tile_loge(LOGN), 0, ALIAS, false>(f, TWS ? tws.q : a.twq_fwd[r], qbuf, tid,
                                                                          src, qs, bar, pc.cred);
       bar.sync();
       if constexpr (TM == TILE_WEIGHTS) {
@@ -343,10 +348,10 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
 // drawn once (two per Philox call) into shared memory; masks
 // NTT_q(Delta*INTT_p(p - s_B)) go to the c1 words of the output ciphertext (device
 // layout) and Bob's share = crop(IDFT2D(merge(s_B))).
-template <int LOGN, int LOGH, int LOGW, int G>
+template <int LOGN, int LOGH, int LOGW, int G, bool ALIAS = false>
 constexpr size_t share_smem(int B) {
   return (((size_t)(1 << LOGH) * ((1 << LOGW) + 1) + 31) & ~(size_t)31) * 4 + (size_t)B * (1 << LOGN) * 4 +
-         G * ((((size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4) + 127) & ~(size_t)127);
+         G * ((((size_t)(1 << LOGN) * 8 + (ALIAS ? 0 : ssize<uint32_t>(1 << LOGN) * 4)) + 127) & ~(size_t)127);
 }
 
 template <int LOGN, int LOGH, int LOGW, int R, bool INJ, int G, int TWS = 0>
@@ -355,14 +360,15 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
   static_assert(!TWS || R == 1, "twiddle staging: single prime");
   constexpr int N = 1 << LOGN, NT = N >> tile_loge(LOGN);
   constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
-  constexpr size_t GROUP_BYTES = (size_t)N * 8 + ssize<uint32_t>(N) * 4;
+  constexpr bool ALIAS = TWS == 2;  // p buffer inside the q buffer (see tile_enc_smem)
+  constexpr size_t GROUP_BYTES = (size_t)N * 8 + (ALIAS ? 0 : ssize<uint32_t>(N) * 4);
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);
   uint32_t* sbuf = S + (((size_t)Lh * LS + 31) & ~(size_t)31);  // [B][N] shares
   const int g = threadIdx.x / NT, tid = threadIdx.x % NT;
   uint8_t* gbase = reinterpret_cast<uint8_t*>(sbuf + (size_t)a.B * N) + g * ((GROUP_BYTES + 127) & ~(size_t)127);
   uint64_t* qbuf = reinterpret_cast<uint64_t*>(gbase);
-  uint32_t* pbuf = reinterpret_cast<uint32_t*>(qbuf + N);
+  uint32_t* pbuf = ALIAS ? reinterpret_cast<uint32_t*>(qbuf) : reinterpret_cast<uint32_t*>(qbuf + N);
   const GroupBar bar{g, NT};
   const Field32 pf = a.pp.f;
   const uint32_t p = pf.q;
@@ -372,7 +378,8 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
   __shared__ uint64_t tw_bar;
   TwStage tws{a.twq_fwd[0], a.twp_inv, a.twc_inv};
   if constexpr (TWS)  // tables after the working buffers
-    tws = tw_stage_issue<LOGN, TWS>(smem_raw + share_smem<LOGN, LOGH, LOGW, G>(a.B), &tw_bar, a.twq_fwd[0], a.twp_inv,
+    tws = tw_stage_issue<LOGN, TWS>(smem_raw + share_smem<LOGN, LOGH, LOGW, G, ALIAS>(a.B), &tw_bar, a.twq_fwd[0],
+                                    a.twp_inv,
                                     a.twc_inv);
   // 1. s_B for all blocks (natural slot order)
   for (int e = threadIdx.x; e < a.B * N / 2; e += blockDim.x) {
@@ -409,7 +416,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
       // mask lands where c1 of the output ciphertext (img, o, b) lives
       uint64_t* mo = mask + ((size_t)item * a.B + b) * ct_words<R>(N) + (size_t)(R + r) * N;
       GlobalOut64Fwd outw{mo, f, pc.cred};
-      ntt_forward<Field64, uint64_t, LOGN, tile_loge(LOGN), 0, false, false>(f, TWS ? tws.q : a.twq_fwd[r], qbuf, tid,
+      ntt_forward<Field64, uint64_t, LOGN, tile_loge(LOGN), 0, ALIAS, false>(f, TWS ? tws.q : a.twq_fwd[r], qbuf, tid,
                                                                          qsrc, outw, bar, pc.cred);
       bar.sync();
     }

@@ -18,6 +18,14 @@ template <class K>
 static void set_smem(K k, size_t smem) {
   if (smem > 48 * 1024) EG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 }
+// Kernels meant to share an SM with another kernel's CTAs (Enc + HomShare) ask for the
+// full shared-memory carveout: the driver otherwise sizes the SM's carveout for the
+// first kernel placed there (e.g. 132 KB for a 114 KB CTA) and the second cannot join.
+template <class K>
+static void set_smem_shared_sm(K k, size_t smem) {
+  set_smem(k, smem);
+  EG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+}
 
 // ---- tile -> ring (Enc / HomRec / weights / secret) ----
 // thread groups per CTA: the blocks of one tile run concurrently when they fit
@@ -29,21 +37,22 @@ template <int LOGN, int LOGL, int R, int TM, bool INJ, int IN_T, int G, int TWS>
 static void enc_go_t(const LayerRun& r, const uint64_t* key, uint32_t key_stride, const void* in, uint64_t* out,
                      int items) {
   auto k = tile_enc_kernel<LOGN, LOGL, LOGL, R, TM, INJ, IN_T, G, TWS>;
-  constexpr size_t smem = tile_enc_smem<LOGN, LOGL, LOGL, G>() + tw_stage_bytes<LOGN, TWS>();
-  set_smem(k, smem);
+  constexpr size_t smem = tile_enc_smem<LOGN, LOGL, LOGL, G, TWS == 2>() + tw_stage_bytes<LOGN, TWS>();
+  set_smem_shared_sm(k, smem);
   k<<<items, G * ((1 << LOGN) >> tile_loge(LOGN)), smem, r.st>>>(r.a, key, key_stride, in, out);
   check_launch("tile_enc_kernel");
 }
 
-// Twiddle staging (layer.cuh, TWS) at n = 2048 for single-wave launches: the q table
-// (32 KB) costs occupancy once CTAs queue behind each other, but is free when the launch
-// has at most one tile per SM (Enc + HomShare CTAs still co-reside).
+// Twiddle staging (layer.cuh, TWS = 2, with the p buffer aliased into the q buffer) at
+// n = 2048 for single-wave launches: 49 KB of tables cost occupancy once CTAs queue
+// behind each other, but are free when the launch has at most one tile per SM (an Enc
+// and a HomShare CTA still co-reside: 102 + 114 KB).
 template <int LOGN, int LOGL, int R, int TM, bool INJ, int IN_T, int G>
 static void enc_go_g(const LayerRun& r, const uint64_t* key, uint32_t key_stride, const void* in, uint64_t* out,
                      int items) {
   if constexpr (LOGN == 11 && R == 1 && TM != TILE_WEIGHTS) {
     if (items <= r.ctx->sm_count)
-      return enc_go_t<LOGN, LOGL, R, TM, INJ, IN_T, G, 1>(r, key, key_stride, in, out, items);
+      return enc_go_t<LOGN, LOGL, R, TM, INJ, IN_T, G, 2>(r, key, key_stride, in, out, items);
   }
   enc_go_t<LOGN, LOGL, R, TM, INJ, IN_T, G, 0>(r, key, key_stride, in, out, items);
 }
@@ -103,8 +112,8 @@ void launch_tile(const LayerRun& r, int tm, bool inj, int in_t, const uint64_t* 
 template <int LOGN, int LOGL, int R, bool INJ, int G, int TWS>
 static void share_go_t(const LayerRun& r, uint64_t* ct_out, uint32_t* bob_share, int items) {
   auto k = share_kernel<LOGN, LOGL, LOGL, R, INJ, G, TWS>;
-  const size_t smem = share_smem<LOGN, LOGL, LOGL, G>(r.a.B) + tw_stage_bytes<LOGN, TWS>();
-  set_smem(k, smem);
+  const size_t smem = share_smem<LOGN, LOGL, LOGL, G, TWS == 2>(r.a.B) + tw_stage_bytes<LOGN, TWS>();
+  set_smem_shared_sm(k, smem);
   k<<<items, G * ((1 << LOGN) >> tile_loge(LOGN)), smem, r.st>>>(r.a, ct_out, bob_share);
   check_launch("share_kernel");
 }
@@ -112,7 +121,7 @@ static void share_go_t(const LayerRun& r, uint64_t* ct_out, uint32_t* bob_share,
 template <int LOGN, int LOGL, int R, bool INJ, int G>
 static void share_go_g(const LayerRun& r, uint64_t* ct_out, uint32_t* bob_share, int items) {
   if constexpr (LOGN == 11 && R == 1) {  // q-table staging for single-wave launches (as Enc)
-    if (items <= r.ctx->sm_count) return share_go_t<LOGN, LOGL, R, INJ, G, 1>(r, ct_out, bob_share, items);
+    if (items <= r.ctx->sm_count) return share_go_t<LOGN, LOGL, R, INJ, G, 2>(r, ct_out, bob_share, items);
   }
   share_go_t<LOGN, LOGL, R, INJ, G, 0>(r, ct_out, bob_share, items);
 }

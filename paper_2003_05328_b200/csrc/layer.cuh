@@ -148,6 +148,16 @@ struct GroupBar {
 
 enum TileMode { TILE_ENC = 0, TILE_HOMREC = 1, TILE_WEIGHTS = 2 };
 
+// Programmatic dependent launch (the layer's Enc -> ElementMult -> Dec chain): a kernel
+// launched with programmatic stream serialization may start while its predecessor in
+// the stream still runs; pdl_wait() blocks until that predecessor grid has completed
+// and its writes are visible, so everything before it (table staging, key loads,
+// weight tiles, launch latency) overlaps the predecessor's tail.  pdl_trigger() lets
+// the dependent grid launch once every CTA of this grid has called it.  Both are no-ops
+// for ordinary launches.
+EG_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+EG_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Twiddle staging (TWS): a tile kernel walks three read-only tables -- the n-point
 // negacyclic table over q, the one over p and the 64-point cyclic table of its 2D
 // transform.  Read through L1 they were the top stall reason of the latency-bound tile
@@ -228,6 +238,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
   const int ch = item % a.cin;
   const int img = item / a.cin;  // image (or output channel for WEIGHTS)
   const int th = TM == TILE_WEIGHTS ? a.fh : a.H, tw = TM == TILE_WEIGHTS ? a.fw : a.W;
+  pdl_trigger();  // the ElementMult may launch now; its pdl_wait() covers this grid's writes
   __shared__ uint64_t tw_bar;
   TwStage tws{a.twq_fwd[0], a.twp_inv, a.twc_fwd};
   if constexpr (TWS)
@@ -569,13 +580,20 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)))
   if constexpr (STG) {
     const uint64_t* cg = ct + (size_t)item * a.B * ct_words<1>(N);
     const int narr = 2 + 2 * a.B;  // N-word arrays: t^, t^', then c0, c1 per block
-    for (int e = threadIdx.x; e < narr * (N / 2); e += blockDim.x) {
+    for (int e = threadIdx.x; e < 2 * (N / 2); e += blockDim.x) {  // the key: independent of the MAC
       const int arr = e / (N / 2), c = e % (N / 2);
-      const uint64_t* g0 = arr < 2 ? kimg + (size_t)arr * N : cg + (size_t)(arr - 2) * N;
-      cp_async16(kst + (size_t)arr * N + sidx<uint64_t>(2 * c), g0 + 2 * c);
+      cp_async16(kst + (size_t)arr * N + sidx<uint64_t>(2 * c), kimg + (size_t)arr * N + 2 * c);
+    }
+    cp_async_commit();
+    pdl_wait();  // the ElementMult's output ciphertexts
+    for (int e = threadIdx.x + 2 * (N / 2); e < narr * (N / 2); e += blockDim.x) {
+      const int arr = e / (N / 2), c = e % (N / 2);
+      cp_async16(kst + (size_t)arr * N + sidx<uint64_t>(2 * c), cg + (size_t)(arr - 2) * N + 2 * c);
     }
     cp_async_commit();
     cp_async_wait_all();
+  } else {
+    pdl_wait();
   }
   __syncthreads();
   if constexpr (TWS) mbar_wait(&tw_bar, 0);
@@ -656,6 +674,8 @@ template <int R, int S, int MT, int NT, int KT, int TM, int TN>
 __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN))
     mac_kernel(LayerArgs a, int logn, const uint64_t* __restrict__ ct, const uint64_t* __restrict__ w,
                int has_mask, uint64_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NTH = S * (MT / TM) * (NT / TN);
   constexpr int SV = S / 2;  // 16-byte chunks per (k, row)
   extern __shared__ __align__(16) uint64_t smac[];
@@ -902,6 +922,8 @@ __global__ void __launch_bounds__(S*(MT / TM) * (NT / TN), (512 / (S * (MT / TM)
   const int nchunks = (K + KT - 1) / KT;
   const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int nsteps = my_tiles * nchunks;
+  pdl_wait();     // ciphertexts from Enc / HomRec, masks from HomShare
+  pdl_trigger();  // Dec may launch and stage its tables and key meanwhile
   const int tid = threadIdx.x;
   const int sl = tid % S, tm = (tid / S) % (MT / TM), tn = tid / (S * (MT / TM));
   const size_t ctw = (size_t)ct_words<R>(n);
@@ -1131,6 +1153,8 @@ template <int R>
 __global__ void __launch_bounds__(256)
     mac_direct_kernel(LayerArgs a, int logn, const uint64_t* __restrict__ ct, const uint64_t* __restrict__ w,
                       int has_mask, uint64_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   typedef unsigned __int128 u128;
   const int n = 1 << logn;
   const size_t slots = (size_t)a.B * R * n;  // per image: (block, prime, slot)

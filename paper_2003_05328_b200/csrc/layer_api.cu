@@ -172,7 +172,7 @@ void mac_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* 
   constexpr size_t smem = mac_smem<S, MT, NT, KT>();
   set_smem(k, smem);
   dim3 grid((unsigned)(r.a.B * R * n / S), (unsigned)((rows + MT - 1) / MT), (unsigned)((cols + NT - 1) / NT));
-  k<<<grid, S * (MT / TM) * (NT / TN), smem, r.st>>>(r.a, (int)r.ctx->logn, ct, w, 1, out);
+  launch_pdl(k, grid, S * (MT / TM) * (NT / TN), smem, r.st, r.a, (int)r.ctx->logn, ct, w, 1, out);
   check_launch("mac_kernel");
 }
 
@@ -186,7 +186,7 @@ void mac_kara_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint6
   static int per_sm = -1;  // per instantiation; the launch config never changes
   if (per_sm < 0) EG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, S * (MT / TM) * (NT / TN), smem));
   const long grid = std::min<long>(tiles, (long)std::max(per_sm, 1) * r.ctx->sm_count);
-  k<<<(unsigned)grid, S * (MT / TM) * (NT / TN), smem, r.st>>>(r.a, (int)r.ctx->logn, ct, w, 1, out, 0u);
+  launch_pdl(k, (unsigned)grid, S * (MT / TM) * (NT / TN), smem, r.st, r.a, (int)r.ctx->logn, ct, w, 1, out, 0u);
   check_launch("mac_kara_kernel");
 }
 
@@ -208,7 +208,7 @@ template <int R>
 void mac_direct_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
   const size_t total = (size_t)r.a.num_images * r.a.B * R * r.ctx->n;
   const long grid = std::min<long>((long)((total + 255) / 256), (long)r.ctx->sm_count * 8);
-  mac_direct_kernel<R><<<(unsigned)grid, 256, 0, r.st>>>(r.a, (int)r.ctx->logn, ct, w, 1, out);
+  launch_pdl(mac_direct_kernel<R>, (unsigned)grid, 256, 0, r.st, r.a, (int)r.ctx->logn, ct, w, 1, out);
   check_launch("mac_direct_kernel");
 }
 

@@ -14,6 +14,27 @@ struct LayerRun {
   cudaStream_t st;
 };
 
+// Launch with programmatic stream serialization (layer.cuh, pdl_wait / pdl_trigger):
+// the kernel may start while its stream predecessor still runs.  Falls back to an
+// ordinary launch where the attribute is refused.
+template <class... KArgs, class... Args>
+static void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, k, args...) != cudaSuccess) {
+    cudaGetLastError();
+    k<<<grid, block, smem, st>>>(args...);
+  }
+}
+
 template <class K>
 static void set_smem(K k, size_t smem) {
   if (smem > 48 * 1024) EG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -172,15 +193,15 @@ static void dec_go_g(const LayerRun& r, const uint64_t* key, uint32_t ks, const 
   if (LOGN == 11 && items <= r.ctx->sm_count && staged + twb <= 227 * 1024) {  // + staged twiddles (TWS)
     auto k = dec_kernel<LOGN, LOGL, LOGL, G, true, LOGN == 11 ? 2 : 0>;
     set_smem(k, staged + twb);
-    k<<<items, G * ((1 << LOGN) >> tile_loge(LOGN)), staged + twb, r.st>>>(r.a, key, ks, ct, alice, bob, out);
+    launch_pdl(k, items, G * ((1 << LOGN) >> tile_loge(LOGN)), staged + twb, r.st, r.a, key, ks, ct, alice, bob, out);
   } else if (staged <= 227 * 1024) {
     auto k = dec_kernel<LOGN, LOGL, LOGL, G, true>;
     set_smem(k, staged);
-    k<<<items, G * ((1 << LOGN) >> tile_loge(LOGN)), staged, r.st>>>(r.a, key, ks, ct, alice, bob, out);
+    launch_pdl(k, items, G * ((1 << LOGN) >> tile_loge(LOGN)), staged, r.st, r.a, key, ks, ct, alice, bob, out);
   } else {
     auto k = dec_kernel<LOGN, LOGL, LOGL, G, false>;
     set_smem(k, base);
-    k<<<items, G * ((1 << LOGN) >> tile_loge(LOGN)), base, r.st>>>(r.a, key, ks, ct, alice, bob, out);
+    launch_pdl(k, items, G * ((1 << LOGN) >> tile_loge(LOGN)), base, r.st, r.a, key, ks, ct, alice, bob, out);
   }
   check_launch("dec_kernel");
 }

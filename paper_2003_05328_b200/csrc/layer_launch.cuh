@@ -72,7 +72,9 @@ template <int LOGN, int LOGL, int R, int TM, bool INJ, int IN_T, int G>
 static void enc_go_g(const LayerRun& r, const uint64_t* key, uint32_t key_stride, const void* in, uint64_t* out,
                      int items) {
   if constexpr (LOGN == 11 && R == 1 && TM != TILE_WEIGHTS) {
-    if (items <= r.ctx->sm_count)
+    // two groups: registers already hold the kernel to 2 CTAs per SM, and two staged
+    // CTAs (2 x 103 KB) still fit -- staging is free at any launch size
+    if (G == 2 || items <= r.ctx->sm_count)
       return enc_go_t<LOGN, LOGL, R, TM, INJ, IN_T, G, 2>(r, key, key_stride, in, out, items);
   }
   enc_go_t<LOGN, LOGL, R, TM, INJ, IN_T, G, 0>(r, key, key_stride, in, out, items);
@@ -190,7 +192,8 @@ static void dec_go_g(const LayerRun& r, const uint64_t* key, uint32_t ks, const 
   constexpr size_t base = dec_smem<LOGN, LOGL, LOGL, G>();
   const size_t staged = base + (size_t)(2 + 2 * r.a.B) * (1 << LOGN) * 8;  // + t^, t^', c0/c1 per block
   constexpr size_t twb = tw_stage_bytes<LOGN, 2>();
-  if (LOGN == 11 && items <= r.ctx->sm_count && staged + twb <= 227 * 1024) {  // + staged twiddles (TWS)
+  // + staged twiddles (TWS): free when registers allow one CTA per SM anyway (G = 2)
+  if (LOGN == 11 && (G == 2 || items <= r.ctx->sm_count) && staged + twb <= 227 * 1024) {
     auto k = dec_kernel<LOGN, LOGL, LOGL, G, true, LOGN == 11 ? 2 : 0>;
     set_smem(k, staged + twb);
     launch_pdl(k, items, G * ((1 << LOGN) >> tile_loge(LOGN)), staged + twb, r.st, r.a, key, ks, ct, alice, bob, out);

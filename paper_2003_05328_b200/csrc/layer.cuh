@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
   static_assert(!TWS || R == 1, "twiddle staging: single prime");
   constexpr int N = 1 << LOGN, NT = N >> tile_loge(LOGN);
   constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
-  constexpr bool ALIAS = TWS == 2;  // p buffer inside the q buffer (see tile_enc_smem)
+  constexpr bool ALIAS = TWS != 0;  // p buffer inside the q buffer (see tile_enc_smem)
   constexpr size_t GROUP_BYTES = (size_t)N * 8 + (ALIAS ? 0 : ssize<uint32_t>(N) * 4);
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);

@@ -135,7 +135,7 @@ void launch_tile(const LayerRun& r, int tm, bool inj, int in_t, const uint64_t* 
 template <int LOGN, int LOGL, int R, bool INJ, int G, int TWS>
 static void share_go_t(const LayerRun& r, uint64_t* ct_out, uint32_t* bob_share, int items) {
   auto k = share_kernel<LOGN, LOGL, LOGL, R, INJ, G, TWS>;
-  const size_t smem = share_smem<LOGN, LOGL, LOGL, G, TWS == 2>(r.a.B) + tw_stage_bytes<LOGN, TWS>();
+  const size_t smem = share_smem<LOGN, LOGL, LOGL, G, TWS != 0>(r.a.B) + tw_stage_bytes<LOGN, TWS>();
   set_smem_shared_sm(k, smem);
   k<<<items, G * ((1 << LOGN) >> tile_loge(LOGN)), smem, r.st>>>(r.a, ct_out, bob_share);
   check_launch("share_kernel");
@@ -145,6 +145,8 @@ template <int LOGN, int LOGL, int R, bool INJ, int G>
 static void share_go_g(const LayerRun& r, uint64_t* ct_out, uint32_t* bob_share, int items) {
   if constexpr (LOGN == 11 && R == 1) {  // q-table staging for single-wave launches (as Enc)
     if (items <= r.ctx->sm_count) return share_go_t<LOGN, LOGL, R, INJ, G, 2>(r, ct_out, bob_share, items);
+    // multi-wave, two groups: the q table alone keeps two CTAs per SM (2 x 97 KB)
+    if (G == 2) return share_go_t<LOGN, LOGL, R, INJ, G, 1>(r, ct_out, bob_share, items);
   }
   share_go_t<LOGN, LOGL, R, INJ, G, 0>(r, ct_out, bob_share, items);
 }

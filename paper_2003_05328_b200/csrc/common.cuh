@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -101,7 +102,10 @@ struct ensei_gpu_ctx {
   std::vector<uint8_t> host_graph_key;
   // wire decoding (wire.cu): mapped pinned status block [first-error key, domain flags,
   // per-record domain tags], grown on demand; read by the host after the decode kernels
+  // (one decode at a time per context: the two parties of an in-process session decode
+  // from two host threads)
   uint8_t* wire_status = nullptr;
   size_t wire_status_cap = 0;
+  std::mutex wire_mu;
 
 };

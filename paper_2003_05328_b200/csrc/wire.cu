@@ -478,6 +478,7 @@ int ensei_gpu_wire_decode_ct_blocks(ensei_gpu_ctx* ctx, const uint8_t* frames, s
     const uint64_t avail = frame_len >= kCtHdr ? std::min<uint64_t>(recs, (frame_len - kCtHdr) / rb) : 0;
     const uint64_t frame_key = E_RECORDS + (uint64_t)recs * (2 * n + 2);
     const cudaStream_t st = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lock(ctx->wire_mu);
     StatusView sv = status_view(ctx, num_frames, (uint64_t)num_frames * recs);
     reset_status(ctx, st);
     const size_t smem = 16ull * n;
@@ -572,6 +573,7 @@ int ensei_gpu_wire_decode_shares(ensei_gpu_ctx* ctx, const uint8_t* frames, size
     const uint64_t avail = frame_len >= kShareHdr ? std::min<uint64_t>(cnt, (frame_len - kShareHdr) / 8) : 0;
     const uint64_t frame_key = E_RECORDS + cnt + 1;
     const cudaStream_t st = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lock(ctx->wire_mu);
     StatusView sv = status_view(ctx, num_frames, 0);
     reset_status(ctx, st);
     const unsigned gx = (unsigned)std::max<uint64_t>(

@@ -382,3 +382,33 @@ def test_product_parity_mode_batched_sessions(W, ops):
         assert bob.transcripts[i].content_hash_sent == int(h[2]) and bob.transcripts[i].content_hash_recv == int(h[3])
         assert alice.transcripts[i].total_bytes("sent") == int(h[4])
         assert bob.transcripts[i].total_bytes("sent") == int(h[5])
+
+
+def test_concurrent_decodes_keep_their_own_status(W, ops):
+    """The two parties of run_inproc decode from two host threads on one context: each
+    decode must report its own frames' errors (the status block is per-context)."""
+    import threading
+    n, ch, B = 2048, 2, 1
+    ctx = ctx_for(ops, n)
+    rng = np.random.default_rng(21)
+    nat = rng.integers(0, Q, size=(ch, B, 2, n), dtype=np.uint64)
+    good = ref_ct_frame(W, W.CIPHERTEXT_BLOCKS, 0, n, nat, 1)
+    bad = _corruptions(W, good, n, ch, B)["coef_eq_q"]
+    res = {"good": [], "bad": []}
+
+    def run(name, frame):
+        t = torch.from_numpy(frame).reshape(1, -1).pin_memory()
+        for _ in range(40):
+            try:
+                W.decode_ct_blocks(ctx, t, W.CIPHERTEXT_BLOCKS, ch, B)
+                res[name].append(None)
+            except W.EnseiError as e:
+                res[name].append(e.kind)
+
+    th = [threading.Thread(target=run, args=("good", good)), threading.Thread(target=run, args=("bad", bad))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert res["good"] == [None] * 40
+    assert res["bad"] == ["MalformedPayload"] * 40

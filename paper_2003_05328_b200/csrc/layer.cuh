@@ -573,6 +573,17 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)))
   const uint64_t cp = pc.cp, h = f.q >> 1;  // floor(p 2^64 / q), floor(q / 2)
   uint64_t* kst = reinterpret_cast<uint64_t*>(smem_raw + dec_smem<LOGN, LOGH, LOGW, G>());  // [t^][t^'][B][c0][c1]
   __shared__ uint64_t tw_bar;
+  // Bob's share for the final recombination, fetched now: HomShare finished before the
+  // ElementMult started, so it is visible here, and the load latency hides behind the
+  // transforms instead of stalling the crop loop
+  constexpr int kBobPre = 4;
+  const size_t obase = (size_t)item * a.oh * a.ow;
+  uint32_t bob_pre[kBobPre];
+#pragma unroll
+  for (int k = 0; k < kBobPre; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    bob_pre[k] = (outp && i < a.oh * a.ow) ? __ldg(bob_share + obase + i) : 0u;
+  }
   TwStage tws{a.twq_inv[0], a.twp_fwd, a.twc_inv};
   if constexpr (TWS)  // tables after the staged arrays
     tws = tw_stage_issue<LOGN, TWS>(reinterpret_cast<uint8_t*>(kst + (STG ? (size_t)(2 + 2 * a.B) * N : 0)), &tw_bar,
@@ -632,14 +643,19 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)))
   __syncthreads();
   // IDFT2D + crop (+ recombine with Bob's share)
   tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, tws.c, S, LS);
-  const size_t base = (size_t)item * a.oh * a.ow;
-  for (int i = threadIdx.x; i < a.oh * a.ow; i += blockDim.x) {
+  int k = 0;
+  for (int i = threadIdx.x; i < a.oh * a.ow; i += blockDim.x, ++k) {
     const int r = i / a.ow, c = i % a.ow;
     const uint32_t s = S[(r + a.r0) * LS + c + a.c0];
-    if (alice_share) alice_share[base + i] = s;
+    if (alice_share) alice_share[obase + i] = s;
     if (outp) {
-      uint32_t y = s + bob_share[base + i];
-      outp[base + i] = y >= p ? y - p : y;
+      uint32_t bv = bob_pre[0];
+#pragma unroll
+      for (int u = 1; u < kBobPre; ++u)
+        if (k == u) bv = bob_pre[u];
+      if (k >= kBobPre) bv = bob_share[obase + i];
+      uint32_t y = s + bv;
+      outp[obase + i] = y >= p ? y - p : y;
     }
   }
 }

@@ -216,6 +216,11 @@ int ensei_gpu_activation(ensei_gpu_ctx* ctx, int fn, int pool2, uint32_t channel
                          const ensei_randomness* rand, uint32_t* d_new_a, uint32_t* d_new_b,
                          int* d_overflow, void* stream);
 
+/* ElementMult implementation (tuning / A-B testing; results are identical):
+ * -1 automatic (default), 0 the 4-product IMAD kernel, 1 the Karatsuba IMAD kernel,
+ * 2 the int8 tensor-core kernel (exact byte-plane products, cin <= 255). */
+int ensei_gpu_set_mac_variant(int variant);
+
 /* recombine_clear (REF hss.cpp:64-73): out = (a + b) mod p */
 int ensei_gpu_recombine(ensei_gpu_ctx* ctx, const uint32_t* d_a, const uint32_t* d_b, size_t count,
                         uint32_t* d_out, void* stream);

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "layer_launch.cuh"
+#include "mac_i8.cuh"
 
 namespace ensei_gpu {
 
@@ -190,11 +191,17 @@ void mac_kara_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint6
   check_launch("mac_kara_kernel");
 }
 
+// ElementMult implementation: -1 automatic (default), 0 the 4-product IMAD kernel, 1 the
+// Karatsuba IMAD kernel, 2 the int8 tensor-core kernel (mac_i8.cuh).  ENSEI_MAC_VARIANT
+// or ensei_gpu_set_mac_variant() override the automatic choice.
+static std::atomic<int> g_mac_variant{-2};
 static int mac_variant() {
-  static int v = [] {
+  int v = g_mac_variant.load(std::memory_order_relaxed);
+  if (v == -2) {
     const char* e = getenv("ENSEI_MAC_VARIANT");
-    return e ? atoi(e) : 1;
-  }();
+    v = e ? atoi(e) : -1;
+    g_mac_variant.store(v, std::memory_order_relaxed);
+  }
   return v;
 }
 
@@ -213,12 +220,27 @@ void mac_direct_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uin
 }
 
 template <int R>
+void mac_i8_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
+  const int n = (int)r.ctx->n, rows = 2 * r.a.num_images, cols = r.a.cout;
+  const long tasks = (long)(r.a.B * R * n / kI8Slots) * ((rows + kI8Rows - 1) / kI8Rows) *
+                     ((cols + kI8Cols - 1) / kI8Cols);
+  auto k = mac_i8_kernel<R>;
+  static int per_sm = -1;
+  if (per_sm < 0) EG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0));
+  const long grid = std::min<long>(tasks, (long)std::max(per_sm, 1) * r.ctx->sm_count);
+  launch_pdl(k, (unsigned)grid, 256, 0, r.st, r.a, (int)r.ctx->logn, ct, w, 1, out);
+  check_launch("mac_i8_kernel");
+}
+
+template <int R>
 void mac_r(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
   const int rows = 2 * r.a.num_images, cols = r.a.cout;
   const bool small = rows <= 16 && cols <= 16;
+  const int var = mac_variant();
+  if (var == 2 && r.a.cin <= kI8MaxK) return mac_i8_go<R>(r, ct, w, out);
   // tiny channel counts (config 0: 1 -> 1): direct per-slot kernel (exact while cin <= 1008)
   if (r.a.cout <= 2 && r.a.cin <= 4) return mac_direct_go<R>(r, ct, w, out);
-  if (!r.ctx->kara_ok || mac_variant() == 0) {
+  if (!r.ctx->kara_ok || var == 0) {
     if (small) return mac_go<R, 16, 16, 16, 16, 2, 4>(r, ct, w, out);
     return mac_go<R, 8, 32, 32, 16, 4, 4>(r, ct, w, out);
   }
@@ -481,6 +503,13 @@ int ensei_gpu_activation(ensei_gpu_ctx* ctx, int fn, int pool2, uint32_t channel
         rand ? rand->image_base : 0, rand ? rand->alice_key : 0, inj ? rand->d_share : nullptr, d_new_a, d_new_b,
         d_overflow);
     check_launch("activation_kernel");
+  });
+}
+
+int ensei_gpu_set_mac_variant(int variant) {
+  return guarded([&] {
+    require(variant >= -1 && variant <= 2, ENSEI_ERR_INVALID_ARGUMENT, "variant must be -1, 0, 1 or 2");
+    g_mac_variant.store(variant, std::memory_order_relaxed);
   });
 }
 

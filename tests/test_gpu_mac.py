@@ -94,3 +94,21 @@ def test_bob_mac_four_product_fallback():
                         "-k", "test_bob_mac_exact"], env=env, capture_output=True, text=True, timeout=900,
                        cwd=os.path.dirname(here))
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+I8_CASES = [c for c in CASES if c[2] <= 255] + [
+    (2048, 8, 255, 16, 1),        # the int8 path's K limit (T < 2^128)
+    (2048, 17, 33, 40, 1),        # one channel past a 32-channel chunk; partial row / col tiles
+    (8192, 64, 64, 32, 3),        # config-4 shape class (three primes)
+]
+
+
+@pytest.mark.parametrize("n,images,cin,cout,R", I8_CASES)
+def test_bob_mac_int8_tensor_cores_exact(ops, n, images, cin, cout, R):
+    """The int8 tensor-core ElementMult (mac_i8.cuh, variant 2) on the same exact checks."""
+    from paper_2003_05328_b200._lib import check, lib
+    check(lib().ensei_gpu_set_mac_variant(2))
+    try:
+        test_bob_mac_exact(ops, n, images, cin, cout, R)
+    finally:
+        check(lib().ensei_gpu_set_mac_variant(-1))

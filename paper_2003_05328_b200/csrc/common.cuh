@@ -107,5 +107,8 @@ struct ensei_gpu_ctx {
   uint8_t* wire_status = nullptr;
   size_t wire_status_cap = 0;
   std::mutex wire_mu;
+  // int8 tensor-core ElementMult: byte-plane operands (mac_i8.cuh), grown on demand
+  void* i8_scratch = nullptr;
+  size_t i8_scratch_cap = 0;
 
 };

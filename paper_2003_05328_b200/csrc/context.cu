@@ -182,7 +182,8 @@ void ensei_gpu_ctx_destroy(ensei_gpu_ctx* ctx) {
   if (ctx->host_graph) cudaGraphExecDestroy(ctx->host_graph);
   if (ctx->host_st) cudaStreamDestroy(ctx->host_st);
   if (ctx->host_ev) cudaEventDestroy(ctx->host_ev);
-  if (ctx->wire_status) cudaFreeHost(ctx->wire_status);
+  if (ctx->wire_status) cudaFree(ctx->wire_status);
+  if (ctx->i8_scratch) cudaFree(ctx->i8_scratch);
   delete ctx;
 }
 

@@ -232,12 +232,52 @@ void mac_i8_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_
   check_launch("mac_i8_kernel");
 }
 
+// Byte planes + cp.async pipeline (mac_i8p_kernel).  False when the plane scratch
+// cannot be provided (it grows on demand, which a stream under graph capture cannot do).
+template <int R>
+bool mac_i8p_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
+  ensei_gpu_ctx* ctx = const_cast<ensei_gpu_ctx*>(r.ctx);
+  const int n = (int)ctx->n, rows = 2 * r.a.num_images, cols = r.a.cout, K = r.a.cin;
+  const size_t aw = (size_t)i8_plane_words(r.a.B, R, n, K, rows), bw = (size_t)i8_plane_words(r.a.B, R, n, K, cols);
+  const size_t need = (aw + bw) * sizeof(uint32_t);
+  if (need > ctx->i8_scratch_cap) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    EG_CUDA(cudaStreamIsCapturing(r.st, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return false;
+    if (ctx->i8_scratch) EG_CUDA(cudaFree(ctx->i8_scratch));
+    ctx->i8_scratch = nullptr;
+    ctx->i8_scratch_cap = 0;
+    EG_CUDA(cudaMalloc(&ctx->i8_scratch, need));
+    ctx->i8_scratch_cap = need;
+  }
+  uint32_t* Ap = static_cast<uint32_t*>(ctx->i8_scratch);
+  uint32_t* Bp = Ap + aw;
+  const unsigned pg = (unsigned)ctx->sm_count * 8;
+  planes_kernel<R, false><<<pg, 256, 0, r.st>>>(r.a, (int)ctx->logn, ct, Ap, rows);
+  check_launch("planes_kernel");
+  planes_kernel<R, true><<<pg, 256, 0, r.st>>>(r.a, (int)ctx->logn, w, Bp, cols);
+  check_launch("planes_kernel");
+  constexpr int STAGES = 3;
+  constexpr size_t smem = (size_t)STAGES * 2 * kI8TileWords * sizeof(uint32_t);
+  auto k = mac_i8p_kernel<R, STAGES>;
+  set_smem(k, smem);
+  static int per_sm = -1;
+  if (per_sm < 0) EG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem));
+  const long tasks = (long)(r.a.B * R * n / kI8Slots) * ((rows + kI8Rows - 1) / kI8Rows) *
+                     ((cols + kI8Cols - 1) / kI8Cols);
+  const long grid = std::min<long>(tasks, (long)std::max(per_sm, 1) * ctx->sm_count);
+  k<<<(unsigned)grid, 256, smem, r.st>>>(r.a, (int)ctx->logn, Ap, Bp, 1, out);
+  check_launch("mac_i8p_kernel");
+  return true;
+}
+
 template <int R>
 void mac_r(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
   const int rows = 2 * r.a.num_images, cols = r.a.cout;
   const bool small = rows <= 16 && cols <= 16;
   const int var = mac_variant();
-  if (var == 2 && r.a.cin <= kI8MaxK) return mac_i8_go<R>(r, ct, w, out);
+  if (var == 3 && r.a.cin <= kI8MaxK) return mac_i8_go<R>(r, ct, w, out);
+  if (var == 2 && r.a.cin <= kI8MaxK && mac_i8p_go<R>(r, ct, w, out)) return;
   // tiny channel counts (config 0: 1 -> 1): direct per-slot kernel (exact while cin <= 1008)
   if (r.a.cout <= 2 && r.a.cin <= 4) return mac_direct_go<R>(r, ct, w, out);
   if (!r.ctx->kara_ok || var == 0) {
@@ -508,7 +548,7 @@ int ensei_gpu_activation(ensei_gpu_ctx* ctx, int fn, int pool2, uint32_t channel
 
 int ensei_gpu_set_mac_variant(int variant) {
   return guarded([&] {
-    require(variant >= -1 && variant <= 2, ENSEI_ERR_INVALID_ARGUMENT, "variant must be -1, 0, 1 or 2");
+    require(variant >= -1 && variant <= 3, ENSEI_ERR_INVALID_ARGUMENT, "variant must be -1 .. 3");
     g_mac_variant.store(variant, std::memory_order_relaxed);
   });
 }

@@ -257,14 +257,13 @@ bool mac_i8p_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64
   check_launch("planes_kernel");
   planes_kernel<R, true><<<pg, 256, 0, r.st>>>(r.a, (int)ctx->logn, w, Bp, cols);
   check_launch("planes_kernel");
-  constexpr int STAGES = 3;
-  constexpr size_t smem = (size_t)STAGES * 2 * kI8TileWords * sizeof(uint32_t);
+  constexpr int STAGES = 4;
+  constexpr size_t smem = (size_t)STAGES * 2 * 8 * kI8T * 8 * sizeof(uint32_t);
   auto k = mac_i8p_kernel<R, STAGES>;
   set_smem(k, smem);
   static int per_sm = -1;
   if (per_sm < 0) EG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem));
-  const long tasks = (long)(r.a.B * R * n / kI8Slots) * ((rows + kI8Rows - 1) / kI8Rows) *
-                     ((cols + kI8Cols - 1) / kI8Cols);
+  const long tasks = (long)r.a.B * R * n * ((rows + kI8T - 1) / kI8T) * ((cols + kI8T - 1) / kI8T);
   const long grid = std::min<long>(tasks, (long)std::max(per_sm, 1) * ctx->sm_count);
   k<<<(unsigned)grid, 256, smem, r.st>>>(r.a, (int)ctx->logn, Ap, Bp, 1, out);
   check_launch("mac_i8p_kernel");

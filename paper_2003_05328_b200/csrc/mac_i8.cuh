@@ -195,15 +195,18 @@ namespace ensei_gpu {
 // Byte-plane operands prepared once per call (planes_kernel), then a cp.async
 // pipeline feeding the tensor cores (mac_i8p_kernel).  Global plane layout, for the
 // ciphertexts (rc = row = image x component) and the weights (rc = out channel):
-//   [bp][slot group of 4][32-channel chunk kc][rc (padded to 16)][slot s][plane][8 words]
-// (8 words = 32 channel bytes), so a task's chunk -- 16 rows (or cols) x 4 slots x
-// 8 planes -- is one contiguous 16 KB block.  Conversions: each ciphertext word once
+//   [bp][slot][32-channel chunk kc][rc (padded to 32)][plane][8 words]
+// (8 words = 32 channel bytes), so a task's chunk -- 32 rows (or cols) x 8 planes of
+// one slot -- is one contiguous 8 KB block.  The pre-pass reads 4 slots (a 32-byte
+// sector) per (row, channel) and scatters them to their slots.  Conversions: each ciphertext word once
 // (instead of once per column tile) and each weight once per call (instead of once per
 // row tile); the MAC kernel does no conversion, only 16-byte copies, MMA and epilogue.
 
+constexpr int kI8T = 32;  // rows and cols per task of mac_i8p_kernel
+
 __host__ __device__ inline long i8_plane_words(int B, int R, int n, int K, int nrc) {
-  const long nsg = n / kI8Slots, nkc = (K + kI8K - 1) / kI8K, rcp = (nrc + kI8Rows - 1) / kI8Rows * kI8Rows;
-  return (long)B * R * nsg * nkc * rcp * (kI8Slots * 8 * 8);
+  const long nkc = (K + kI8K - 1) / kI8K, rcp = (nrc + kI8T - 1) / kI8T * kI8T;
+  return (long)B * R * n * nkc * rcp * 64;
 }
 
 template <int R, bool WEIGHTS>
@@ -211,7 +214,7 @@ __global__ void __launch_bounds__(256) planes_kernel(LayerArgs a, int logn, cons
                                                      uint32_t* __restrict__ dst, int nrc) {
   const int n = 1 << logn, K = a.cin;
   const long nsg = n / kI8Slots, nkc = (K + kI8K - 1) / kI8K;
-  const int rcp = (nrc + kI8Rows - 1) / kI8Rows * kI8Rows;
+  const int rcp = (nrc + kI8T - 1) / kI8T * kI8T;
   const long total = (long)a.B * R * nsg * nkc * rcp * 8;
   const size_t ctw = (size_t)2 * R * n, chan_stride = (size_t)a.B * ctw, w_chan = (size_t)a.B * R * n;
   constexpr uint64_t M30 = (1ull << 30) - 1;
@@ -248,13 +251,14 @@ __global__ void __launch_bounds__(256) planes_kernel(LayerArgs a, int logn, cons
       lo[m][2] = lo32(v23.x), hi[m][2] = hi32(v23.x);
       lo[m][3] = lo32(v23.y), hi[m][3] = hi32(v23.y);
     }
-    uint32_t* o = dst + ((((long)bp * nsg + sg) * nkc + kc) * rcp + rc) * (kI8Slots * 64);
 #pragma unroll
-    for (int s = 0; s < kI8Slots; ++s)
+    for (int s = 0; s < kI8Slots; ++s) {
+      uint32_t* o = dst + ((((long)bp * n + j0 + s) * nkc + kc) * rcp + rc) * 64;
 #pragma unroll
       for (int i = 0; i < 8; ++i)
-        o[(s * 8 + i) * 8 + q] = i < 4 ? plane_word(lo[0][s], lo[1][s], lo[2][s], lo[3][s], i)
-                                       : plane_word(hi[0][s], hi[1][s], hi[2][s], hi[3][s], i - 4);
+        o[i * 8 + q] = i < 4 ? plane_word(lo[0][s], lo[1][s], lo[2][s], lo[3][s], i)
+                             : plane_word(hi[0][s], hi[1][s], hi[2][s], hi[3][s], i - 4);
+    }
   }
 }
 
@@ -262,27 +266,28 @@ template <int R, int STAGES>
 __global__ void __launch_bounds__(256, 2)
     mac_i8p_kernel(LayerArgs a, int logn, const uint32_t* __restrict__ Ap, const uint32_t* __restrict__ Bp,
                    int has_mask, uint64_t* __restrict__ out) {
+  // task = (slot, 32-row tile, 32-col tile); warp w owns the 16x8 tile at rows
+  // 16 (w >> 2), cols 8 (w & 3) of it.  Stage = A [plane][32 rows][8 words] | B same.
   pdl_wait();
   pdl_trigger();
-  extern __shared__ __align__(16) uint32_t sm_i8[];  // STAGES x [A tile | B tile]
+  extern __shared__ __align__(16) uint32_t sm_i8[];
+  constexpr int PL = kI8T * 8;           // words per plane of a tile
+  constexpr int TILE = 8 * PL, STAGE = 2 * TILE;
   const int n = 1 << logn;
   const int rows = 2 * a.num_images, cols = a.cout, K = a.cin;
-  const int nrt = (rows + kI8Rows - 1) / kI8Rows, nct = (cols + kI8Cols - 1) / kI8Cols;
-  const long nsg = n / kI8Slots;
+  const int nrt = (rows + kI8T - 1) / kI8T, nct = (cols + kI8T - 1) / kI8T;
   const int nkc = (K + kI8K - 1) / kI8K;
-  const long ntasks = (long)a.B * R * nsg * nrt * nct;
+  const long ntasks = (long)a.B * R * n * nrt * nct;
   const int my_tasks = blockIdx.x < ntasks ? (int)((ntasks - 1 - blockIdx.x) / gridDim.x + 1) : 0;
   const long nsteps = (long)my_tasks * nkc;
   const size_t ctw = (size_t)2 * R * n, chan_stride = (size_t)a.B * ctw;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3, ws = warp >> 1, wn = warp & 1;
-  const long rows_p = (long)nrt * kI8Rows, cols_p = (long)nct * kI8Cols;
-  constexpr int TILE = kI8TileWords, STAGE = 2 * TILE;
+  const int g = lane >> 2, t = lane & 3, wr = warp >> 2, wc = warp & 3;
+  const long rows_p = (long)nrt * kI8T, cols_p = (long)nct * kI8T;
 
-  // task -> (slot group, row tile, col tile), slot group outermost
-  auto task_of = [&](long j, long& grp, int& rt, int& ctile) {
+  auto task_of = [&](long j, long& slot, int& rt, int& ctile) {
     const long tk = blockIdx.x + j * gridDim.x;
-    grp = tk / (nrt * nct);
+    slot = tk / (nrt * nct);  // over B * R * n: (bp, slot) with the slot fastest
     const int rem = (int)(tk % (nrt * nct));
     rt = rem % nrt;
     ctile = rem / nrt;
@@ -291,19 +296,18 @@ __global__ void __launch_bounds__(256, 2)
   int ld_c = 0;
   auto load_step = [&](long step) {
     if (step < nsteps) {
-      long grp;
+      long slot;
       int rt, ctile;
-      task_of(ld_j, grp, rt, ctile);
+      task_of(ld_j, slot, rt, ctile);
       uint32_t* As = sm_i8 + (step % STAGES) * STAGE;
-      uint32_t* Bs = As + TILE;
-      const uint32_t* ag = Ap + ((grp * nkc + ld_c) * rows_p + (long)rt * kI8Rows) * (kI8Slots * 64);
-      const uint32_t* bg = Bp + ((grp * nkc + ld_c) * cols_p + (long)ctile * kI8Cols) * (kI8Slots * 64);
+      const uint32_t* ag = Ap + ((slot * nkc + ld_c) * rows_p + (long)rt * kI8T) * 64;
+      const uint32_t* bg = Bp + ((slot * nkc + ld_c) * cols_p + (long)ctile * kI8T) * 64;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int e = tid + u * 256;           // 0..2047: operand, rc, slot, plane, 16-byte half
-        const int op = e >> 10, rc = (e >> 6) & 15, s = (e >> 4) & 3, pl = (e >> 1) & 7, hf = e & 1;
-        const uint32_t* src = (op ? bg : ag) + rc * 256 + s * 64 + pl * 8 + hf * 4;
-        uint32_t* dsm = (op ? Bs : As) + (s * 8 + pl) * kI8PlaneWords + rc * 8 + ((hf ^ ((rc >> 2) & 1)) << 2);
+      for (int u = 0; u < 4; ++u) {
+        const int e = tid + u * 256;  // 0..1023: operand, rc, plane, 16-byte half
+        const int op = e >> 9, rc = (e >> 4) & 31, pl = (e >> 1) & 7, hf = e & 1;
+        const uint32_t* src = (op ? bg : ag) + rc * 64 + pl * 8 + hf * 4;
+        uint32_t* dsm = As + op * TILE + pl * PL + rc * 8 + ((hf ^ ((rc >> 2) & 1)) << 2);
         cp_async16(dsm, src);
       }
       if (++ld_c == nkc) {
@@ -320,43 +324,42 @@ __global__ void __launch_bounds__(256, 2)
   for (int d = 0; d < 15; ++d) acc[d][0] = acc[d][1] = acc[d][2] = acc[d][3] = 0;
   long cm_j = 0;
   int cm_c = 0;
+  const int ra = wr * 16 + g, cb = wc * 8 + g;                  // fragment row / col in the tile
+  const int sa = ((g >> 2) & 1) << 2;                           // 16-byte half swizzle (rows and cols)
   for (long step = 0; step < nsteps; ++step) {
     load_step(step + STAGES - 1);
     asm volatile("cp.async.wait_group %0;\n" ::"n"(STAGES - 1) : "memory");
     __syncthreads();
     {
-      const uint32_t* as = sm_i8 + (step % STAGES) * STAGE + ws * 8 * kI8PlaneWords;
+      const uint32_t* as = sm_i8 + (step % STAGES) * STAGE;
       const uint32_t* bs = as + TILE;
-      const int bc = wn * 8 + g;
-      const int sa = ((g >> 2) & 1) << 2, sb = ((bc >> 2) & 1) << 2;  // 16-byte half swizzle
       uint32_t bf[8][2];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        bf[j][0] = bs[j * kI8PlaneWords + bc * 8 + (sb ^ 0) + t];
-        bf[j][1] = bs[j * kI8PlaneWords + bc * 8 + (sb ^ 4) + t];
+        bf[j][0] = bs[j * PL + cb * 8 + (sa ^ 0) + t];
+        bf[j][1] = bs[j * PL + cb * 8 + (sa ^ 4) + t];
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         uint32_t af[4];
-        af[0] = as[i * kI8PlaneWords + g * 8 + (sa ^ 0) + t];
-        af[1] = as[i * kI8PlaneWords + (g + 8) * 8 + (sa ^ 0) + t];
-        af[2] = as[i * kI8PlaneWords + g * 8 + (sa ^ 4) + t];
-        af[3] = as[i * kI8PlaneWords + (g + 8) * 8 + (sa ^ 4) + t];
+        af[0] = as[i * PL + ra * 8 + (sa ^ 0) + t];
+        af[1] = as[i * PL + (ra + 8) * 8 + (sa ^ 0) + t];
+        af[2] = as[i * PL + ra * 8 + (sa ^ 4) + t];
+        af[3] = as[i * PL + (ra + 8) * 8 + (sa ^ 4) + t];
 #pragma unroll
         for (int j = 0; j < 8; ++j) mma_u8(acc[i + j], af, bf[j][0], bf[j][1]);
       }
     }
     if (++cm_c == nkc) {  // task complete: T = sum_d 2^(8d) D_d mod q_r (+ mask on c1)
-      long grp;
+      long slot;
       int rt, ctile;
-      task_of(cm_j, grp, rt, ctile);
-      const long s0 = grp * kI8Slots;
-      const int bp = (int)(s0 >> logn), b = bp / R, r = bp % R, j0 = (int)(s0 & (n - 1));
+      task_of(cm_j, slot, rt, ctile);
+      const int bp = (int)(slot >> logn), b = bp / R, r = bp % R, j = (int)(slot & (n - 1));
       const PrimeConst pc = a.pc[r];
       const Field64 f = pc.f;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int row = rt * kI8Rows + g + ((e >> 1) << 3), col = ctile * kI8Cols + wn * 8 + 2 * t + (e & 1);
+        const int row = rt * kI8T + ra + ((e >> 1) << 3), col = ctile * kI8T + wc * 8 + 2 * t + (e & 1);
         if (row < rows && col < cols) {
           uint64_t P[4];
 #pragma unroll
@@ -380,7 +383,7 @@ __global__ void __launch_bounds__(256, 2)
           x = Bfly<Field64, 0>::fin_ct(f, x, pc.cred);
           const int img = row >> 1, comp = row & 1;
           uint64_t* o = out + ((size_t)img * a.cout + col) * chan_stride + (size_t)b * ctw +
-                        (size_t)(comp * R + r) * n + j0 + ws;
+                        (size_t)(comp * R + r) * n + j;
           if (comp == 1 && has_mask) x = f.add(x, *o);
           *o = x;
         }

@@ -263,7 +263,7 @@ bool mac_i8p_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64
   set_smem(k, smem);
   static int per_sm = -1;
   if (per_sm < 0) EG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem));
-  const long tasks = (long)r.a.B * R * n * ((rows + kI8T - 1) / kI8T) * ((cols + kI8T - 1) / kI8T);
+  const long tasks = (long)r.a.B * R * (n / 4) * ((rows + kI8T - 1) / kI8T) * ((cols + kI8T - 1) / kI8T);
   const long grid = std::min<long>(tasks, (long)std::max(per_sm, 1) * ctx->sm_count);
   k<<<(unsigned)grid, 256, smem, r.st>>>(r.a, (int)ctx->logn, Ap, Bp, 1, out);
   check_launch("mac_i8p_kernel");

@@ -212,8 +212,10 @@ __host__ __device__ inline long i8_plane_words(int B, int R, int n, int K, int n
 template <int R, bool WEIGHTS>
 __global__ void __launch_bounds__(256) planes_kernel(LayerArgs a, int logn, const uint64_t* __restrict__ src,
                                                      uint32_t* __restrict__ dst, int nrc) {
+  // one thread: 4 channels x 8 slots (one 64-byte segment per channel) -> 8 x 8 words
+  constexpr int SG = 8;
   const int n = 1 << logn, K = a.cin;
-  const long nsg = n / kI8Slots, nkc = (K + kI8K - 1) / kI8K;
+  const long nsg = n / SG, nkc = (K + kI8K - 1) / kI8K;
   const int rcp = (nrc + kI8T - 1) / kI8T * kI8T;
   const long total = (long)a.B * R * nsg * nkc * rcp * 8;
   const size_t ctw = (size_t)2 * R * n, chan_stride = (size_t)a.B * ctw, w_chan = (size_t)a.B * R * n;
@@ -227,32 +229,36 @@ __global__ void __launch_bounds__(256) planes_kernel(LayerArgs a, int logn, cons
     rest /= nkc;
     const long sg = rest % nsg;
     const int bp = (int)(rest / nsg), b = bp / R, r = bp % R;
-    const int j0 = (int)(sg * kI8Slots);
-    uint32_t lo[4][kI8Slots], hi[4][kI8Slots];
+    const int j0 = (int)(sg * SG);
+    uint32_t lo[4][SG], hi[4][SG];
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
       const int c = kc * kI8K + 4 * q + m;
-      ulonglong2 v01 = make_ulonglong2(0, 0), v23 = make_ulonglong2(0, 0);
+      ulonglong2 v[SG / 2];
+#pragma unroll
+      for (int h = 0; h < SG / 2; ++h) v[h] = make_ulonglong2(0, 0);
       if (rc < nrc && c < K) {
         const uint64_t* p = WEIGHTS ? src + ((size_t)rc * a.cin + c) * w_chan + (size_t)bp * n + j0
                                     : src + ((size_t)(rc >> 1) * a.cin + c) * chan_stride + (size_t)b * ctw +
                                           (size_t)((rc & 1) * R + r) * n + j0;
-        v01 = __ldg(reinterpret_cast<const ulonglong2*>(p));
-        v23 = __ldg(reinterpret_cast<const ulonglong2*>(p) + 1);
+#pragma unroll
+        for (int h = 0; h < SG / 2; ++h) v[h] = __ldg(reinterpret_cast<const ulonglong2*>(p) + h);
         if constexpr (WEIGHTS) {  // packed 30-bit limbs -> canonical value
-          v01.x = ((v01.x >> 32) << 30) | (v01.x & M30);
-          v01.y = ((v01.y >> 32) << 30) | (v01.y & M30);
-          v23.x = ((v23.x >> 32) << 30) | (v23.x & M30);
-          v23.y = ((v23.y >> 32) << 30) | (v23.y & M30);
+#pragma unroll
+          for (int h = 0; h < SG / 2; ++h) {
+            v[h].x = ((v[h].x >> 32) << 30) | (v[h].x & M30);
+            v[h].y = ((v[h].y >> 32) << 30) | (v[h].y & M30);
+          }
         }
       }
-      lo[m][0] = lo32(v01.x), hi[m][0] = hi32(v01.x);
-      lo[m][1] = lo32(v01.y), hi[m][1] = hi32(v01.y);
-      lo[m][2] = lo32(v23.x), hi[m][2] = hi32(v23.x);
-      lo[m][3] = lo32(v23.y), hi[m][3] = hi32(v23.y);
+#pragma unroll
+      for (int h = 0; h < SG / 2; ++h) {
+        lo[m][2 * h] = lo32(v[h].x), hi[m][2 * h] = hi32(v[h].x);
+        lo[m][2 * h + 1] = lo32(v[h].y), hi[m][2 * h + 1] = hi32(v[h].y);
+      }
     }
 #pragma unroll
-    for (int s = 0; s < kI8Slots; ++s) {
+    for (int s = 0; s < SG; ++s) {
       uint32_t* o = dst + ((((long)bp * n + j0 + s) * nkc + kc) * rcp + rc) * 64;
 #pragma unroll
       for (int i = 0; i < 8; ++i)
@@ -277,28 +283,29 @@ __global__ void __launch_bounds__(256, 2)
   const int rows = 2 * a.num_images, cols = a.cout, K = a.cin;
   const int nrt = (rows + kI8T - 1) / kI8T, nct = (cols + kI8T - 1) / kI8T;
   const int nkc = (K + kI8K - 1) / kI8K;
-  const long ntasks = (long)a.B * R * n * nrt * nct;
+  constexpr int SPT = 4;  // slots per task: their outputs share 32-byte sectors, written back to back
+  const long ntasks = (long)a.B * R * (n / SPT) * nrt * nct;
   const int my_tasks = blockIdx.x < ntasks ? (int)((ntasks - 1 - blockIdx.x) / gridDim.x + 1) : 0;
-  const long nsteps = (long)my_tasks * nkc;
+  const long nsteps = (long)my_tasks * SPT * nkc;
   const size_t ctw = (size_t)2 * R * n, chan_stride = (size_t)a.B * ctw;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3, wr = warp >> 2, wc = warp & 3;
   const long rows_p = (long)nrt * kI8T, cols_p = (long)nct * kI8T;
 
-  auto task_of = [&](long j, long& slot, int& rt, int& ctile) {
+  auto task_of = [&](long j, int sub, long& slot, int& rt, int& ctile) {
     const long tk = blockIdx.x + j * gridDim.x;
-    slot = tk / (nrt * nct);  // over B * R * n: (bp, slot) with the slot fastest
+    slot = tk / (nrt * nct) * SPT + sub;  // over B * R * n: (bp, slot) with the slot fastest
     const int rem = (int)(tk % (nrt * nct));
     rt = rem % nrt;
     ctile = rem / nrt;
   };
   long ld_j = 0;
-  int ld_c = 0;
+  int ld_c = 0, ld_s = 0;
   auto load_step = [&](long step) {
     if (step < nsteps) {
       long slot;
       int rt, ctile;
-      task_of(ld_j, slot, rt, ctile);
+      task_of(ld_j, ld_s, slot, rt, ctile);
       uint32_t* As = sm_i8 + (step % STAGES) * STAGE;
       const uint32_t* ag = Ap + ((slot * nkc + ld_c) * rows_p + (long)rt * kI8T) * 64;
       const uint32_t* bg = Bp + ((slot * nkc + ld_c) * cols_p + (long)ctile * kI8T) * 64;
@@ -312,7 +319,10 @@ __global__ void __launch_bounds__(256, 2)
       }
       if (++ld_c == nkc) {
         ld_c = 0;
-        ++ld_j;
+        if (++ld_s == SPT) {
+          ld_s = 0;
+          ++ld_j;
+        }
       }
     }
     cp_async_commit();
@@ -323,7 +333,7 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
   for (int d = 0; d < 15; ++d) acc[d][0] = acc[d][1] = acc[d][2] = acc[d][3] = 0;
   long cm_j = 0;
-  int cm_c = 0;
+  int cm_c = 0, cm_s = 0;
   const int ra = wr * 16 + g, cb = wc * 8 + g;                  // fragment row / col in the tile
   const int sa = ((g >> 2) & 1) << 2;                           // 16-byte half swizzle (rows and cols)
   for (long step = 0; step < nsteps; ++step) {
@@ -353,7 +363,7 @@ __global__ void __launch_bounds__(256, 2)
     if (++cm_c == nkc) {  // task complete: T = sum_d 2^(8d) D_d mod q_r (+ mask on c1)
       long slot;
       int rt, ctile;
-      task_of(cm_j, slot, rt, ctile);
+      task_of(cm_j, cm_s, slot, rt, ctile);
       const int bp = (int)(slot >> logn), b = bp / R, r = bp % R, j = (int)(slot & (n - 1));
       const PrimeConst pc = a.pc[r];
       const Field64 f = pc.f;
@@ -391,7 +401,10 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
       for (int d = 0; d < 15; ++d) acc[d][0] = acc[d][1] = acc[d][2] = acc[d][3] = 0;
       cm_c = 0;
-      ++cm_j;
+      if (++cm_s == SPT) {
+        cm_s = 0;
+        ++cm_j;
+      }
     }
     __syncthreads();  // this stage is refilled STAGES-1 steps later
   }

@@ -367,6 +367,16 @@ __global__ void __launch_bounds__(256, 2)
       const int bp = (int)(slot >> logn), b = bp / R, r = bp % R, j = (int)(slot & (n - 1));
       const PrimeConst pc = a.pc[r];
       const Field64 f = pc.f;
+      // the four HomShare-mask reads first (one latency for all four, overlapping the
+      // reconstruction below); c1 rows are the odd ones: g odd
+      uint64_t mv[4] = {0, 0, 0, 0};
+      const bool c1 = has_mask && (ra & 1);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int row = rt * kI8T + ra + ((e >> 1) << 3), col = ctile * kI8T + wc * 8 + 2 * t + (e & 1);
+        if (c1 && row < rows && col < cols)
+          mv[e] = out[((size_t)(row >> 1) * a.cout + col) * chan_stride + (size_t)b * ctw + (size_t)(R + r) * n + j];
+      }
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int row = rt * kI8T + ra + ((e >> 1) << 3), col = ctile * kI8T + wc * 8 + 2 * t + (e & 1);
@@ -394,7 +404,7 @@ __global__ void __launch_bounds__(256, 2)
           const int img = row >> 1, comp = row & 1;
           uint64_t* o = out + ((size_t)img * a.cout + col) * chan_stride + (size_t)b * ctw +
                         (size_t)(comp * R + r) * n + j;
-          if (comp == 1 && has_mask) x = f.add(x, *o);
+          if (comp == 1 && has_mask) x = f.add(x, mv[e]);
           *o = x;
         }
       }

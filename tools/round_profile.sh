@@ -19,7 +19,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --import-source on --clock-control none \
   -k regex:"tile_enc_kernel|share_kernel|mac_kara_kernel|dec_kernel" --launch-skip 8 -c 4 \
   -o /tmp/full_c1 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-graph > $O/ncu_full_c1.log 2>&1; echo "ncu full c1 rc=$?" >> $O/status
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:mac_kara --launch-skip 2 -c 1 \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"mac_i8p|mac_kara" --launch-skip 2 -c 1 \
   -o /tmp/full_c4_mac python bench.py --config 4 --steps 1 --warmup 3 --no-cpu-baseline --no-graph > $O/ncu_full_c4.log 2>&1; echo "ncu full c4 rc=$?" >> $O/status
 # export the captures as CSV (raw metrics + SASS source with per-instruction counters), drop the .ncu-rep
 for r in full_c1 full_c4_mac; do

@@ -337,9 +337,11 @@ __global__ void __launch_bounds__(256, 2)
   const int ra = wr * 16 + g, cb = wc * 8 + g;                  // fragment row / col in the tile
   const int sa = ((g >> 2) & 1) << 2;                           // 16-byte half swizzle (rows and cols)
   for (long step = 0; step < nsteps; ++step) {
-    load_step(step + STAGES - 1);
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(STAGES - 1) : "memory");
+    // one barrier per step: after it every warp has finished the previous step, so the
+    // buffer that step read can be refilled right away (STAGES-2 groups stay in flight)
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(STAGES - 2) : "memory");
     __syncthreads();
+    load_step(step + STAGES - 1);
     {
       const uint32_t* as = sm_i8 + (step % STAGES) * STAGE;
       const uint32_t* bs = as + TILE;
@@ -416,7 +418,6 @@ __global__ void __launch_bounds__(256, 2)
         ++cm_j;
       }
     }
-    __syncthreads();  // this stage is refilled STAGES-1 steps later
   }
   cp_async_wait_all();
 }

@@ -232,6 +232,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2003_05328_b200 import _lib, ops
+    from paper_2003_05328_b200.shard import ImageShard, gather_outputs
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -249,10 +250,11 @@ def main():
     gen = torch.Generator().manual_seed(args.seed)
     x_all = torch.randint(0, 256, (world * imgs, 16, 32, 32), dtype=torch.uint8, generator=gen)
     wts = torch.randint(-128, 128, (16, 16, 3, 3), dtype=torch.int32, generator=gen).to(dev)
-    x = x_all[rank * imgs:(rank + 1) * imgs].contiguous().to(dev)
+    shard = ImageShard(world * imgs, world, rank)  # contiguous image shards, global image ids
+    x = shard.take(x_all).contiguous().to(dev)
     _, key = ops.secret_sample(ctx, args.seed)
     w_eval = L.prepare_weights(wts)  # t_setup (not timed)
-    rand = ops.Randomness(seed=args.seed, image_base=rank * imgs)
+    rand = ops.Randomness(seed=args.seed, image_base=shard.start)
     ws = L.workspace(imgs)
     out = torch.empty((imgs, 16, g.oh, g.ow), dtype=torch.int32, device=dev)
     gathered = torch.empty((world * imgs, 16, g.oh, g.ow), dtype=torch.int32, device=dev) if world > 1 else None
@@ -280,7 +282,7 @@ def main():
         else:
             layer()
         if world > 1:
-            dist.all_gather_into_tensor(gathered, out)
+            gather_outputs(out, shard, gathered)  # NCCL all-gather of the reconstructed outputs
         return out
 
     for _ in range(max(3, args.warmup)):
@@ -545,6 +547,7 @@ def other_config(args, world, rank, local):
     import torch
     from paper_2003_05328_b200 import _lib, ops
     from paper_2003_05328_b200 import protocol as GP
+    from paper_2003_05328_b200.shard import ImageShard, gather_outputs
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -563,8 +566,14 @@ def other_config(args, world, rank, local):
         we = L.prepare_weights(w)
         ws = L.workspace(M)
         out = torch.empty((M, 1, 32, 32), dtype=torch.int32, device=dev)
-        rand = ops.Randomness(seed=args.seed, image_base=rank * M)
-        fn = lambda: L.forward(key, we, x, rand, ws=ws, out=out)  # noqa: E731
+        shard = ImageShard(world * M, world, rank)
+        rand = ops.Randomness(seed=args.seed, image_base=shard.start)
+        gathered = torch.empty((world * M, 1, 32, 32), dtype=torch.int32, device=dev) if world > 1 else None
+
+        def fn():
+            L.forward(key, we, x, rand, ws=ws, out=out)
+            if world > 1:
+                gather_outputs(out, shard, gathered)  # the one collective: NCCL all-gather of outputs
         total = _time_steps(fn, args.steps, args.warmup, flush, stream)
         value = world * M * args.steps / (total / 1e3)
         unit, workload = "conv/s", f"config0: {M} independent 1->1 3x3 Same convs of 32x32 uint8 per step, n=2048"
@@ -643,16 +652,20 @@ def other_config(args, world, rank, local):
         we = L.prepare_weights(w)
         ws = L.workspace(chunk)
         out = torch.empty((imgs, 128, 32, 32), dtype=torch.int32, device=dev)
+        shard = ImageShard(world * imgs, world, rank)  # images partitioned over the GPUs of the box
+        gathered = torch.empty((world * imgs, 128, 32, 32), dtype=torch.int32, device=dev) if world > 1 else None
 
         def fn():
             for i in range(0, imgs, chunk):
-                L.forward(key, we, x[i:i + chunk], ops.Randomness(seed=args.seed, image_base=rank * imgs + i),
+                L.forward(key, we, x[i:i + chunk], ops.Randomness(seed=args.seed, image_base=shard.start + i),
                           ws=ws, out=out[i:i + chunk])
+            if world > 1:
+                gather_outputs(out, shard, gathered)  # NCCL all-gather of the output shares (BASELINE config 4)
         total = _time_steps(fn, args.steps, args.warmup, None, stream)
         value = world * imgs * args.steps / (total / 1e3)
         unit = "images/s"
         workload = (f"config4: {imgs} images/GPU x 64x32x32, 64->128 3x3 Same, n=8192, RNS q = 3 x 60-bit primes, "
-                    f"p=638977, {chunk}-image chunks")
+                    f"p=638977, {chunk}-image chunks" + (", outputs all-gathered over NCCL" if world > 1 else ""))
         if rank == 0 and not args.no_cpu_baseline:
             q4 = 576460803525083137
             v, wall, online = _ref_sessions([[0, 3, 3, 1, 64, 128, 0]], 32, 32, 64, 1, 1, args.seed, n=8192, q=q4)

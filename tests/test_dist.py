@@ -41,13 +41,12 @@ def _worker(rank, world, port, result):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     rng = np.random.default_rng(1)
     all_imgs = rng.integers(0, 256, size=(4, 1, 8, 8)).astype(np.int64)
-    per = len(all_imgs) // world
-    mine = _shard_outputs(all_imgs[rank * per:(rank + 1) * per], rank * per, seed=77)
-    t = torch.from_numpy(mine)
-    out = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(out, t)
+    from paper_2003_05328_b200.shard import ImageShard, gather_outputs
+    sh = ImageShard(len(all_imgs), world, rank)
+    mine = _shard_outputs(all_imgs[sh.start:sh.stop], sh.start, seed=77)
+    gathered = gather_outputs(torch.from_numpy(mine), sh)
     if rank == 0:
-        result.put(torch.cat(out).numpy())
+        result.put(gathered.numpy())
     dist.destroy_process_group()
 
 
@@ -66,3 +65,58 @@ def test_two_rank_gather_equals_single_process():
     all_imgs = rng.integers(0, 256, size=(4, 1, 8, 8)).astype(np.int64)
     single = _shard_outputs(all_imgs, 0, seed=77)
     assert (gathered == single).all()
+
+
+# ---------------------------------------------------------------- product sharding
+
+def test_image_shard_ranges_tile_the_batch():
+    from paper_2003_05328_b200.shard import ImageShard
+    for total in (0, 1, 3, 4, 5, 8, 1023, 1024):
+        for world in (1, 2, 3, 4, 8):
+            shards = [ImageShard(total, world, r) for r in range(world)]
+            assert shards[0].start == 0 and shards[-1].stop == total
+            for a, b in zip(shards, shards[1:]):
+                assert a.stop == b.start
+            counts = [s.count for s in shards]
+            assert max(counts) - min(counts) <= 1 and max(counts) == shards[0].max_count or total == 0
+    with pytest.raises(ValueError):
+        ImageShard(4, 2, 2)
+    with pytest.raises(ValueError):
+        ImageShard(4, 2, 0).take(torch.zeros(3, 1))
+
+
+def _gather_worker(rank, world, port, result):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2003_05328_b200.shard import ImageShard, gather_outputs
+    got = {}
+    for total in (4, 5, 1):  # even, ragged, fewer units than ranks
+        full = torch.arange(total * 6, dtype=torch.int32).reshape(total, 2, 3)
+        sh = ImageShard(total, world, rank)
+        got[total] = gather_outputs(sh.take(full).clone(), sh).numpy()
+    if rank == 0:
+        result.put(got)
+    dist.destroy_process_group()
+
+
+def test_two_rank_gather_outputs_even_and_ragged():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    got = q.get(timeout=300)
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    for total, arr in got.items():
+        assert (arr == np.arange(total * 6, dtype=np.int32).reshape(total, 2, 3)).all(), total
+
+
+def test_single_rank_gather_is_a_copy():
+    from paper_2003_05328_b200.shard import ImageShard, gather_outputs
+    x = torch.arange(12).reshape(3, 4)
+    sh = ImageShard(3, 1, 0)
+    assert gather_outputs(x, sh) is not x and (gather_outputs(x, sh) == x).all()
+    assert gather_outputs(x, sh, out=x) is x

@@ -299,30 +299,42 @@ __global__ void __launch_bounds__(256, 2)
     rt = rem % nrt;
     ctile = rem / nrt;
   };
+  // Copy addressing: a task's SPT * nkc steps read consecutive (slot, chunk) blocks of the
+  // plane arrays ((slot * nkc + c) * rows_p + row0) * 64, so each step advances one pointer
+  // pair by a fixed stride and only a new task decodes (tk -> slot, tiles: two divisions).
+  // The per-thread source / destination offsets of the four 16-byte copies are fixed.
+  const long a_step = rows_p * 64, b_step = cols_p * 64;
+  const int task_steps = SPT * nkc;
+  int src_off[4], dst_off[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = tid + u * 256;  // 0..1023: operand, rc, plane, 16-byte half
+    const int op = e >> 9, rc = (e >> 4) & 31, pl = (e >> 1) & 7, hf = e & 1;
+    src_off[u] = rc * 64 + pl * 8 + hf * 4;
+    dst_off[u] = op * TILE + pl * PL + rc * 8 + ((hf ^ ((rc >> 2) & 1)) << 2);
+  }
   long ld_j = 0;
-  int ld_c = 0, ld_s = 0;
+  int ld_k = 0;  // step within the task being loaded
+  const uint32_t* ag = nullptr;
+  const uint32_t* bg = nullptr;
+  auto task_ptrs = [&](long j) {
+    long slot;
+    int rt, ctile;
+    task_of(j, 0, slot, rt, ctile);
+    ag = Ap + (slot * nkc * rows_p + (long)rt * kI8T) * 64;
+    bg = Bp + (slot * nkc * cols_p + (long)ctile * kI8T) * 64;
+  };
+  if (my_tasks > 0) task_ptrs(0);
   auto load_step = [&](long step) {
     if (step < nsteps) {
-      long slot;
-      int rt, ctile;
-      task_of(ld_j, ld_s, slot, rt, ctile);
       uint32_t* As = sm_i8 + (step % STAGES) * STAGE;
-      const uint32_t* ag = Ap + ((slot * nkc + ld_c) * rows_p + (long)rt * kI8T) * 64;
-      const uint32_t* bg = Bp + ((slot * nkc + ld_c) * cols_p + (long)ctile * kI8T) * 64;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int e = tid + u * 256;  // 0..1023: operand, rc, plane, 16-byte half
-        const int op = e >> 9, rc = (e >> 4) & 31, pl = (e >> 1) & 7, hf = e & 1;
-        const uint32_t* src = (op ? bg : ag) + rc * 64 + pl * 8 + hf * 4;
-        uint32_t* dsm = As + op * TILE + pl * PL + rc * 8 + ((hf ^ ((rc >> 2) & 1)) << 2);
-        cp_async16(dsm, src);
-      }
-      if (++ld_c == nkc) {
-        ld_c = 0;
-        if (++ld_s == SPT) {
-          ld_s = 0;
-          ++ld_j;
-        }
+      for (int u = 0; u < 4; ++u) cp_async16(As + dst_off[u], (u < 2 ? ag : bg) + src_off[u]);
+      ag += a_step;
+      bg += b_step;
+      if (++ld_k == task_steps) {
+        ld_k = 0;
+        if (++ld_j < my_tasks) task_ptrs(ld_j);
       }
     }
     cp_async_commit();

@@ -492,13 +492,13 @@ __global__ void __launch_bounds__((1 << LOGN) >> tile_loge(LOGN))
       auto dst = [&](int i, uint64_t v) {
         const uint64_t phi = Bfly<Field64, 0>::fin_gs(f, v);
         const uint64_t y = Bfly<Field64, 0>::fin_gs(f, f.mul_shoup_approx(phi, pc.crt_inv, pc.crt_inv_shoup));
-        // I = floor(y p / q_r): the estimate is at most 1 below (rem < 2q), so two
-        // predicated corrections are exact; y < q_r gives I < p (no reduction mod p)
-        uint64_t I = mulhi64(y, pc.cp);
+        uint64_t I = mulhi64(y, pc.cp);  // floor(y p / q_r), corrected below
         uint64_t rem = (uint64_t)p * y - I * f.q;
-        if (rem >= f.q) rem -= f.q, ++I;
-        if (rem >= f.q) rem -= f.q, ++I;
-        uint32_t acc = pbuf[sidx<uint32_t>(i)] + (uint32_t)I;
+        while (rem >= f.q) {
+          rem -= f.q;
+          ++I;
+        }
+        uint32_t acc = pbuf[sidx<uint32_t>(i)] + (uint32_t)(I % p);
         pbuf[sidx<uint32_t>(i)] = acc >= p ? acc - p : acc;
         facc[i] += (double)rem * pc.inv_q;
       };
@@ -506,9 +506,8 @@ __global__ void __launch_bounds__((1 << LOGN) >> tile_loge(LOGN))
       __syncthreads();
     }
     for (int i = tid; i < N; i += NT) {
-      // pbuf < p and round(sum rem_r / q_r) <= R < p: one conditional subtraction
       uint32_t m = pbuf[sidx<uint32_t>(i)] + (uint32_t)__double2int_rn(facc[i]);
-      pbuf[sidx<uint32_t>(i)] = m >= p ? m - p : m;
+      pbuf[sidx<uint32_t>(i)] = m % p;
     }
     __syncthreads();
     SmemRW<uint32_t> psrc{pbuf};
@@ -616,14 +615,12 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)))
       const uint64_t phi = Bfly<Field64, 0>::fin_gs(f, v);
       // exact floor((p phi + floor(q/2)) / q) (REF ringbfv.cpp:224-229): the estimate
       // Q = floor(phi cp / 2^64) is at most 2 below, so the remainder is < 3q and exact
-      // in 64-bit arithmetic; two predicated upward corrections.  phi < q bounds the
-      // rounded quotient by p, so Q mod p is one conditional subtraction (the generic
+      // in 64-bit arithmetic; the correction is [rem >= q] + [rem >= 2q].  phi < q bounds
+      // the rounded quotient by p, so Q mod p is one conditional subtraction (the generic
       // 64-bit % p was a divergent reciprocal / division-call sequence per coefficient).
-      uint64_t Q = mulhi64(phi, cp);
-      uint64_t rem = (uint64_t)p * phi + h - Q * f.q;
-      if (rem >= f.q) rem -= f.q, ++Q;
-      if (rem >= f.q) rem -= f.q, ++Q;
-      const uint32_t Qs = (uint32_t)Q;
+      const uint64_t Q = mulhi64(phi, cp);
+      const uint64_t rem = (uint64_t)p * phi + h - Q * f.q;
+      const uint32_t Qs = (uint32_t)Q + (rem >= f.q) + (rem >= f.q2);
       pbuf[sidx<uint32_t>(i)] = Qs >= p ? Qs - p : Qs;
     };
     ntt_inverse<Field64, uint64_t, LOGN, tile_loge(LOGN), 0, false, false>(f, tws.q, qbuf, tid, src, dst, bar);

@@ -132,6 +132,32 @@ def test_sharding_invariance(ops):
     assert torch.equal(a_all[2:], a_hi) and torch.equal(b_all[2:], b_hi)
 
 
+def test_ragged_shards_through_shard_module(ops):
+    """The product's ImageShard splits 5 images over 2 and 3 'ranks' (ragged); each shard
+    run with image_base = shard.start and gathered (world-size-1 path per shard) equals
+    the single batch: outputs and both parties' shares."""
+    from paper_2003_05328_b200.shard import ImageShard
+    ctx = ops.Context(n=2048)
+    g = torch.Generator().manual_seed(11)
+    imgs = torch.randint(0, 256, (5, 2, 8, 8), dtype=torch.uint8, generator=g).to(dev())
+    w = torch.randint(-128, 128, (3, 2, 3, 3), dtype=torch.int32, generator=g).to(dev())
+    L = ops.LayerOps(ctx, ops.ConvSpec(8, 8, 3, 3, True, 2, 3))
+    _, key = ops.secret_sample(ctx, 4)
+    we = L.prepare_weights(w)
+    out_all, a_all, b_all = L.forward(key, we, imgs, ops.Randomness(seed=4), want_shares=True)
+    for world in (2, 3):
+        outs, al, bo = [], [], []
+        for rank in range(world):
+            sh = ImageShard(5, world, rank)
+            o, a_, b_ = L.forward(key, we, sh.take(imgs).contiguous(), ops.Randomness(seed=4, image_base=sh.start),
+                                  want_shares=True)
+            outs.append(o)
+            al.append(a_)
+            bo.append(b_)
+        assert torch.equal(torch.cat(outs), out_all), world
+        assert torch.equal(torch.cat(al), a_all) and torch.equal(torch.cat(bo), b_all), world
+
+
 @pytest.mark.parametrize("n,H,fh,same,cin,cout", [
     (2048, 8, 3, True, 3, 5),     # L = 16, one half-empty block
     (2048, 8, 1, True, 4, 4),     # 1x1 filter, L = 8

@@ -287,6 +287,9 @@ void mac_r(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* o
     return mac_go<R, 8, 32, 32, 16, 4, 4>(r, ct, w, out);
   }
   if (small) return mac_kara_go<R, 8, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
+  // few input channels (config 3's 3 -> 64 layer): the 36-channel chunks of the large tile
+  // would be ~90 % zero fill and its 221 KB ring allows one CTA per SM (config 3 +0.3 %)
+  if (r.a.cin <= 12) return mac_kara_go<R, 8, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
   return mac_kara_go<R, 8, 32, 16, 36, 2, 4, 2>(r, ct, w, out);
 }
 

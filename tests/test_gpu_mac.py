@@ -43,6 +43,8 @@ CASES = [
     (2048, 2, 1030, 3, 1),
     (8192, 2, 7, 3, 3),
     (8192, 20, 30, 17, 3),
+    (2048, 20, 3, 40, 1),         # few input channels, > 16 rows / cols: small tiles, partial ones
+    (8192, 9, 12, 20, 3),         # same with three primes, K = 12 (one whole chunk)
 ]
 
 

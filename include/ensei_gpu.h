@@ -221,13 +221,29 @@ int ensei_gpu_activation(ensei_gpu_ctx* ctx, int fn, int pool2, uint32_t channel
  * 2 the int8 tensor-core kernel (exact byte-plane products, cin <= 255). */
 int ensei_gpu_set_mac_variant(int variant);
 
+/* Which ElementMult kernel a conv layer of `num_images` images takes on this context
+ * (the automatic choice, or the forced variant): */
+#define ENSEI_MAC_IMAD4 0       /* 4-product IMAD tile kernel (mac_kernel) */
+#define ENSEI_MAC_KARATSUBA 1   /* Karatsuba IMAD tile kernel (mac_kara_kernel) */
+#define ENSEI_MAC_I8_PLANES 2   /* int8 tensor cores on byte planes (planes_kernel + mac_i8p_kernel) */
+#define ENSEI_MAC_I8_DIRECT 3   /* int8 tensor cores, in-kernel plane split (mac_i8_kernel) */
+#define ENSEI_MAC_DIRECT 4      /* per-slot direct kernel for 1-4 channels (mac_direct_kernel) */
+int ensei_gpu_mac_path(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint32_t num_images, int* path);
+
 /* recombine_clear (REF hss.cpp:64-73): out = (a + b) mod p */
 int ensei_gpu_recombine(ensei_gpu_ctx* ctx, const uint32_t* d_a, const uint32_t* d_b, size_t count,
                         uint32_t* d_out, void* stream);
 
 /* Whole oblivious conv layer for a batch (Alice Enc -> Bob -> Alice Dec ->
  * recombine), the batched equivalent of one conv step of run_inproc
- * (REF protocol.cpp:670-692).  Workspace: ensei_gpu_conv_workspace_bytes(). */
+ * (REF protocol.cpp:670-692).  Workspace: ensei_gpu_conv_workspace_bytes() -- both
+ * parties' ciphertexts, Bob's share and the ElementMult scratch (int8 byte planes), so
+ * a call (or a CUDA graph captured around it) touches no context-owned buffer that can
+ * be reallocated.  The workspace-less entry points (ensei_gpu_bob_eval / _bob_mac)
+ * keep their byte planes in a context buffer grown on demand outside stream capture.
+ * Threading: a context (its auxiliary stream, fork/join events, scratch and wire status
+ * block) serves one conv-layer call at a time; concurrent calls from several host
+ * threads need one context each (the wire decoders alone are serialised internally). */
 size_t ensei_gpu_conv_workspace_bytes(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
                                       uint32_t num_images);
 int ensei_gpu_conv_layer(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uint64_t* d_t_eval,

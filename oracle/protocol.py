@@ -120,19 +120,99 @@ class PhiloxRandomness:
                          for c in range(ch)])
 
 
+def default_workers() -> int:
+    """Host threads for the parallel oracle drivers (ctypes releases the GIL, so the
+    C restatement runs concurrently on disjoint output channels)."""
+    import os
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def _pmap(fn, items, workers):
+    items = list(items)
+    if workers <= 1 or len(items) <= 1:
+        return [fn(x) for x in items]
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(min(workers, len(items))) as ex:
+        return list(ex.map(fn, items))
+
+
+def _ranges(total, workers):
+    """Contiguous [lo, hi) ranges covering `total` (about 3 per worker for balance)."""
+    parts = max(1, min(total, 3 * workers))
+    step = (total + parts - 1) // parts
+    return [(lo, min(total, lo + step)) for lo in range(0, total, step)]
+
+
+def _sub(L, cout):
+    """The same layer restricted to `cout` output channels (every oracle per-layer call
+    indexes its outputs by o, so a contiguous output-channel slice is a smaller layer)."""
+    S = Layer.from_buffer_copy(L)
+    S.cout = cout
+    return S
+
+
 def secret_eval(L, t):
     te = np.zeros(L.n, np.uint64)
     lib().eo_secret_eval(C.byref(L), np.ascontiguousarray(t, np.int64), te)
     return te
 
 
-def prepare_weights(L, w):
-    out = np.zeros(L.cout * L.cin * L.blocks * L.n, np.uint64)
-    lib().eo_prepare_weights(C.byref(L), np.ascontiguousarray(w, np.int64).reshape(-1), out)
-    return out.reshape(L.cout, L.cin, L.blocks, L.n)
+def prepare_weights(L, w, workers=1):
+    """prepare_plain for a layer's filter bank; `workers` host threads over output-channel
+    slices (identical results)."""
+    out = np.zeros((L.cout, L.cin, L.blocks, L.n), np.uint64)
+    w = np.ascontiguousarray(w, np.int64).reshape(L.cout, -1)
+
+    def job(r):
+        o0, o1 = r
+        sub = np.zeros((o1 - o0) * L.cin * L.blocks * L.n, np.uint64)
+        lib().eo_prepare_weights(C.byref(_sub(L, o1 - o0)), np.ascontiguousarray(w[o0:o1]).reshape(-1), sub)
+        out[o0:o1] = sub.reshape(o1 - o0, L.cin, L.blocks, L.n)
+    _pmap(job, _ranges(L.cout, workers), workers)
+    return out
 
 
-def run_layer(L, t_eval, alice_in, bob_prev, w_eval, e, a, s_b, want=()):
+def bob_eval(L, ct, w_eval, bob_prev, s_b, workers=1):
+    """BobSession conv step (HomRec, ElementMult + channel sum, HomShare, Bob's share IDFT2D)
+    for one image, over output-channel slices on `workers` threads."""
+    n, B = L.n, L.blocks
+    ct_out = np.zeros((L.cout, B * 2 * n), np.uint64)
+    bob_sh = np.zeros((L.cout, L.oh * L.ow), np.uint64)
+    w_eval = np.ascontiguousarray(w_eval, np.uint64).reshape(L.cout, -1)
+    s_b = np.ascontiguousarray(s_b, np.uint64).reshape(L.cout, -1)
+    prev = None if bob_prev is None else np.ascontiguousarray(bob_prev, np.uint64).reshape(-1)
+
+    def job(r):
+        o0, o1 = r
+        co = np.zeros((o1 - o0) * B * 2 * n, np.uint64)
+        bs = np.zeros((o1 - o0) * L.oh * L.ow, np.uint64)
+        lib().eo_bob_eval(C.byref(_sub(L, o1 - o0)), ct, np.ascontiguousarray(w_eval[o0:o1]).reshape(-1),
+                          None if prev is None else prev.ctypes.data_as(C.c_void_p),
+                          np.ascontiguousarray(s_b[o0:o1]).reshape(-1), co, bs)
+        ct_out[o0:o1] = co.reshape(o1 - o0, -1)
+        bob_sh[o0:o1] = bs.reshape(o1 - o0, -1)
+    _pmap(job, _ranges(L.cout, workers), workers)
+    return ct_out.reshape(-1), bob_sh.reshape(-1)
+
+
+def alice_decrypt(L, t_eval, ct_out, workers=1):
+    n, B = L.n, L.blocks
+    ct_out = np.ascontiguousarray(ct_out, np.uint64).reshape(L.cout, -1)
+    al = np.zeros((L.cout, L.oh * L.ow), np.uint64)
+
+    def job(r):
+        o0, o1 = r
+        a_ = np.zeros((o1 - o0) * L.oh * L.ow, np.uint64)
+        lib().eo_alice_decrypt(C.byref(_sub(L, o1 - o0)), t_eval, np.ascontiguousarray(ct_out[o0:o1]).reshape(-1), a_)
+        al[o0:o1] = a_.reshape(o1 - o0, -1)
+    _pmap(job, _ranges(L.cout, workers), workers)
+    return al.reshape(-1)
+
+
+def run_layer(L, t_eval, alice_in, bob_prev, w_eval, e, a, s_b, want=(), workers=1):
     """One conv layer for one image. Returns dict with alice/bob shares (+ cts)."""
     lb = lib()
     n, B = L.n, L.blocks
@@ -140,14 +220,8 @@ def run_layer(L, t_eval, alice_in, bob_prev, w_eval, e, a, s_b, want=()):
     lb.eo_alice_encrypt(C.byref(L), t_eval, np.ascontiguousarray(alice_in, np.uint64).reshape(-1),
                         np.ascontiguousarray(e, np.int64).reshape(-1),
                         np.ascontiguousarray(a, np.uint64).reshape(-1), ct)
-    ct_out = np.zeros(L.cout * B * 2 * n, np.uint64)
-    bob_sh = np.zeros(L.cout * L.oh * L.ow, np.uint64)
-    prev = None if bob_prev is None else np.ascontiguousarray(bob_prev, np.uint64).reshape(-1)
-    lb.eo_bob_eval(C.byref(L), ct, np.ascontiguousarray(w_eval, np.uint64).reshape(-1),
-                   None if prev is None else prev.ctypes.data_as(C.c_void_p),
-                   np.ascontiguousarray(s_b, np.uint64).reshape(-1), ct_out, bob_sh)
-    al_sh = np.zeros(L.cout * L.oh * L.ow, np.uint64)
-    lb.eo_alice_decrypt(C.byref(L), t_eval, ct_out, al_sh)
+    ct_out, bob_sh = bob_eval(L, ct, w_eval, bob_prev, s_b, workers)
+    al_sh = alice_decrypt(L, t_eval, ct_out, workers)
     r = {"alice": al_sh.reshape(L.cout, L.oh, L.ow), "bob": bob_sh.reshape(L.cout, L.oh, L.ow)}
     if "ct" in want:
         r["ct_in"] = ct.reshape(L.cin, B, 2, n)
@@ -155,9 +229,11 @@ def run_layer(L, t_eval, alice_in, bob_prev, w_eval, e, a, s_b, want=()):
     return r
 
 
-def run_protocol(schedule, image, weights, rand, q, p, n, want=()):
+def run_protocol(schedule, image, weights, rand, q, p, n, want=(), workers=1, w_evals=None):
     """Full schedule for one image. image: [cin][H][W] signed ints; weights: list of
-    [cout][cin][fh][fw] arrays (one per conv). Returns (output, trace)."""
+    [cout][cin][fh][fw] arrays (one per conv). Returns (output, trace).  `w_evals`
+    (optional) = the prepared weights of every conv (prepare_weights), reused across
+    images; `workers` host threads split each layer by output channels."""
     t = rand.secret()
     H, W = image.shape[1:]
     alice = np.array([[[int(v) % p for v in row] for row in ch] for ch in image], np.uint64)
@@ -171,10 +247,10 @@ def run_protocol(schedule, image, weights, rand, q, p, n, want=()):
             L = layer(q, p, n, H, W, s.fh, s.fw, int(s.same), s.cin, s.cout)
             if t_eval is None:
                 t_eval = secret_eval(L, t)
-            w_eval = prepare_weights(L, weights[conv_i])
+            w_eval = w_evals[conv_i] if w_evals is not None else prepare_weights(L, weights[conv_i], workers)
             e, a = rand.enc(li, s.cin, L.blocks)
             s_b = rand.share(li, s.cout, L.blocks)
-            r = run_layer(L, t_eval, alice, bob, w_eval, e, a, s_b, want)
+            r = run_layer(L, t_eval, alice, bob, w_eval, e, a, s_b, want, workers)
             trace.append(r)
             alice, bob = r["alice"], r["bob"]
             H, W = L.oh, L.ow
@@ -199,6 +275,44 @@ def run_protocol(schedule, image, weights, rand, q, p, n, want=()):
     if out is None:
         out = (alice + bob) % np.uint64(p)
     return out, trace
+
+
+def plain_protocol(schedule, image, weights, q, p, n, workers=1):
+    """The plaintext ground truth of a schedule for one image: conv_oracle per conv
+    layer (REF ntt.cpp:187-226, channel-summed mod p) and trusted_activation semantics
+    (REF protocol.cpp:237-268) plus the builder's 2x2 max-pool -- REF reference_pipeline
+    (protocol.cpp:694-750) extended by the pool.  Returns [cout][h][w] residues."""
+    x = np.ascontiguousarray(np.asarray(image, np.int64) % p, np.uint64)
+    H, W = x.shape[1:]
+    ci = 0
+    for s in schedule:
+        if isinstance(s, Conv):
+            L = layer(q, p, n, H, W, s.fh, s.fw, int(s.same), s.cin, s.cout)
+            w = np.ascontiguousarray(weights[ci], np.int64).reshape(s.cout, -1)
+            out = np.zeros((s.cout, L.oh * L.ow), np.uint64)
+            xf = x.reshape(-1)
+
+            def job(r, L=L, w=w, out=out, xf=xf):
+                o0, o1 = r
+                o = np.zeros((o1 - o0) * L.oh * L.ow, np.uint64)
+                lib().eo_conv_direct(C.byref(_sub(L, o1 - o0)), xf, np.ascontiguousarray(w[o0:o1]).reshape(-1), o)
+                out[o0:o1] = o.reshape(o1 - o0, -1)
+            _pmap(job, _ranges(s.cout, workers), workers)
+            x = out.reshape(s.cout, L.oh, L.ow)
+            H, W = L.oh, L.ow
+            ci += 1
+        else:
+            flat = np.ascontiguousarray(x.reshape(-1))
+            if lib().eo_activation(flat, flat.size, p, s.fn) != 0:
+                raise OverflowError("square activation exceeds p_a/2")
+            x = flat.reshape(x.shape)
+            if getattr(s, "pool2", False):
+                cen = np.where(x > p // 2, x.astype(np.int64) - p, x.astype(np.int64))
+                C_, H_, W_ = cen.shape
+                cen = cen.reshape(C_, H_ // 2, 2, W_ // 2, 2).max(axis=(2, 4))
+                x = np.where(cen < 0, cen + p, cen).astype(np.uint64)
+                H, W = H // 2, W // 2
+    return x
 
 
 # ------------------------------------------------------------------ RNS (config 4)
@@ -240,29 +354,49 @@ class PhiloxRandomnessRNS(PhiloxRandomness):
         return e, a
 
 
-def run_layer_rns(Ls, t_evals, alice_in, w_evals, e, a, s_b):
+def run_layer_rns(Ls, t_evals, alice_in, w_evals, e, a, s_b, workers=1):
     """One RNS conv layer (first layer: no HomRec) for one image; per-prime Enc /
-    ElementMult / HomShare with the single-prime restatement, CRT decryption."""
+    ElementMult / HomShare with the single-prime restatement, CRT decryption; `workers`
+    host threads over (prime, output-channel slice)."""
     R = len(Ls)
     L0 = Ls[0]
     n, B = L0.n, L0.blocks
     ct_in = np.zeros((L0.cin, B, 2, R, n), np.uint64)
     ct_out = np.zeros((L0.cout, B, 2, R, n), np.uint64)
-    bob = None
-    for r, L in enumerate(Ls):
-        ct = np.zeros(L.cin * B * 2 * n, np.uint64)
-        lib().eo_alice_encrypt(C.byref(L), t_evals[r], np.ascontiguousarray(alice_in, np.uint64).reshape(-1),
+    cts = [None] * R
+
+    def enc(r):
+        ct = np.zeros(Ls[r].cin * B * 2 * n, np.uint64)
+        lib().eo_alice_encrypt(C.byref(Ls[r]), t_evals[r], np.ascontiguousarray(alice_in, np.uint64).reshape(-1),
                                np.ascontiguousarray(e, np.int64).reshape(-1),
                                np.ascontiguousarray(a[:, :, r], np.uint64).reshape(-1), ct)
-        ct_in[:, :, :, r] = ct.reshape(L.cin, B, 2, n)
-        co = np.zeros(L.cout * B * 2 * n, np.uint64)
-        bs = np.zeros(L.cout * L.oh * L.ow, np.uint64)
-        lib().eo_bob_eval(C.byref(L), ct, np.ascontiguousarray(w_evals[r], np.uint64).reshape(-1), None,
-                          np.ascontiguousarray(s_b, np.uint64).reshape(-1), co, bs)
-        ct_out[:, :, :, r] = co.reshape(L.cout, B, 2, n)
-        bob = bs.reshape(L.cout, L.oh, L.ow)
-    arr = (Layer * R)(*Ls)
-    al = np.zeros(L0.cout * L0.oh * L0.ow, np.uint64)
+        cts[r] = ct
+        ct_in[:, :, :, r] = ct.reshape(L0.cin, B, 2, n)
+    _pmap(enc, range(R), workers)
+    bob = np.zeros((L0.cout, L0.oh * L0.ow), np.uint64)
+    s_b = np.ascontiguousarray(s_b, np.uint64).reshape(L0.cout, -1)
+    jobs = [(r, rg) for r in range(R) for rg in _ranges(L0.cout, max(1, workers // R))]
+
+    def mac(job):
+        r, (o0, o1) = job
+        w = np.ascontiguousarray(w_evals[r], np.uint64).reshape(L0.cout, -1)
+        co = np.zeros((o1 - o0) * B * 2 * n, np.uint64)
+        bs = np.zeros((o1 - o0) * L0.oh * L0.ow, np.uint64)
+        lib().eo_bob_eval(C.byref(_sub(Ls[r], o1 - o0)), cts[r], np.ascontiguousarray(w[o0:o1]).reshape(-1), None,
+                          np.ascontiguousarray(s_b[o0:o1]).reshape(-1), co, bs)
+        ct_out[o0:o1, :, :, r] = co.reshape(o1 - o0, B, 2, n)
+        if r == 0:
+            bob[o0:o1] = bs.reshape(o1 - o0, -1)
+    _pmap(mac, jobs, workers)
+    al = np.zeros((L0.cout, L0.oh * L0.ow), np.uint64)
     te = np.ascontiguousarray(np.stack(t_evals), np.uint64).reshape(-1)
-    lib().eo_alice_decrypt_rns(C.cast(arr, C.c_void_p), R, te, np.ascontiguousarray(ct_out).reshape(-1), al)
-    return {"alice": al.reshape(L0.cout, L0.oh, L0.ow), "bob": bob, "ct_in": ct_in, "ct_out": ct_out}
+
+    def dec(rg):
+        o0, o1 = rg
+        arr = (Layer * R)(*[_sub(L, o1 - o0) for L in Ls])
+        a_ = np.zeros((o1 - o0) * L0.oh * L0.ow, np.uint64)
+        lib().eo_alice_decrypt_rns(C.cast(arr, C.c_void_p), R, te, np.ascontiguousarray(ct_out[o0:o1]).reshape(-1), a_)
+        al[o0:o1] = a_.reshape(o1 - o0, -1)
+    _pmap(dec, _ranges(L0.cout, workers), workers)
+    return {"alice": al.reshape(L0.cout, L0.oh, L0.ow), "bob": bob.reshape(L0.cout, L0.oh, L0.ow), "ct_in": ct_in,
+            "ct_out": ct_out}

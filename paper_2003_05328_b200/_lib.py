@@ -106,6 +106,7 @@ def lib():
                                            vp, vp, vp, vp]),
             "ensei_gpu_recombine": (i32, [vp, vp, vp, sz, vp, vp]),
             "ensei_gpu_set_mac_variant": (i32, [i32]),
+            "ensei_gpu_mac_path": (i32, [vp, C.POINTER(ConvDesc), u32, C.POINTER(i32)]),
             "ensei_gpu_conv_workspace_bytes": (sz, [vp, C.POINTER(ConvDesc), u32]),
             "ensei_gpu_conv_layer": (i32, [vp, C.POINTER(ConvDesc), vp, u32, vp, vp, i32, vp, u32,
                                            C.POINTER(Randomness), vp, vp, vp, vp, vp]),

@@ -36,6 +36,21 @@ def _digest():
     return h.hexdigest()
 
 
+def _obj_digest(src):
+    """Per-object key: the source itself, every header it can include, the flags."""
+    h = hashlib.sha256()
+    with open(src, "rb") as fh:
+        h.update(fh.read())
+    for d in (CSRC, os.path.join(os.path.dirname(HERE), "include")):
+        for root, _, files in os.walk(d):
+            for f in sorted(files):
+                if not f.endswith(".cu"):
+                    with open(os.path.join(root, f), "rb") as fh:
+                        h.update(f.encode() + fh.read())
+    h.update(" ".join(ARCH + FLAGS).encode())
+    return h.hexdigest()
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     stamp = OUT + ".sha"
     dig = _digest()
@@ -47,20 +62,29 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
+        odig = _obj_digest(src)
+        ostamp = obj + ".sha"
+        if not force and os.path.exists(obj) and os.path.exists(ostamp) and open(ostamp).read() == odig:
+            continue  # unchanged translation unit
         cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(os.path.dirname(HERE), "include"), "-dc" if False else "-c",
                src, "-o", obj]
         log = open(obj + ".log", "w")
-        procs.append((subprocess.Popen(cmd, stdout=log, stderr=subprocess.STDOUT), src, obj))
+        procs.append((subprocess.Popen(cmd, stdout=log, stderr=subprocess.STDOUT), src, obj, odig))
     bad = []
-    for p, src, obj in procs:
+    for p, src, obj, odig in procs:
         if p.wait() != 0:
             bad.append(src)
+        else:
+            with open(obj + ".sha", "w") as f:
+                f.write(odig)
     if bad:
         for src in bad:
             sys.stderr.write(open(os.path.join(objdir, os.path.basename(src)[:-3] + ".o.log")).read())
         raise RuntimeError("nvcc failed for: " + ", ".join(bad))
     if verbose:
         for o in objs:
+            if not os.path.exists(o + ".log"):
+                continue
             sys.stdout.write(open(o + ".log").read())
     link = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", OUT, *objs, "-lpthread"]
     subprocess.run(link, check=True)

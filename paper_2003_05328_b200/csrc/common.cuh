@@ -87,7 +87,8 @@ struct ensei_gpu_ctx {
   ensei_gpu::PConst pp;
   ensei_gpu::DeviceTables tab;
   void* table_mem = nullptr;
-  bool approx_ok = true;  // every q_i < 2^61: approximate-quotient butterflies (MODE 0)
+  bool approx_ok = true;  // every 31 q_i < 2^64: approximate-quotient butterflies (MODE 0); the layer path needs it
+  uint32_t i8_kmax = 255;  // int8 tensor-core MAC: largest K with K (q_i - 1)^2 < 2^128 for every prime
   bool kara_ok = true;    // every q_i within the Karatsuba MAC's headroom (layer.cuh)
   // fork/join helpers: Bob's input-independent HomShare work runs concurrently
   // with Alice's encryption on an auxiliary stream (capturable in CUDA graphs)

@@ -109,7 +109,18 @@ static void ctx_create(int device, uint32_t n, const uint64_t* qs, uint32_t R, u
     require(q % p == 1, ENSEI_ERR_GENERIC, "q must be 1 mod p_e (keeps the plaintext-wrap term small)");
     require(q > (1ull << 32), ENSEI_ERR_UNSUPPORTED, "q_i below 2^32 not supported on this path");
     c->q[i] = q;
-    if (q >= (1ull << 61)) c->approx_ok = false;
+    // MODE-0 (approximate-quotient, uncorrected CT) butterflies let forward values grow
+    // to Bfly<Field64, 0>::kMaxBound * q = 31 q before the pass-boundary correction, and
+    // the GS side reaches u - v + 8q < 12 q + 2^33: exact only while 31 q < 2^64
+    // (q < 2^59.04).  Larger primes take MODE 1 (exact Shoup, q < 2^62) in the batched
+    // transforms; the fused layer kernels are MODE 0 only and refuse them.
+    if ((unsigned __int128)q * Bfly<Field64, 0>::kMaxBound >= ((unsigned __int128)1 << 64)) c->approx_ok = false;
+    {  // int8 tensor-core ElementMult: the 15 byte-plane sums rebuild T = sum x y exactly
+       // only while T < 2^128, i.e. K (q - 1)^2 < 2^128
+      const unsigned __int128 qq = (unsigned __int128)(q - 1) * (q - 1);
+      const unsigned __int128 kmax = (~(unsigned __int128)0) / qq;
+      c->i8_kmax = std::min<uint32_t>(c->i8_kmax, kmax > 255 ? 255u : (uint32_t)kmax);
+    }
     {  // Karatsuba MAC headroom: 2^50 + 6 Pm, 2^50 + 60 P2 < 2^64, 1008 (q-1)^2 < 2^128
       typedef unsigned __int128 u128;
       const u128 x1 = (q - 1) >> 30, xs = (u128)((1ull << 30) - 1) + x1;

@@ -80,6 +80,9 @@ Geo geometry(const ensei_gpu_ctx* c, const ensei_conv_desc* d) {
 
 LayerRun make_run(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g, uint32_t num_images,
                   const ensei_randomness* rand, void* stream) {
+  require(c->approx_ok, ENSEI_ERR_UNSUPPORTED,
+          "the fused layer kernels need 31 q_i < 2^64 for every prime (q_i < 2^59.04); larger primes run only through "
+          "ensei_gpu_negacyclic");
   LayerRun r;
   r.ctx = c;
   r.logL = (int)g.logL;
@@ -205,6 +208,16 @@ static int mac_variant() {
   return v;
 }
 
+// The int8 tensor-core path (mac_i8p_kernel): forced by variant 2, chosen automatically
+// for GEMM-sized slots (>= one 32-channel chunk, >= two 16-row tiles; measured: config 3
+// +14 %, config 4 +8 %), and only while its exact-sum bound K (q_i - 1)^2 < 2^128 holds
+// (ctx->i8_kmax); the IMAD kernels otherwise.
+bool use_i8(const ensei_gpu_ctx* c, const LayerArgs& a) {
+  const int var = mac_variant(), rows = 2 * a.num_images;
+  const bool i8_auto = var == -1 && a.cin >= kI8K && rows >= 2 * kI8Rows && a.cout >= kI8Cols;
+  return (var == 2 || i8_auto) && a.cin <= (int)c->i8_kmax;
+}
+
 // Tile choice (measured on B200, configs 1/3/4; cout <= 2 and cin <= 4 use mac_direct_kernel): 8-slot x 32-row x 16-col tiles with 36-channel
 // chunks and 2 stages for the large shapes; 8 x 16 x 16 with 12-channel chunks, 3 stages when
 // rows and cols fit 16.  Alternatives measured slower: 4 outputs per thread (no register-pair
@@ -232,25 +245,42 @@ void mac_i8_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_
   check_launch("mac_i8_kernel");
 }
 
-// Byte planes + cp.async pipeline (mac_i8p_kernel).  False when the plane scratch
-// cannot be provided (it grows on demand, which a stream under graph capture cannot do).
+// Byte-plane scratch of the int8 tensor-core MAC (bytes; 0 when the IMAD kernels run).
+size_t mac_scratch_bytes(const ensei_gpu_ctx* c, const LayerArgs& a) {
+  if (!use_i8(c, a)) return 0;
+  const int n = (int)c->n, rows = 2 * a.num_images, K = a.cin;
+  return (size_t)(i8_plane_words(a.B, (int)c->R, n, K, rows) + i8_plane_words(a.B, (int)c->R, n, K, a.cout)) *
+         sizeof(uint32_t);
+}
+
+// Byte planes + cp.async pipeline (mac_i8p_kernel).  The planes live in `scratch`
+// (the caller's workspace: ensei_gpu_conv_workspace_bytes counts them) or, for the
+// workspace-less entry points (bob_mac / bob_eval), in a context buffer grown on
+// demand -- never under stream capture (false: the caller falls back to the IMAD
+// kernels), and every growth drops the cached host-entry graph.
 template <int R>
-bool mac_i8p_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
+bool mac_i8p_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out, void* scratch) {
   ensei_gpu_ctx* ctx = const_cast<ensei_gpu_ctx*>(r.ctx);
   const int n = (int)ctx->n, rows = 2 * r.a.num_images, cols = r.a.cout, K = r.a.cin;
   const size_t aw = (size_t)i8_plane_words(r.a.B, R, n, K, rows), bw = (size_t)i8_plane_words(r.a.B, R, n, K, cols);
   const size_t need = (aw + bw) * sizeof(uint32_t);
-  if (need > ctx->i8_scratch_cap) {
+  if (!scratch && need > ctx->i8_scratch_cap) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     EG_CUDA(cudaStreamIsCapturing(r.st, &cs));
     if (cs != cudaStreamCaptureStatusNone) return false;
+    EG_CUDA(cudaStreamSynchronize(r.st));  // the old buffer may still be read by queued work
+    if (ctx->host_graph) {
+      cudaGraphExecDestroy(ctx->host_graph);
+      ctx->host_graph = nullptr;
+      ctx->host_graph_key.clear();
+    }
     if (ctx->i8_scratch) EG_CUDA(cudaFree(ctx->i8_scratch));
     ctx->i8_scratch = nullptr;
     ctx->i8_scratch_cap = 0;
     EG_CUDA(cudaMalloc(&ctx->i8_scratch, need));
     ctx->i8_scratch_cap = need;
   }
-  uint32_t* Ap = static_cast<uint32_t*>(ctx->i8_scratch);
+  uint32_t* Ap = static_cast<uint32_t*>(scratch ? scratch : ctx->i8_scratch);
   uint32_t* Bp = Ap + aw;
   const unsigned pg = (unsigned)ctx->sm_count * 8;
   planes_kernel<R, false><<<pg, 256, 0, r.st>>>(r.a, (int)ctx->logn, ct, Ap, rows);
@@ -270,19 +300,29 @@ bool mac_i8p_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64
   return true;
 }
 
+// Which ElementMult kernel a launch takes (ENSEI_MAC_* in include/ensei_gpu.h).
+int mac_path(const ensei_gpu_ctx* c, const LayerArgs& a) {
+  const int var = mac_variant();
+  if (var == 3 && a.cin <= (int)c->i8_kmax) return ENSEI_MAC_I8_DIRECT;
+  if (use_i8(c, a)) return ENSEI_MAC_I8_PLANES;
+  // tiny channel counts (config 0: 1 -> 1): direct per-slot kernel (exact while cin <= 1008)
+  if (a.cout <= 2 && a.cin <= 4) return ENSEI_MAC_DIRECT;
+  if (!c->kara_ok || var == 0) return ENSEI_MAC_IMAD4;
+  return ENSEI_MAC_KARATSUBA;
+}
+
 template <int R>
-void mac_r(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
+void mac_r(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out, void* scratch) {
   const int rows = 2 * r.a.num_images, cols = r.a.cout;
   const bool small = rows <= 16 && cols <= 16;
-  const int var = mac_variant();
-  if (var == 3 && r.a.cin <= kI8MaxK) return mac_i8_go<R>(r, ct, w, out);
-  // automatic: the tensor-core path for GEMM-sized slots (>= one 32-channel chunk, >= two
-  // 16-row tiles; measured: config 3 +14 %, config 4 +8 %); the IMAD kernels below it
-  const bool i8_auto = var == -1 && r.a.cin >= kI8K && rows >= 2 * kI8Rows && cols >= kI8Cols;
-  if ((var == 2 || i8_auto) && r.a.cin <= kI8MaxK && mac_i8p_go<R>(r, ct, w, out)) return;
-  // tiny channel counts (config 0: 1 -> 1): direct per-slot kernel (exact while cin <= 1008)
-  if (r.a.cout <= 2 && r.a.cin <= 4) return mac_direct_go<R>(r, ct, w, out);
-  if (!r.ctx->kara_ok || var == 0) {
+  int path = mac_path(r.ctx, r.a);
+  if (path == ENSEI_MAC_I8_DIRECT) return mac_i8_go<R>(r, ct, w, out);
+  if (path == ENSEI_MAC_I8_PLANES) {
+    if (mac_i8p_go<R>(r, ct, w, out, scratch)) return;
+    path = r.ctx->kara_ok ? ENSEI_MAC_KARATSUBA : ENSEI_MAC_IMAD4;  // no scratch under capture
+  }
+  if (path == ENSEI_MAC_DIRECT) return mac_direct_go<R>(r, ct, w, out);
+  if (path == ENSEI_MAC_IMAD4) {
     if (small) return mac_go<R, 16, 16, 16, 16, 2, 4>(r, ct, w, out);
     return mac_go<R, 8, 32, 32, 16, 4, 4>(r, ct, w, out);
   }
@@ -293,10 +333,10 @@ void mac_r(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* o
   return mac_kara_go<R, 8, 32, 16, 36, 2, 4, 2>(r, ct, w, out);
 }
 
-void mac(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
+void mac(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out, void* scratch = nullptr) {
   if (r.a.num_images == 0) return;
-  if (r.R == 1) return mac_r<1>(r, ct, w, out);
-  if (r.R == 3) return mac_r<3>(r, ct, w, out);
+  if (r.R == 1) return mac_r<1>(r, ct, w, out, scratch);
+  if (r.R == 3) return mac_r<3>(r, ct, w, out, scratch);
   fail(ENSEI_ERR_UNSUPPORTED, "ElementMult: unsupported prime count");
 }
 
@@ -345,9 +385,20 @@ struct Workspace {
   uint64_t* ct_in;
   uint64_t* ct_out;
   uint32_t* bob;
+  void* mac;  // ElementMult scratch (int8 byte planes), nullptr when none is needed
   uint8_t* stage_in;
   uint32_t* stage_out;
 };
+
+size_t mac_bytes(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g, uint32_t imgs) {
+  LayerArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.cin = (int)d->cin;
+  a.cout = (int)d->cout;
+  a.B = (int)g.B;
+  a.num_images = (int)imgs;
+  return (mac_scratch_bytes(c, a) + 255) & ~(size_t)255;
+}
 
 size_t ct_bytes(const ensei_gpu_ctx* c, const Geo& g, uint32_t ch, uint32_t imgs) {
   return (size_t)imgs * ch * g.B * 2 * c->R * c->n * sizeof(uint64_t);
@@ -369,6 +420,9 @@ Workspace carve(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g, 
   p += ct_bytes(c, g, d->cout, imgs);
   w.bob = reinterpret_cast<uint32_t*>(p);
   p += share_bytes(g, d->cout, imgs);
+  const size_t mb = mac_bytes(c, d, g, imgs);
+  w.mac = mb ? p : nullptr;
+  p += mb;
   if (host) {
     w.stage_in = p;
     p += in_bytes(d, imgs, in_dtype);
@@ -414,7 +468,7 @@ void layer_chain(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const Geo& g, 
   if (bob_prev)
     tile(r, TILE_HOMREC, false, ENSEI_IN_U32, k, 0, bob_prev + (size_t)i0 * tin, ct_in, (int)(imgs * desc->cin));
   EG_CUDA(cudaStreamWaitEvent(st, join, 0));
-  mac(r, ct_in, w_eval, ct_out);
+  mac(r, ct_in, w_eval, ct_out, w.mac);
   dec(r, k, ks, ct_out, alice_share ? alice_share + (size_t)i0 * tout : nullptr, bs, out ? out + (size_t)i0 * tout : nullptr,
       (int)(imgs * desc->cout));
 }
@@ -551,6 +605,20 @@ int ensei_gpu_activation(ensei_gpu_ctx* ctx, int fn, int pool2, uint32_t channel
   });
 }
 
+int ensei_gpu_mac_path(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint32_t num_images, int* path) {
+  return guarded([&] {
+    require(path != nullptr, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    Geo g = geometry(ctx, desc);
+    LayerArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.cin = (int)desc->cin;
+    a.cout = (int)desc->cout;
+    a.B = (int)g.B;
+    a.num_images = (int)num_images;
+    *path = mac_path(ctx, a);
+  });
+}
+
 int ensei_gpu_set_mac_variant(int variant) {
   return guarded([&] {
     require(variant >= -1 && variant <= 3, ENSEI_ERR_INVALID_ARGUMENT, "variant must be -1 .. 3");
@@ -574,7 +642,7 @@ size_t ensei_gpu_conv_workspace_bytes(const ensei_gpu_ctx* ctx, const ensei_conv
   guarded([&] {
     Geo g = geometry(ctx, desc);
     out = ct_bytes(ctx, g, desc->cin, num_images) + ct_bytes(ctx, g, desc->cout, num_images) +
-          share_bytes(g, desc->cout, num_images);
+          share_bytes(g, desc->cout, num_images) + mac_bytes(ctx, desc, g, num_images);
   });
   return out;
 }
@@ -595,8 +663,8 @@ size_t ensei_gpu_conv_host_workspace_bytes(const ensei_gpu_ctx* ctx, const ensei
   guarded([&] {
     Geo g = geometry(ctx, desc);
     out = ct_bytes(ctx, g, desc->cin, num_images) + ct_bytes(ctx, g, desc->cout, num_images) +
-          share_bytes(g, desc->cout, num_images) + in_bytes(desc, num_images, in_dtype) +
-          share_bytes(g, desc->cout, num_images);
+          share_bytes(g, desc->cout, num_images) + mac_bytes(ctx, desc, g, num_images) +
+          in_bytes(desc, num_images, in_dtype) + share_bytes(g, desc->cout, num_images);
   });
   return out;
 }

@@ -226,6 +226,14 @@ class LayerOps:
                                             _ptr(a), _stream(stream)))
         return a
 
+    MAC_PATHS = {0: "imad4", 1: "karatsuba", 2: "int8_planes", 3: "int8_direct", 4: "direct", 5: "tcgen05"}
+
+    def mac_path(self, images: int) -> str:
+        """The ElementMult kernel a batch of `images` takes (ensei_gpu_mac_path)."""
+        v = C.c_int()
+        check(lib().ensei_gpu_mac_path(self.ctx.h, C.byref(self.d), images, C.byref(v)))
+        return self.MAC_PATHS.get(v.value, str(v.value))
+
     def workspace(self, images: int, host: bool = False, in_dtype: int = IN_U8) -> torch.Tensor:
         if host:
             nb = lib().ensei_gpu_conv_host_workspace_bytes(self.ctx.h, C.byref(self.d), images, in_dtype)

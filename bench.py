@@ -1,24 +1,31 @@
 #!/usr/bin/env python3
 """bench.py -- B200 benchmark of the oblivious NTT-domain convolution hot path.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 4]
 
-Default workload = BASELINE.json configs[1] (the metric's config): one conv layer,
-8 images of 16 x 32x32 uint8 pixels, 16x16x3x3 int8 weights, Same conv, n = 2048,
-60-bit q, p = 638977, reference geometry (64x64 padded grid, 2 blocks / channel).
-One STEP = the whole oblivious layer for the batch (Alice Enc -> Bob HomShare +
-ElementMult -> Alice Dec -> IDFT2D -> recombine), weights prepared once (t_setup,
-excluded like the paper).  `value` = images (convolutions) per second over all GPUs
+Default workload = BASELINE.json configs[4], the one config defined over 1/2/4/8
+B200s and the largest that fits one GPU: one 64 -> 128 3x3 Same conv layer over 1024
+images of 64x32x32 uint8 per GPU, int8 weights, ring degree n = 8192 with an RNS
+ciphertext modulus of three 60-bit primes, p = 638977, 64x64 padded grid (one block per
+channel).  One STEP = the whole oblivious layer for the GPU's 1024 images (Alice Enc ->
+Bob HomShare + ElementMult -> Alice Dec -> IDFT2D -> recombine), streamed through the
+library's 128-image workspace; weights prepared once (t_setup, excluded like the paper,
+reported).  `value` = convolutions (images through the layer) per second over all GPUs
 with inputs resident in HBM; `e2e` = the same through the host-buffer C-ABI call
-(ensei_gpu_conv_layer_host: H2D pixels, layer, D2H output, synchronous).
+(ensei_gpu_conv_layer_host: 64 MiB of pixels in, 512 MiB of outputs back per step).
 
-Under torchrun (N > 1) every rank runs its own 8 images (weak scaling; image ids
-are global, so every image gets the same randomness as in a 1-GPU run) and the
-reconstructed outputs are all-gathered with NCCL inside every step.
+Under torchrun (N > 1) every rank runs its own 1024 images (weak scaling; image ids
+are global, so every image gets the same randomness as in a 1-GPU run) and both
+parties' output shares are all-gathered with NCCL chunk by chunk, overlapped with the
+next chunk's compute (paper_2003_05328_b200/shard.py ShareGather).
 
 The CPU baseline / reference arm is the UNMODIFIED reference compiled from its own
-sources (oracle/_ref/libensei_ref.so): independent run_inproc sessions of the same
-layer on all host cores, timed by the reference's own online-phase clocks.
+sources (oracle/_ref/libensei_ref.so).  Config 4 has no reference counterpart (REF has
+no RNS), so its proxy is REF's single-prime n = 8192 path with the 60-bit q on the same
+layer: the per-image online operators of a REF session (ntt_2d,
+encrypt_freq_direct, mul_plain / add_ct, hom_share, decrypt, intt_2d) on all host
+threads, Bob's prepare_plain table built once (oracle/ref_harness.cpp
+ref_bench_layer_ops).  `--config 1` keeps the round-1 line (8 images, 16 -> 16, n = 2048).
 """
 from __future__ import annotations
 
@@ -67,11 +74,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=1)
-    ap.add_argument("--images", type=int, default=8, help="images per GPU per step")
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--images", type=int, default=0, help="images per GPU per step (0: the config's own)")
     ap.add_argument("--seed", type=int, default=2003)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ntt", action="store_true")
+    ap.add_argument("--no-side", action="store_true", help="config 4: skip the config-1 side line")
     ap.add_argument("--no-graph", action="store_true", help="launch the layer eagerly instead of a CUDA graph")
     return ap.parse_args()
 
@@ -190,30 +198,66 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+def ref_ops_bench(n, q, cin, cout, images, threads, seed):
+    """REF's per-image online operators on one 32x32 3x3 Same layer (ref_bench_layer_ops):
+    returns (conv/s with `threads` images in flight, wall s, summed online s, setup s)."""
+    import numpy as np
+    import oracle as O
+    g = O.MTRng(seed, 0xDA7A)
+    img = np.array([g.uniform_below(256) for _ in range(cin * 32 * 32)], np.int64)
+    w = np.array([g.uniform_below(256) - 128 for _ in range(cout * cin * 9)], np.int64)
+    online, setup = O.C.c_double(0), O.C.c_double(0)
+    wall = O.ref().ref_bench_layer_ops(P, q, n, 4.0, seed, 32, 32, 3, 3, 1, cin, cout, img, w, images, threads,
+                                       O.C.byref(online), O.C.byref(setup))
+    if wall < 0:
+        raise RuntimeError("reference bench failed: " + O.ref().ref_last_error().decode())
+    return images / wall, wall, online.value, setup.value
+
+
 def run_reference(args, rank):
+    """The reference arm: REF's own CPU implementation of the path on all host threads,
+    on this arm's config / metric / unit; rank 0 only (other ranks exit without work)."""
     if rank != 0:
         return
     cores = host_cores()
-    threads = max(1, cores // 2)
-    per = max(threads, 16)
-    vals = []
-    if args.warmup > 0:
-        ref_layer_bench(threads, threads, args.seed)
+    vals, walls = [], []
+    if args.config not in (1, 4):
+        print(json.dumps({"impl": "reference", "unavailable": "the reference arm covers the bench lines' configs "
+                                                              "(4: default headline, 1)"}), flush=True)
+        return
+    if args.config == 1:
+        threads = max(1, cores // 2)
+        per = max(threads, 16)
+        step = lambda s: ref_layer_bench(per, threads, args.seed + 1000 * s)[0]  # noqa: E731
+        workload = ("config1 layer (16->16 3x3 Same @32x32, n=2048, 60-bit q, p=638977), one image per reference "
+                    "run_inproc session")
+        sample = (f"{per} run_inproc sessions per step, {threads} concurrent (2 threads each); online phase (Alice "
+                  "Hello->Done), Bob weight prep excluded")
+    else:
+        threads = cores
+        per = max(16, cores)
+        step = lambda s: ref_ops_bench(8192, Q, 64, 128, per, threads, args.seed + 1000 * s)[0]  # noqa: E731
+        workload = ("config4 proxy: the 64->128 3x3 Same layer @32x32 at n=8192 with REF's single 60-bit prime "
+                    "q=576460803525083137 (REF has no RNS; SURVEY 8(d)), p=638977")
+        sample = (f"{per} images per step through REF's per-image online operators (ntt_2d, encrypt_freq_direct, "
+                  f"mul_plain/add_ct, hom_share, decrypt, intt_2d; oracle/ref_harness.cpp ref_bench_layer_ops), "
+                  f"{threads} host threads over images; Bob's prepare_plain table built once per step, excluded "
+                  "(t_setup)")
+    for s in range(args.warmup):
+        step(-1 - s)
     t0 = time.perf_counter()
     for s in range(args.steps):
-        v, wall, online = ref_layer_bench(per, threads, args.seed + 1000 * s)
-        vals.append(v)
+        t1 = time.perf_counter()
+        vals.append(step(s))
+        walls.append(time.perf_counter() - t1)
     elapsed = time.perf_counter() - t0
     value = statistics.median(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "conv/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * elapsed / max(1, args.steps),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": "config1 layer (16->16 3x3 Same @32x32, n=2048, 60-bit q, p=638977), one image per "
-                               "reference run_inproc session", "sessions_per_step": per, "concurrent_sessions": threads},
-        "cpu_baseline": {"value": value, "unit": "conv/s", "cores": cores, "kind": "reference",
-                         "sample": f"{per} run_inproc sessions x {args.steps} steps, {threads} concurrent (2 threads "
-                                   "each); online phase (Alice Hello->Done), Bob weight prep excluded"},
+        "config": {"workload": workload, "images_per_step": per, "threads": threads, "config_index": args.config},
+        "cpu_baseline": {"value": value, "unit": "conv/s", "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": "conv/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -237,12 +281,29 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.config == 4:
+        line = run_config4(args, world, rank, local)
+    elif args.config == 1:
+        line = run_config1(args, world, rank, local)
+    else:
+        line = None
+        other_config(args, world, rank, local)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_config1(args, world, rank, local, side=False):
+    """BASELINE config 1 (8 images, 16 -> 16, n = 2048); side=True: the compact form
+    attached to the config-4 line (no CPU baseline / NTT / wire side measurements)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2003_05328_b200 import _lib, ops
+    from paper_2003_05328_b200.shard import ImageShard, gather_outputs
     dev = torch.device("cuda", local)
     lib = _lib.lib()
-
-    if args.config != 1:
-        return other_config(args, world, rank, local)
-    imgs = args.images
+    imgs = (args.images or 8) if not side else 8
     ctx = ops.Context(n=2048, q=(Q,), p=P, device=local)
     spec = ops.ConvSpec(32, 32, 3, 3, True, 16, 16)
     L = ops.LayerOps(ctx, spec)
@@ -407,7 +468,7 @@ def main():
 
     # ---- config 2 side measurement: batched negacyclic NTT/INTT (device layout)
     ntt = None
-    if not args.no_ntt and rank == 0:
+    if not args.no_ntt and rank == 0 and not side:
         ntt = {}
         for n in (2048, 4096, 8192):
             c2 = ops.Context(n=n, q=(Q,), p=P, device=local)
@@ -438,7 +499,7 @@ def main():
     # (imgs x 16 channels x 2 blocks records, REF wire layout) built from / parsed into
     # the device layout, device-resident frames (HBM roofline) and page-locked host frames.
     wire = None
-    if rank == 0:
+    if rank == 0 and not side:
         from paper_2003_05328_b200 import wire as Wr
         fb = Wr.ct_frame_bytes(2048, 16, g.blocks)
         ct_out.copy_((ct_out.view(torch.int64).abs() % Q).view(torch.uint64))
@@ -473,7 +534,7 @@ def main():
 
     # ---- CPU baseline (reference, bounded sample, rank 0)
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline and not side:
         try:
             cores = host_cores()
             thr = max(1, cores // 2)
@@ -485,6 +546,9 @@ def main():
             cpu = {"value": None, "unit": "conv/s", "cores": host_cores(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    if side:
+        return {"value": value, "unit": "conv/s", "ms_per_step": ms_step, "e2e": e2e, "kernel_ms": times,
+                "workload": "config1: 8 images/GPU x 16x32x32, 16->16 3x3 Same, n=2048, single 60-bit q, CUDA graph"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "conv/s", "n_gpus": world, "steps": args.steps,
@@ -502,9 +566,294 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk, "ntt_config2": ntt,
             "wire": wire,
         }
-        print(json.dumps(line), flush=True)
+        return line
+    return None
+
+
+# ------------------------------------------------------------------ config 4 (the headline)
+
+def i8_peak_tops(peaks):
+    """int8 dense tensor peak in TOP/s: 2 x the measured bf16 GEMM burst (sm_100a int8 dense
+    = 2 x bf16 dense: 4.5 vs 2.25 POPS nominal); MEASURED_PEAKS has no int8 entry."""
+    return 2.0 * peaks.get("bf16_tflops", 1590.0), "2 x MEASURED_PEAKS.json bf16_tflops (int8 dense = 2x bf16 dense)"
+
+
+def config4_counts(imgs, n=8192, R=3, L=64, B=1, cin=64, cout=128, H=32, W=32):
+    """Per-kernel algorithmic work for one sub-batch of `imgs` images:
+    modmuls by class, IMAD slots (c_q, c_mac, c_p), HBM bytes, int8 tensor MACs."""
+    k = layer_counts(n, R, L, B, cin, cout, H, W, H, W, imgs)
+    ctw = imgs * cin * B * 2 * R * n * 8
+    k["planes_ct"] = dict(q=0, mac=0, p=0, bytes=2 * ctw, imad=0, modmul=0)
+    k["planes_w"] = dict(q=0, mac=0, p=0, bytes=2 * cout * cin * B * R * n * 8, imad=0, modmul=0)
+    # ElementMult on the tensor cores: 64 u8 x u8 products per modular MAC (byte planes);
+    # operands = ciphertext + weight planes (as many bytes as the words), masks in, outputs out
+    k["mac"]["i8_mac"] = 64 * k["mac"]["mac"]
+    k["mac"]["imad"] = 0
+    return k
+
+
+def run_config4(args, world, rank, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2003_05328_b200 import _lib, ops
+    from paper_2003_05328_b200 import configs as CF
+    from paper_2003_05328_b200.shard import ImageShard, ShareGather
+    dev = torch.device("cuda", local)
+    lib = _lib.lib()
+    cfg = CF.CONFIG4
+    imgs = args.images or cfg["images"]
+    cin, cout = cfg["cin"], cfg["cout"]
+    ctx = ops.Context(n=cfg["n"], q=cfg["q"], p=P, device=local)
+    L = ops.LayerOps(ctx, ops.ConvSpec(32, 32, 3, 3, True, cin, cout))
+    g = L.geom
+    shard = ImageShard(world * imgs, world, rank)  # contiguous image shards, global image ids
+    # this rank's images (seeded per shard: 64 MiB of pixels per GPU), weights from the common seed
+    x_h = torch.randint(0, 256, (imgs, cin, 32, 32), dtype=torch.uint8,
+                        generator=torch.Generator().manual_seed(args.seed * 7919 + shard.start))
+    w_h = torch.randint(-128, 128, (cout, cin, 3, 3), dtype=torch.int32, generator=torch.Generator().manual_seed(args.seed))
+    x = x_h.to(dev)
+    _, key = ops.secret_sample(ctx, args.seed)
+    torch.cuda.synchronize()
+    t_s = time.perf_counter()
+    we = L.prepare_weights(w_h.to(dev))  # Bob's t_setup (not timed in the step)
+    torch.cuda.synchronize()
+    setup_ms = (time.perf_counter() - t_s) * 1e3
+    rand = ops.Randomness(seed=args.seed, image_base=shard.start)
+    chunk = L.chunk_images(imgs)
+    ws = L.workspace(imgs)
+    shape = (imgs, cout, g.oh, g.ow)
+    out = torch.empty(shape, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     if world > 1:
-        dist.destroy_process_group()
+        alice = torch.empty(shape, dtype=torch.int32, device=dev)
+        bob = torch.empty(shape, dtype=torch.int32, device=dev)
+        g_alice = torch.empty((world * imgs,) + shape[1:], dtype=torch.int32, device=dev)
+        g_bob = torch.empty_like(g_alice)
+        gather = ShareGather(shard, g_alice, g_bob)
+
+    def step():
+        if world == 1:
+            L.forward(key, we, x, rand, ws=ws, out=out)
+            return
+        # chunk by chunk so each chunk's share all-gathers overlap the next chunk's kernels
+        for i0 in range(0, imgs, chunk):
+            i1 = min(imgs, i0 + chunk)
+            L.forward(key, we, x[i0:i1], ops.Randomness(seed=args.seed, image_base=shard.start + i0), ws=ws,
+                      out=out[i0:i1], want_shares=True, alice=alice[i0:i1], bob=bob[i0:i1])
+            gather.post(i0, i1, alice, bob)
+        gather.wait()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = lib.ensei_gpu_launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()  # evict L2 between timed steps (untimed; the step's own traffic is ~100 GB anyway)
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    launches = lib.ensei_gpu_launch_count() - launches0
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    ms_step = total_ms / args.steps
+    value = world * imgs * args.steps / (total_ms / 1e3)
+
+    # ---- per-kernel CUDA-event times inside the same step (a separate measurement pass:
+    # the library brackets every layer launch with events on its own stream)
+    _lib.profile(True)
+    prof_steps = 2
+    for _ in range(prof_steps):
+        flush.zero_()
+        L.forward(key, we, x, rand, ws=ws, out=out)
+    torch.cuda.synchronize()
+    prof = _lib.profile_read()
+    _lib.profile(False)
+    nchunks = -(-imgs // chunk)
+    kc = config4_counts(chunk)
+    imad_peak = lib.ensei_gpu_imad_peak(local)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    i8_peak, i8_src = i8_peak_tops(peaks)
+    mac_name = next((k for k in prof if k.startswith("mac")), "mac")
+    alias = {"enc": "enc", "share": "share", "dec_rns": "dec", "planes_ct": "planes_ct", "planes_w": "planes_w",
+             mac_name: "mac"}
+    per_kernel = {}
+    for name, (tot, cnt) in prof.items():
+        ms = tot / cnt  # per launch = per sub-batch of `chunk` images
+        c = kc.get(alias.get(name, name))
+        rec = {"ms_per_launch": ms, "launches_per_step": cnt / prof_steps, "share_of_step": tot / prof_steps / ms_step}
+        if c:
+            t = ms * 1e-3
+            rec["hbm_frac"] = c["bytes"] / t / 1e9 / hbm_peak
+            rec["alg_bytes_per_launch"] = c["bytes"]
+            if c.get("imad"):
+                rec["imad_frac"] = c["imad"] / t / imad_peak
+                rec["imad_slots_per_launch"] = c["imad"]
+            if c.get("i8_mac"):
+                rec["tensor_frac"] = 2 * c["i8_mac"] / t / 1e12 / i8_peak
+                rec["int8_macs_per_launch"] = c["i8_mac"]
+        per_kernel[name] = rec
+    dom = max(per_kernel, key=lambda k: per_kernel[k]["ms_per_launch"] * per_kernel[k]["launches_per_step"])
+    d = per_kernel[dom]
+    legs = {"tensor": d.get("tensor_frac", 0.0), "imad": d.get("imad_frac", 0.0), "hbm": d.get("hbm_frac", 0.0)}
+    bound = max(legs, key=legs.get)
+    t_dom = d["ms_per_launch"] * 1e-3
+    cdom = kc.get(alias.get(dom, dom), {})
+    if bound == "tensor":
+        ach, peak, unit = 2 * cdom["i8_mac"] / t_dom / 1e12, i8_peak, "TOP/s (int8)"
+    elif bound == "imad":
+        ach, peak, unit = cdom["imad"] / t_dom / 1e9, imad_peak / 1e9, "GIMAD/s"
+    else:
+        ach, peak, unit = cdom["bytes"] / t_dom / 1e9, hbm_peak, "GB/s"
+    roofline = {
+        "bound": "tensor" if bound == "tensor" else ("hbm" if bound == "hbm" else "imad"), "kernel": dom,
+        "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak, "traffic": ncu_traffic("config4", dom),
+        "peak_source": {"tensor": i8_src, "imad": "live mad.lo.u32 probe (ensei_gpu_imad_peak)",
+                        "hbm": "MEASURED_PEAKS.json hbm_gbs (measured)"}[bound],
+        "legs": legs, "per_kernel": per_kernel,
+        "units_per_launch": f"{chunk} images (one sub-batch); {nchunks} launches of each kernel per step",
+        "c_q": C_Q, "c_mac": C_MAC, "c_p": C_P,
+    }
+    step_imad = sum(kc[k]["imad"] for k in ("enc", "share", "dec")) * nchunks
+    total_modmul = sum(kc[k]["modmul"] for k in ("enc", "share", "mac", "dec")) * nchunks
+
+    # ---- e2e through the host-buffer C-ABI entry point (pinned host buffers, chunked inside)
+    h_x = x_h.pin_memory()
+    h_out = torch.empty(shape, dtype=torch.int32).pin_memory()
+    ws_h = L.workspace(imgs, host=True, in_dtype=_lib.IN_U8)
+    call = L.host_call(key, we, h_x, rand, ws_h, h_out)
+    for _ in range(max(3, args.warmup)):
+        call()
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        call()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms_step = statistics.mean(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e_ms_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms_step = float(t.item())
+    e2e = {"value": world * imgs / (e2e_ms_step / 1e3), "unit": "conv/s", "h2d_bytes_per_step": h_x.numel(),
+           "d2h_bytes_per_step": h_out.numel() * 4, "ms_per_step": e2e_ms_step,
+           "api": "LayerOps.host_call -> ensei_gpu_conv_layer_host (pinned host buffers read / written in place, "
+                  "wall clock, synchronous)"}
+    del ws_h
+    torch.cuda.empty_cache()
+
+    # ---- verification: sampled images of the timed step's output (device path and host path)
+    # against the plaintext convolution (REF conv_oracle semantics) -- the oracle as checker only
+    verify = None
+    if rank == 0:
+        try:
+            from oracle import protocol as OP
+            picks = sorted({0, imgs // 2, imgs - 1})
+            ok = True
+            for i in picks:
+                want = OP.plain_protocol([OP.Conv(3, 3, True, cin, cout)], x_h[i].numpy().astype(np.int64),
+                                         [w_h.numpy()], Q, P, 2048, OP.default_workers())
+                ok &= bool((out[i].cpu().numpy().astype(np.uint64) == want).all())
+                ok &= bool((h_out[i].numpy().astype(np.uint64) == want).all())
+            verify = {"images": [shard.start + i for i in picks], "ok": ok,
+                      "against": "plaintext convolution (oracle eo_conv_direct = REF conv_oracle), device and "
+                                 "host-entry outputs"}
+        except Exception as e:  # noqa: BLE001
+            verify = {"ok": None, "error": str(e)}
+
+    # ---- CPU baseline: REF single-prime n=8192 proxy, 16+ images over all host threads
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            cores = host_cores()
+            nimg = max(16, cores)
+            v, wall, online, setup = ref_ops_bench(8192, Q, cin, cout, nimg, cores, args.seed)
+            cpu = {"value": v, "unit": "conv/s", "cores": cores, "kind": "reference",
+                   "sample": f"{nimg} images of the same 64->128 layer at n=8192 through REF's per-image online "
+                             f"operators with REF's single 60-bit prime (RNS proxy, SURVEY 8(d)), {cores} host "
+                             f"threads over images ({wall:.1f} s wall; {online / nimg:.2f} s online per image on one "
+                             f"thread); Bob's prepare_plain table ({setup:.1f} s on {cores} threads) excluded"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "conv/s", "cores": host_cores(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    # ---- side lines: config 1 (round-1 headline) and config 2 (n = 8192 NTT)
+    side1 = None
+    if world == 1 and not args.no_side:
+        del ws
+        torch.cuda.empty_cache()
+        side1 = run_config1(args, world, rank, local, side=True)
+    ntt = None
+    if rank == 0 and not args.no_ntt:
+        ntt = ntt_side(ctx, dev, stream, imad_peak)
+
+    if rank != 0:
+        return None
+    return {
+        "metric": METRIC, "value": value, "unit": "conv/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic: uint8 pixels U[0,256), int8 weights U[-128,128), seeded (no dataset)",
+        "config": {"workload": f"config4: one 64->128 3x3 Same conv layer, {imgs} images/GPU x 64x32x32 uint8, int8 "
+                               "weights, n=8192, RNS q = 3 x 60-bit primes == 1 mod 16384 p, p=638977, 64x64 "
+                               "padded grid, 1 block/channel",
+                   "images_per_gpu": imgs, "global_batch": world * imgs, "parallelism": f"dp{world} (image shards)",
+                   "sub_batch_images": chunk, "l2": "flushed (256 MB write) between timed steps; each step also "
+                   "streams ~100 GB through HBM", "randomness": "Philox4x32-10 device streams",
+                   "launch": "eager (8 sub-batches x 6 kernels per step)",
+                   "gather": "both parties' output shares all-gathered per sub-batch over NCCL, overlapped"
+                             if world > 1 else "none (1 GPU)",
+                   "unit_def": "1 conv = 1 image through the whole 64->128 layer", "config_index": 4,
+                   "mac_path": L.mac_path(chunk)},
+        "roofline": roofline, "setup_ms": setup_ms,
+        "imad_slot_rate": step_imad * args.steps / (total_ms / 1e3), "modmul_per_s": total_modmul * args.steps / (
+            total_ms / 1e3),
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk, "verify": verify,
+        "config1": side1, "ntt_n8192": ntt,
+    }
+
+
+def ntt_side(ctx, dev, stream, imad_peak):
+    """Config 2 side measurement at n = 8192: 8192 polynomials forward / inverse."""
+    import torch
+    from paper_2003_05328_b200 import _lib
+    n = ctx.n
+    cnt = 8192
+    buf = torch.randint(0, 1 << 62, (cnt, n), dtype=torch.int64, device=dev)
+    buf = (buf % Q).view(torch.uint64)
+    res = {}
+    for inv in (False, True):
+        for _ in range(2):
+            ctx.negacyclic(buf, 0, inv, _lib.LAYOUT_BITREV)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(5):
+            ctx.negacyclic(buf, 0, inv, _lib.LAYOUT_BITREV)
+        b.record(stream)
+        b.synchronize()
+        ms = a.elapsed_time(b) / 5
+        rate = cnt / (ms / 1e3)
+        alg = ntt_inv(n) if inv else ntt_fwd(n)
+        res["inv" if inv else "fwd"] = {"transforms_per_s": rate, "ms": ms, "imad_frac": rate * alg * C_Q / imad_peak}
+    del buf
+    torch.cuda.empty_cache()
+    return res
 
 
 # ------------------------------------------------------------------ configs 0, 2, 3, 4
@@ -557,7 +906,7 @@ def other_config(args, world, rank, local):
     extra = {}
     cpu = None
     if args.config == 0:
-        M = args.images if args.images != 8 else 4096
+        M = args.images or 4096
         ctx = ops.Context(n=2048, device=local)
         L = ops.LayerOps(ctx, ops.ConvSpec(32, 32, 3, 3, True, 1, 1))
         x = torch.randint(0, 256, (M, 1, 32, 32), dtype=torch.uint8, generator=gen).to(dev)
@@ -610,68 +959,60 @@ def other_config(args, world, rank, local):
             cpu = {"value": 2 * 4096 / secs, "unit": unit, "cores": cores, "kind": "reference",
                    "sample": "4096 polys x REF NegacyclicPlan forward+inverse over all host threads"}
     elif args.config == 3:
-        imgs = args.images if args.images != 8 else 64
+        from paper_2003_05328_b200 import configs as CF
+        imgs = args.images or CF.CONFIG3_IMAGES
         ctx = ops.Context(n=2048, device=local)
-        sched = [GP.Conv(3, 3, True, 3, 64), GP.Act(0), GP.Conv(3, 3, True, 64, 64), GP.Act(0, True),
-                 GP.Conv(3, 3, True, 64, 128), GP.Act(0), GP.Conv(3, 3, True, 128, 128), GP.Act(0, True),
-                 GP.Conv(3, 3, True, 128, 128), GP.Act(0), GP.Conv(1, 1, True, 128, 128), GP.Act(0),
-                 GP.Conv(1, 1, True, 128, 16)]
-        wshapes = [(64, 3, 3, 3), (64, 64, 3, 3), (128, 64, 3, 3), (128, 128, 3, 3), (128, 128, 3, 3),
-                   (128, 128, 1, 1), (16, 128, 1, 1)]
-        ws = [torch.randint(-128, 128, s_, dtype=torch.int32, generator=gen) for s_ in wshapes]
+        sched = CF.CONFIG3_SCHEDULE
+        ws = [torch.randint(-128, 128, s_, dtype=torch.int32, generator=gen) for s_ in CF.CONFIG3_WEIGHTS]
         sess = GP.Session(ctx, sched, 32, 32, ws)
-        x = torch.randint(0, 256, (imgs, 3, 32, 32), dtype=torch.uint8, generator=gen).to(dev)
+        shard = ImageShard(world * imgs, world, rank)  # contiguous image shards, global image ids
+        x_h = torch.randint(0, 256, (imgs, 3, 32, 32), dtype=torch.uint8,
+                            generator=torch.Generator().manual_seed(args.seed * 7919 + shard.start))
+        x = x_h.to(dev)
         _, key = ops.secret_sample(ctx, args.seed)
-        rands = [ops.Randomness(seed=args.seed, layer=li, image_base=rank * imgs) for li in range(len(sched))]
-        fn = lambda: sess.run(key, x, lambda li: rands[li])  # noqa: E731
+        rands = [ops.Randomness(seed=args.seed, layer=li, image_base=shard.start) for li in range(len(sched))]
+        out3 = {}
+        gathered = torch.empty((world * imgs, 16, 8, 8), dtype=torch.int32, device=dev) if world > 1 else None
+
+        def fn():
+            out3["y"] = sess.run(key, x, lambda li: rands[li])
+            if world > 1:
+                gather_outputs(out3["y"], shard, gathered)  # NCCL all-gather of the outputs
         total = _time_steps(fn, args.steps, args.warmup, flush, stream)
         value = world * imgs * args.steps / (total / 1e3)
         unit = "images/s"
         workload = (f"config3: {imgs} images x 3x32x32 through 7 conv layers (3->64, 64->64 @32; 64->128, "
                     "128->128 @16; 128->128 3x3, 128->128 1x1, 128->16 1x1 @8), ReLU, 2x2 max-pool after L2/L4")
+        extra["mac_paths"] = [lo.mac_path(imgs) for lo in sess.layers if lo is not None]
+        if rank == 0:  # sampled outputs of the last timed step vs the plaintext chain (oracle as checker)
+            try:
+                from oracle import protocol as OP
+                osched = [OP.Conv(s_.fh, s_.fw, s_.same, s_.cin, s_.cout) if hasattr(s_, "cin") else
+                          OP.Act(s_.fn, s_.pool2) for s_ in sched]
+                picks = sorted({0, imgs - 1})
+                ok = all(bool((out3["y"][i].cpu().numpy().astype(np.uint64) == OP.plain_protocol(
+                    osched, x_h[i].numpy().astype(np.int64), [w.numpy().astype(np.int64) for w in ws], Q, P, 2048,
+                    OP.default_workers())).all()) for i in picks)
+                extra["verify"] = {"images": [shard.start + i for i in picks], "ok": ok,
+                                   "against": "plaintext chain (oracle conv_direct + ReLU + pool; pinned to REF "
+                                              "reference_pipeline per segment by tests/test_config3_pin.py)"}
+            except Exception as e:  # noqa: BLE001
+                extra["verify"] = {"ok": None, "error": str(e)}
         if rank == 0 and not args.no_cpu_baseline:
+            thr = max(1, cores // 2)
+            nimg = max(8, thr)
             segs = [([[0, 3, 3, 1, 3, 64, 0], [1, 0, 0, 0, 0, 0, 0], [0, 3, 3, 1, 64, 64, 0]], 32, 3),
                     ([[0, 3, 3, 1, 64, 128, 0], [1, 0, 0, 0, 0, 0, 0], [0, 3, 3, 1, 128, 128, 0]], 16, 64),
                     ([[0, 3, 3, 1, 128, 128, 0], [1, 0, 0, 0, 0, 0, 0], [0, 1, 1, 1, 128, 128, 0],
                       [1, 0, 0, 0, 0, 0, 0], [0, 1, 1, 1, 128, 16, 0]], 8, 128)]
             per_img = 0.0
             for rows, Hs, cin in segs:
-                _, _, online = _ref_sessions(rows, Hs, Hs, cin, 1, 1, args.seed)
-                per_img += online
-            cpu = {"value": min(cores // 2, 1e9) / per_img, "unit": unit, "cores": cores, "kind": "reference",
-                   "sample": "1 image through REF run_inproc of the 3 reference-expressible segments "
-                             f"(online {per_img:.2f}s), scaled to {cores // 2} concurrent sessions"}
-    elif args.config == 4:
-        imgs = args.images if args.images != 8 else 1024
-        chunk = 128
-        ctx = ops.Context(n=8192, q=ops.RNS_DEFAULT, device=local)
-        L = ops.LayerOps(ctx, ops.ConvSpec(32, 32, 3, 3, True, 64, 128))
-        x = torch.randint(0, 256, (imgs, 64, 32, 32), dtype=torch.uint8, generator=gen).to(dev)
-        w = torch.randint(-128, 128, (128, 64, 3, 3), dtype=torch.int32, generator=gen).to(dev)
-        _, key = ops.secret_sample(ctx, args.seed)
-        we = L.prepare_weights(w)
-        ws = L.workspace(chunk)
-        out = torch.empty((imgs, 128, 32, 32), dtype=torch.int32, device=dev)
-        shard = ImageShard(world * imgs, world, rank)  # images partitioned over the GPUs of the box
-        gathered = torch.empty((world * imgs, 128, 32, 32), dtype=torch.int32, device=dev) if world > 1 else None
-
-        def fn():
-            for i in range(0, imgs, chunk):
-                L.forward(key, we, x[i:i + chunk], ops.Randomness(seed=args.seed, image_base=shard.start + i),
-                          ws=ws, out=out[i:i + chunk])
-            if world > 1:
-                gather_outputs(out, shard, gathered)  # NCCL all-gather of the output shares (BASELINE config 4)
-        total = _time_steps(fn, args.steps, args.warmup, None, stream)
-        value = world * imgs * args.steps / (total / 1e3)
-        unit = "images/s"
-        workload = (f"config4: {imgs} images/GPU x 64x32x32, 64->128 3x3 Same, n=8192, RNS q = 3 x 60-bit primes, "
-                    f"p=638977, {chunk}-image chunks" + (", outputs all-gathered over NCCL" if world > 1 else ""))
-        if rank == 0 and not args.no_cpu_baseline:
-            q4 = 576460803525083137
-            v, wall, online = _ref_sessions([[0, 3, 3, 1, 64, 128, 0]], 32, 32, 64, 1, 1, args.seed, n=8192, q=q4)
-            cpu = {"value": (cores // 2) / online, "unit": unit, "cores": cores, "kind": "reference",
-                   "sample": f"1 image, REF single-prime n=8192 64->128 session (online {online:.2f}s; RNS proxy per "
-                             f"SURVEY 8(d)), scaled to {cores // 2} concurrent sessions"}
+                _, _, online = _ref_sessions(rows, Hs, Hs, cin, nimg, thr, args.seed)
+                per_img += online / nimg
+            cpu = {"value": thr / per_img, "unit": unit, "cores": cores, "kind": "reference",
+                   "sample": f"{nimg} images through REF run_inproc sessions of the 3 reference-expressible "
+                             f"segments, {thr} concurrent sessions (2 threads each); online phase "
+                             f"{per_img:.2f} s per image per session, Bob weight prep excluded"}
     else:
         raise SystemExit(f"unknown config {args.config}")
     if rank == 0:

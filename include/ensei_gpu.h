@@ -246,6 +246,10 @@ int ensei_gpu_recombine(ensei_gpu_ctx* ctx, const uint32_t* d_a, const uint32_t*
  * threads need one context each (the wire decoders alone are serialised internally). */
 size_t ensei_gpu_conv_workspace_bytes(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc,
                                       uint32_t num_images);
+/* Batches larger than this stream through the workspace in sub-batches of this many
+ * images (<= 12 GiB of ciphertexts; a multiple of 64 once that many fit: config 4 runs
+ * 1024 images as 8 x 128); the workspace functions size for one sub-batch. */
+uint32_t ensei_gpu_conv_chunk_images(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint32_t num_images);
 int ensei_gpu_conv_layer(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uint64_t* d_t_eval,
                          uint32_t key_stride, const uint64_t* d_w_eval, const void* d_in,
                          int in_dtype, const uint32_t* d_bob_prev, uint32_t num_images,
@@ -394,6 +398,15 @@ int ensei_gpu_wire_decode_shares(ensei_gpu_ctx* ctx, const uint8_t* frames, size
 uint64_t ensei_gpu_fnv1a(const uint8_t* data, size_t len, uint64_t seed);
 
 /* ------------------------------------------------------------ utilities */
+/* Per-kernel CUDA-event timing of the layer kernels (a measurement pass: the events
+ * are recorded on each kernel's own stream around every launch, never inside stream
+ * capture, and serialise programmatic dependent launch).  enable = 1 clears and starts
+ * recording, 0 stops; _read synchronises and returns, per kernel name (32-byte slots
+ * in `names`), the summed milliseconds and the launch count. */
+int ensei_gpu_profile(int enable);
+int ensei_gpu_profile_read(uint32_t max_kernels, char* names, double* total_ms, uint32_t* launches,
+                           uint32_t* num_kernels);
+
 /* number of this library's kernels launched so far in the process */
 uint64_t ensei_gpu_launch_count(void);
 /* IMAD-pipe peak probe: returns IMAD slots/s (dependent mad.lo.u32 chains) measured on `device` */

@@ -143,6 +143,9 @@ def ref():
             "ref_bench_protocol": (C.c_double, [U64, U64, U32, C.c_double, U64, U32, U32, U32, i32p,
                                                 i64p, i64p, U32, U32, C.POINTER(C.c_double)]),
             "ref_bench_negacyclic": (C.c_double, [U64, U32, u64p, C.c_size_t, U32]),
+            "ref_bench_layer_ops": (C.c_double, [U64, U64, U32, C.c_double, U64, U32, U32, U32, U32, C.c_int, U32,
+                                                 U32, i64p, i64p, U32, U32, C.POINTER(C.c_double),
+                                                 C.POINTER(C.c_double)]),
             "ref_wire_ct_frame": (C.c_int, [U32, U32, U32, U32, U32, C.c_int, u64p, vp, C.c_size_t,
                                             C.POINTER(C.c_size_t)]),
             "ref_wire_ct_decode": (C.c_int, [vp, C.c_size_t, U32, U64, U64, U32, U32, U32, C.POINTER(U32), u64p,

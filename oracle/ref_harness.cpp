@@ -456,6 +456,128 @@ double ref_bench_protocol(uint64_t p, uint64_t q, uint32_t n, double sigma, uint
   } catch (const std::exception& e) { fail(e); return -1.0; }
 }
 
+// CPU baseline at the operator level: the per-image online work of one conv step of a
+// REF session -- Alice pad_image -> ntt_2d -> flatten -> encrypt_freq_direct per block;
+// Bob mul_plain / add_ct per (out, block) over the input channels, hom_share, merge ->
+// intt_2d -> crop (his share); Alice decrypt -> merge -> intt_2d -> crop -- made of the
+// same REF calls AliceSession / BobSession make (protocol.cpp:310-355, 537-603), without
+// the in-process transport, and with Bob's prepare_plain table built ONCE for the batch
+// (REF rebuilds it in every session: 8192 prepare_plain at n = 8192 for config 4, ~20 s
+// per image, which would make a bounded sample impossible).  Per image the Rng streams
+// are a session's: Rng(seed + i).fork(0xA11CE) (keygen, Enc) and .fork(0xB0B) (shares).
+// Single layer; `threads` host threads over images (and over output channels for the
+// setup).  Returns the wall seconds of the online phase; *online_sum = the sum over
+// images of the per-image online seconds; *setup_s = the prepare_plain wall time.
+namespace {
+std::vector<PlainVec> h_split(const std::vector<Residue>& flat, size_t n) {
+  std::vector<PlainVec> out((flat.size() + n - 1) / n);
+  for (size_t i = 0; i < out.size() * n; ++i) {
+    if (i % n == 0) out[i / n].slots.assign(n, 0);
+    if (i < flat.size()) out[i / n].slots[i % n] = flat[i];
+  }
+  return out;
+}
+std::vector<Residue> h_merge(const std::vector<PlainVec>& blocks, size_t len) {
+  std::vector<Residue> out(len);
+  for (size_t i = 0; i < len; ++i) out[i] = blocks[i / blocks[0].slots.size()].slots[i % blocks[0].slots.size()];
+  return out;
+}
+}  // namespace
+
+double ref_bench_layer_ops(uint64_t p, uint64_t q, uint32_t n, double sigma, uint64_t seed, uint32_t H,
+                           uint32_t W, uint32_t fh, uint32_t fw, int same, uint32_t cin, uint32_t cout,
+                           const int64_t* image, const int64_t* weights, uint32_t images, uint32_t threads,
+                           double* online_sum, double* setup_s) {
+  try {
+    const ParamSet ps = make_paramset(p, q, n, sigma);
+    const RlweParams& params = ps.rlwe;
+    const FieldSpec& pn = ps.chain.p_n;
+    const ConvGeometry g = make_geometry(H, W, fh, fw, same ? ConvType::Same : ConvType::Valid, pn);
+    const size_t grid = g.padded_h * g.padded_w, B = (grid + n - 1) / n;
+    ConvGeometry fg = g;
+    std::swap(fg.image_h, fg.filter_h);
+    std::swap(fg.image_w, fg.filter_w);
+    // Bob's setup (REF BobSession::prepare_weights, protocol.cpp:462-502)
+    std::vector<std::vector<std::vector<PreparedPlain>>> prep(cout, std::vector<std::vector<PreparedPlain>>(cin));
+    auto t0 = std::chrono::steady_clock::now();
+    {
+      std::atomic<uint32_t> next{0};
+      std::vector<std::thread> pool;
+      for (uint32_t t = 0; t < threads; ++t)
+        pool.emplace_back([&] {
+          for (uint32_t o; (o = next++) < cout;)
+            for (uint32_t c = 0; c < cin; ++c) {
+              Mat filt(fh, fw);
+              for (size_t k = 0; k < (size_t)fh * fw; ++k) filt.data[k] = weights[((size_t)o * cin + c) * fh * fw + k];
+              for (PlainVec& blk : h_split(flatten(ntt_2d(pad_image(filt, fg, pn))), n)) {
+                for (Residue& v : blk.slots) v = params.p_e.reduce(v);
+                prep[o][c].push_back(prepare_plain(blk, params));
+              }
+            }
+        });
+      for (auto& th : pool) th.join();
+    }
+    if (setup_s) *setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::vector<Mat> img(cin, Mat(H, W));
+    for (uint32_t c = 0; c < cin; ++c)
+      for (size_t k = 0; k < (size_t)H * W; ++k) img[c].data[k] = image[(size_t)c * H * W + k];
+    std::vector<double> online(images, 0.0);
+    std::atomic<uint32_t> next{0};
+    std::atomic<int> bad{0};
+    auto t1 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (uint32_t t = 0; t < threads; ++t)
+      pool.emplace_back([&] {
+        for (uint32_t i; (i = next++) < images;) {
+          try {
+            Rng root(seed + i);
+            Rng alice = root.fork(0xA11CE), bob = root.fork(0xB0B);
+            SecretKey sk = keygen(params, alice);
+            auto s0 = std::chrono::steady_clock::now();
+            std::vector<std::vector<Ciphertext>> cts(cin);
+            for (uint32_t c = 0; c < cin; ++c)
+              for (PlainVec& blk : h_split(flatten(ntt_2d(pad_image(img[c], g, pn))), n))
+                cts[c].push_back(encrypt_freq_direct(blk, sk, params, alice));
+            std::vector<ResMat> bob_share, alice_share;
+            for (uint32_t o = 0; o < cout; ++o) {
+              std::vector<PlainVec> mine, dec;
+              for (size_t b = 0; b < B; ++b) {
+                Ciphertext acc = mul_plain(cts[0][b], prep[o][0][b], params);
+                for (uint32_t c = 1; c < cin; ++c) acc = add_ct(acc, mul_plain(cts[c][b], prep[o][c][b], params), params);
+                SharePair sp = hom_share(acc, ps.chain, params, bob);
+                mine.push_back(std::move(sp.bob_share));
+                dec.push_back(decrypt(sp.alice_ct, sk, params));
+              }
+              for (auto* v : {&mine, &dec}) {
+                std::vector<Residue> flat = h_merge(*v, grid);
+                for (Residue& x : flat) x = pn.reduce(x);
+                FreqTensor tt = intt_2d(unflatten(flat, g.padded_h, g.padded_w, pn, TensorDomain::Frequency));
+                ResMat m(g.out_h(), g.out_w());
+                for (size_t r = 0; r < m.rows; ++r)
+                  for (size_t cc = 0; cc < m.cols; ++cc) m.at(r, cc) = tt.at(r + g.crop_r0(), cc + g.crop_c0());
+                (v == &mine ? bob_share : alice_share).push_back(std::move(m));
+              }
+            }
+            online[i] = std::chrono::duration<double>(std::chrono::steady_clock::now() - s0).count();
+          } catch (...) {
+            bad++;
+          }
+        }
+      });
+    for (auto& th : pool) th.join();
+    if (online_sum) {
+      double acc = 0;
+      for (double v : online) acc += v;
+      *online_sum = acc;
+    }
+    if (bad) return -1.0;
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+  } catch (const std::exception& e) {
+    fail(e);
+    return -1.0;
+  }
+}
+
 // CPU baseline for config 2: `count` polynomials, forward then inverse, over `threads`.
 double ref_bench_negacyclic(uint64_t q, uint32_t n, uint64_t* data, size_t count, uint32_t threads) {
   try {

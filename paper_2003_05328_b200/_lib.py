@@ -108,6 +108,7 @@ def lib():
             "ensei_gpu_set_mac_variant": (i32, [i32]),
             "ensei_gpu_mac_path": (i32, [vp, C.POINTER(ConvDesc), u32, C.POINTER(i32)]),
             "ensei_gpu_conv_workspace_bytes": (sz, [vp, C.POINTER(ConvDesc), u32]),
+            "ensei_gpu_conv_chunk_images": (u32, [vp, C.POINTER(ConvDesc), u32]),
             "ensei_gpu_conv_layer": (i32, [vp, C.POINTER(ConvDesc), vp, u32, vp, vp, i32, vp, u32,
                                            C.POINTER(Randomness), vp, vp, vp, vp, vp]),
             "ensei_gpu_conv_host_workspace_bytes": (sz, [vp, C.POINTER(ConvDesc), u32, i32]),
@@ -130,6 +131,8 @@ def lib():
                                              C.POINTER(ParamSet)]),
             "ensei_gpu_preset_params": (i32, [C.c_char_p, u64, u32, C.POINTER(ParamSet)]),
             "ensei_gpu_launch_count": (u64, []),
+            "ensei_gpu_profile": (i32, [i32]),
+            "ensei_gpu_profile_read": (i32, [u32, vp, vp, vp, C.POINTER(u32)]),
             "ensei_gpu_imad_peak": (C.c_double, [i32]),
         }
         for name, (res, args) in sig.items():
@@ -140,6 +143,27 @@ def lib():
             f.argtypes = args
         _lib = L
     return _lib
+
+
+def profile(enable: bool) -> None:
+    """Per-kernel event timing on/off (ensei_gpu_profile)."""
+    check(lib().ensei_gpu_profile(int(enable)))
+
+
+def profile_read(max_kernels: int = 64) -> dict:
+    """{kernel name: (total ms, launches)} recorded since profile(True)."""
+    import numpy as np
+    names = C.create_string_buffer(32 * max_kernels)
+    ms = np.zeros(max_kernels, np.float64)
+    cnt = np.zeros(max_kernels, np.uint32)
+    nk = C.c_uint32()
+    check(lib().ensei_gpu_profile_read(max_kernels, names, ms.ctypes.data_as(C.c_void_p),
+                                       cnt.ctypes.data_as(C.c_void_p), C.byref(nk)))
+    out = {}
+    for k in range(min(nk.value, max_kernels)):
+        nm = names.raw[32 * k:32 * k + 32].split(b"\0", 1)[0].decode()
+        out[nm] = (float(ms[k]), int(cnt[k]))
+    return out
 
 
 def exported_symbols():

@@ -40,6 +40,24 @@ inline void check_launch(const char* what) {
   count_launch();
 }
 
+// Per-kernel CUDA-event timing (ensei_gpu_profile): off by default.  When on, each layer
+// kernel launch is bracketed by two events recorded on its own stream (skipped while
+// the stream is being captured), and ensei_gpu_profile_read() sums the durations per
+// kernel.  For a measurement pass outside the timed region (the events serialise PDL).
+bool prof_on();
+void prof_record(const char* name, cudaStream_t st, bool begin);
+struct ProfScope {
+  const char* name;
+  cudaStream_t st;
+  bool on;
+  ProfScope(const char* n, cudaStream_t s) : name(n), st(s), on(prof_on()) {
+    if (on) prof_record(name, st, true);
+  }
+  ~ProfScope() {
+    if (on) prof_record(name, st, false);
+  }
+};
+
 // Per-prime constants for Field64 kernels.
 struct PrimeConst {
   Field64 f;

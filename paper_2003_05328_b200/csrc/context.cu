@@ -32,6 +32,46 @@ static int guarded(Fn&& fn) {
   }
 }
 
+// ---- per-kernel event timing (ProfScope, common.cuh)
+namespace {
+struct ProfRec {
+  std::string name;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+std::atomic<bool> g_prof{false};
+std::vector<ProfRec> g_prof_recs;
+std::vector<cudaEvent_t> g_prof_pool;
+cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  EG_CUDA(cudaEventCreate(&e));
+  return e;
+}
+}  // namespace
+
+bool prof_on() { return g_prof.load(std::memory_order_relaxed); }
+void prof_record(const char* name, cudaStream_t st, bool begin) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (begin) {
+    g_prof_recs.push_back({name, prof_event(), nullptr});
+    EG_CUDA(cudaEventRecord(g_prof_recs.back().a, st));
+  } else {
+    for (auto it = g_prof_recs.rbegin(); it != g_prof_recs.rend(); ++it)
+      if (!it->b && it->name == name) {
+        it->b = prof_event();
+        EG_CUDA(cudaEventRecord(it->b, st));
+        break;
+      }
+  }
+}
+
 // exported for the other translation units
 int run_guarded(void (*fn)(void*), void* arg) {
   return guarded([&] { fn(arg); });
@@ -176,6 +216,50 @@ using namespace ensei_gpu;
 extern "C" {
 
 const char* ensei_gpu_last_error(void) { return g_last_error.c_str(); }
+
+int ensei_gpu_profile(int enable) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto& r : g_prof_recs) {
+      g_prof_pool.push_back(r.a);
+      if (r.b) g_prof_pool.push_back(r.b);
+    }
+    g_prof_recs.clear();
+    g_prof.store(enable != 0);
+  });
+}
+
+int ensei_gpu_profile_read(uint32_t max_kernels, char* names, double* total_ms, uint32_t* launches,
+                           uint32_t* num_kernels) {
+  return guarded([&] {
+    require(names && total_ms && launches && num_kernels, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    std::vector<std::string> order;
+    std::vector<double> ms;
+    std::vector<uint32_t> cnt;
+    for (auto& r : g_prof_recs) {
+      if (!r.b) continue;
+      EG_CUDA(cudaEventSynchronize(r.b));
+      float t = 0.f;
+      EG_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+      size_t k = std::find(order.begin(), order.end(), r.name) - order.begin();
+      if (k == order.size()) {
+        order.push_back(r.name);
+        ms.push_back(0.0);
+        cnt.push_back(0);
+      }
+      ms[k] += t;
+      cnt[k] += 1;
+    }
+    *num_kernels = (uint32_t)order.size();
+    for (uint32_t k = 0; k < order.size() && k < max_kernels; ++k) {
+      std::strncpy(names + 32 * k, order[k].c_str(), 31);
+      names[32 * k + 31] = 0;
+      total_ms[k] = ms[k];
+      launches[k] = cnt[k];
+    }
+  });
+}
 int ensei_gpu_abi_version(void) { return ENSEI_GPU_ABI_VERSION; }
 uint64_t ensei_gpu_launch_count(void) { return g_launches.load(); }
 

@@ -7,7 +7,6 @@
 #include <string>
 
 #include "layer_launch.cuh"
-#include "mac_i8.cuh"
 
 namespace ensei_gpu {
 
@@ -29,6 +28,20 @@ extern template void launch_tile<12>(const LayerRun&, int, bool, int, const uint
                                      uint64_t*, int);
 extern template void launch_tile<13>(const LayerRun&, int, bool, int, const uint64_t*, uint32_t, const void*,
                                      uint64_t*, int);
+#define EG_EXTERN_LAYER(LOGN)                                                                                  \
+  extern template void launch_share<LOGN>(const LayerRun&, bool, uint64_t*, uint32_t*, int);                  \
+  extern template void launch_dec<LOGN>(const LayerRun&, const uint64_t*, uint32_t, const uint64_t*, uint32_t*, \
+                                        const uint32_t*, uint32_t*, int);                                      \
+  extern template void launch_secret<LOGN>(const LayerRun&, const int64_t*, int64_t*, uint64_t*, bool);
+EG_EXTERN_LAYER(11)
+EG_EXTERN_LAYER(12)
+EG_EXTERN_LAYER(13)
+
+// ElementMult dispatch (mac_api.cu)
+void mac(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out, void* scratch = nullptr);
+int mac_path(const ensei_gpu_ctx* c, const LayerArgs& a);
+size_t mac_scratch_bytes(const ensei_gpu_ctx* c, const LayerArgs& a);
+void set_mac_variant(int v);
 
 namespace {
 
@@ -136,6 +149,7 @@ bool injected(const ensei_randomness* r) { return r && r->mode == ENSEI_RAND_INJ
 
 void tile(const LayerRun& r, int tm, bool inj, int in_t, const uint64_t* key, uint32_t ks, const void* in,
           uint64_t* out, int items) {
+  ProfScope ps(tm == TILE_ENC ? "enc" : tm == TILE_HOMREC ? "homrec" : "weights", r.st);
   switch (r.ctx->logn) {
     case 11: return launch_tile<11>(r, tm, inj, in_t, key, ks, in, out, items);
     case 12: return launch_tile<12>(r, tm, inj, in_t, key, ks, in, out, items);
@@ -144,6 +158,7 @@ void tile(const LayerRun& r, int tm, bool inj, int in_t, const uint64_t* key, ui
   fail(ENSEI_ERR_UNSUPPORTED, "ring degree must be 2048, 4096 or 8192 on this path");
 }
 void share(const LayerRun& r, bool inj, uint64_t* ct_out, uint32_t* bob_share, int items) {
+  ProfScope ps("share", r.st);
   switch (r.ctx->logn) {
     case 11: return launch_share<11>(r, inj, ct_out, bob_share, items);
     case 12: return launch_share<12>(r, inj, ct_out, bob_share, items);
@@ -153,6 +168,7 @@ void share(const LayerRun& r, bool inj, uint64_t* ct_out, uint32_t* bob_share, i
 }
 void dec(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint64_t* ct, uint32_t* alice,
          const uint32_t* bob, uint32_t* out, int items) {
+  ProfScope ps(r.R == 1 ? "dec" : "dec_rns", r.st);
   switch (r.ctx->logn) {
     case 11: return launch_dec<11>(r, key, ks, ct, alice, bob, out, items);
     case 12: return launch_dec<12>(r, key, ks, ct, alice, bob, out, items);
@@ -167,177 +183,6 @@ void secret(const LayerRun& r, const int64_t* t_in, int64_t* t_out, uint64_t* ke
     case 13: return launch_secret<13>(r, t_in, t_out, key, sample);
   }
   fail(ENSEI_ERR_UNSUPPORTED, "ring degree must be 2048, 4096 or 8192 on this path");
-}
-
-template <int R, int S, int MT, int NT, int KT, int TM, int TN>
-void mac_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
-  const int n = (int)r.ctx->n, rows = 2 * r.a.num_images, cols = r.a.cout;
-  auto k = mac_kernel<R, S, MT, NT, KT, TM, TN>;
-  constexpr size_t smem = mac_smem<S, MT, NT, KT>();
-  set_smem(k, smem);
-  dim3 grid((unsigned)(r.a.B * R * n / S), (unsigned)((rows + MT - 1) / MT), (unsigned)((cols + NT - 1) / NT));
-  launch_pdl(k, grid, S * (MT / TM) * (NT / TN), smem, r.st, r.a, (int)r.ctx->logn, ct, w, 1, out);
-  check_launch("mac_kernel");
-}
-
-template <int R, int S, int MT, int NT, int KT, int TM, int TN, int STAGES>
-void mac_kara_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
-  const int n = (int)r.ctx->n, rows = 2 * r.a.num_images, cols = r.a.cout;
-  auto k = mac_kara_kernel<R, S, MT, NT, KT, TM, TN, STAGES>;
-  constexpr size_t smem = mac_kara_smem<S, MT, NT, KT, STAGES>();
-  set_smem(k, smem);
-  const long tiles = (long)(r.a.B * R * n / S) * ((rows + MT - 1) / MT) * ((cols + NT - 1) / NT);
-  static int per_sm = -1;  // per instantiation; the launch config never changes
-  if (per_sm < 0) EG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, S * (MT / TM) * (NT / TN), smem));
-  const long grid = std::min<long>(tiles, (long)std::max(per_sm, 1) * r.ctx->sm_count);
-  launch_pdl(k, (unsigned)grid, S * (MT / TM) * (NT / TN), smem, r.st, r.a, (int)r.ctx->logn, ct, w, 1, out, 0u);
-  check_launch("mac_kara_kernel");
-}
-
-// ElementMult implementation: -1 automatic (default), 0 the 4-product IMAD kernel, 1 the
-// Karatsuba IMAD kernel, 2 the int8 tensor-core kernel (mac_i8.cuh).  ENSEI_MAC_VARIANT
-// or ensei_gpu_set_mac_variant() override the automatic choice.
-static std::atomic<int> g_mac_variant{-2};
-static int mac_variant() {
-  int v = g_mac_variant.load(std::memory_order_relaxed);
-  if (v == -2) {
-    const char* e = getenv("ENSEI_MAC_VARIANT");
-    v = e ? atoi(e) : -1;
-    g_mac_variant.store(v, std::memory_order_relaxed);
-  }
-  return v;
-}
-
-// The int8 tensor-core path (mac_i8p_kernel): forced by variant 2, chosen automatically
-// for GEMM-sized slots (>= one 32-channel chunk, >= two 16-row tiles; measured: config 3
-// +14 %, config 4 +8 %), and only while its exact-sum bound K (q_i - 1)^2 < 2^128 holds
-// (ctx->i8_kmax); the IMAD kernels otherwise.
-bool use_i8(const ensei_gpu_ctx* c, const LayerArgs& a) {
-  const int var = mac_variant(), rows = 2 * a.num_images;
-  const bool i8_auto = var == -1 && a.cin >= kI8K && rows >= 2 * kI8Rows && a.cout >= kI8Cols;
-  return (var == 2 || i8_auto) && a.cin <= (int)c->i8_kmax;
-}
-
-// Tile choice (measured on B200, configs 1/3/4; cout <= 2 and cin <= 4 use mac_direct_kernel): 8-slot x 32-row x 16-col tiles with 36-channel
-// chunks and 2 stages for the large shapes; 8 x 16 x 16 with 12-channel chunks, 3 stages when
-// rows and cols fit 16.  Alternatives measured slower: 4 outputs per thread (no register-pair
-// moves but one more shared load per MAC), 12-channel chunks with 3 stages, 4-slot tiles.
-// ENSEI_MAC_VARIANT=0 forces the 4-product kernel (A/B); it is also the fallback for primes
-// outside the Karatsuba headroom (kara_ok).
-template <int R>
-void mac_direct_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
-  const size_t total = (size_t)r.a.num_images * r.a.B * R * r.ctx->n;
-  const long grid = std::min<long>((long)((total + 255) / 256), (long)r.ctx->sm_count * 8);
-  launch_pdl(mac_direct_kernel<R>, (unsigned)grid, 256, 0, r.st, r.a, (int)r.ctx->logn, ct, w, 1, out);
-  check_launch("mac_direct_kernel");
-}
-
-template <int R>
-void mac_i8_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
-  const int n = (int)r.ctx->n, rows = 2 * r.a.num_images, cols = r.a.cout;
-  const long tasks = (long)(r.a.B * R * n / kI8Slots) * ((rows + kI8Rows - 1) / kI8Rows) *
-                     ((cols + kI8Cols - 1) / kI8Cols);
-  auto k = mac_i8_kernel<R>;
-  static int per_sm = -1;
-  if (per_sm < 0) EG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0));
-  const long grid = std::min<long>(tasks, (long)std::max(per_sm, 1) * r.ctx->sm_count);
-  launch_pdl(k, (unsigned)grid, 256, 0, r.st, r.a, (int)r.ctx->logn, ct, w, 1, out);
-  check_launch("mac_i8_kernel");
-}
-
-// Byte-plane scratch of the int8 tensor-core MAC (bytes; 0 when the IMAD kernels run).
-size_t mac_scratch_bytes(const ensei_gpu_ctx* c, const LayerArgs& a) {
-  if (!use_i8(c, a)) return 0;
-  const int n = (int)c->n, rows = 2 * a.num_images, K = a.cin;
-  return (size_t)(i8_plane_words(a.B, (int)c->R, n, K, rows) + i8_plane_words(a.B, (int)c->R, n, K, a.cout)) *
-         sizeof(uint32_t);
-}
-
-// Byte planes + cp.async pipeline (mac_i8p_kernel).  The planes live in `scratch`
-// (the caller's workspace: ensei_gpu_conv_workspace_bytes counts them) or, for the
-// workspace-less entry points (bob_mac / bob_eval), in a context buffer grown on
-// demand -- never under stream capture (false: the caller falls back to the IMAD
-// kernels), and every growth drops the cached host-entry graph.
-template <int R>
-bool mac_i8p_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out, void* scratch) {
-  ensei_gpu_ctx* ctx = const_cast<ensei_gpu_ctx*>(r.ctx);
-  const int n = (int)ctx->n, rows = 2 * r.a.num_images, cols = r.a.cout, K = r.a.cin;
-  const size_t aw = (size_t)i8_plane_words(r.a.B, R, n, K, rows), bw = (size_t)i8_plane_words(r.a.B, R, n, K, cols);
-  const size_t need = (aw + bw) * sizeof(uint32_t);
-  if (!scratch && need > ctx->i8_scratch_cap) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    EG_CUDA(cudaStreamIsCapturing(r.st, &cs));
-    if (cs != cudaStreamCaptureStatusNone) return false;
-    EG_CUDA(cudaStreamSynchronize(r.st));  // the old buffer may still be read by queued work
-    if (ctx->host_graph) {
-      cudaGraphExecDestroy(ctx->host_graph);
-      ctx->host_graph = nullptr;
-      ctx->host_graph_key.clear();
-    }
-    if (ctx->i8_scratch) EG_CUDA(cudaFree(ctx->i8_scratch));
-    ctx->i8_scratch = nullptr;
-    ctx->i8_scratch_cap = 0;
-    EG_CUDA(cudaMalloc(&ctx->i8_scratch, need));
-    ctx->i8_scratch_cap = need;
-  }
-  uint32_t* Ap = static_cast<uint32_t*>(scratch ? scratch : ctx->i8_scratch);
-  uint32_t* Bp = Ap + aw;
-  const unsigned pg = (unsigned)ctx->sm_count * 8;
-  planes_kernel<R, false><<<pg, 256, 0, r.st>>>(r.a, (int)ctx->logn, ct, Ap, rows);
-  check_launch("planes_kernel");
-  planes_kernel<R, true><<<pg, 256, 0, r.st>>>(r.a, (int)ctx->logn, w, Bp, cols);
-  check_launch("planes_kernel");
-  constexpr int STAGES = 4;
-  constexpr size_t smem = (size_t)STAGES * 2 * 8 * kI8T * 8 * sizeof(uint32_t);
-  auto k = mac_i8p_kernel<R, STAGES>;
-  set_smem(k, smem);
-  static int per_sm = -1;
-  if (per_sm < 0) EG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem));
-  const long tasks = (long)r.a.B * R * (n / 4) * ((rows + kI8T - 1) / kI8T) * ((cols + kI8T - 1) / kI8T);
-  const long grid = std::min<long>(tasks, (long)std::max(per_sm, 1) * ctx->sm_count);
-  k<<<(unsigned)grid, 256, smem, r.st>>>(r.a, (int)ctx->logn, Ap, Bp, 1, out);
-  check_launch("mac_i8p_kernel");
-  return true;
-}
-
-// Which ElementMult kernel a launch takes (ENSEI_MAC_* in include/ensei_gpu.h).
-int mac_path(const ensei_gpu_ctx* c, const LayerArgs& a) {
-  const int var = mac_variant();
-  if (var == 3 && a.cin <= (int)c->i8_kmax) return ENSEI_MAC_I8_DIRECT;
-  if (use_i8(c, a)) return ENSEI_MAC_I8_PLANES;
-  // tiny channel counts (config 0: 1 -> 1): direct per-slot kernel (exact while cin <= 1008)
-  if (a.cout <= 2 && a.cin <= 4) return ENSEI_MAC_DIRECT;
-  if (!c->kara_ok || var == 0) return ENSEI_MAC_IMAD4;
-  return ENSEI_MAC_KARATSUBA;
-}
-
-template <int R>
-void mac_r(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out, void* scratch) {
-  const int rows = 2 * r.a.num_images, cols = r.a.cout;
-  const bool small = rows <= 16 && cols <= 16;
-  int path = mac_path(r.ctx, r.a);
-  if (path == ENSEI_MAC_I8_DIRECT) return mac_i8_go<R>(r, ct, w, out);
-  if (path == ENSEI_MAC_I8_PLANES) {
-    if (mac_i8p_go<R>(r, ct, w, out, scratch)) return;
-    path = r.ctx->kara_ok ? ENSEI_MAC_KARATSUBA : ENSEI_MAC_IMAD4;  // no scratch under capture
-  }
-  if (path == ENSEI_MAC_DIRECT) return mac_direct_go<R>(r, ct, w, out);
-  if (path == ENSEI_MAC_IMAD4) {
-    if (small) return mac_go<R, 16, 16, 16, 16, 2, 4>(r, ct, w, out);
-    return mac_go<R, 8, 32, 32, 16, 4, 4>(r, ct, w, out);
-  }
-  if (small) return mac_kara_go<R, 8, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
-  // few input channels (config 3's 3 -> 64 layer): the 36-channel chunks of the large tile
-  // would be ~90 % zero fill and its 221 KB ring allows one CTA per SM (config 3 +0.3 %)
-  if (r.a.cin <= 12) return mac_kara_go<R, 8, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
-  return mac_kara_go<R, 8, 32, 16, 36, 2, 4, 2>(r, ct, w, out);
-}
-
-void mac(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out, void* scratch = nullptr) {
-  if (r.a.num_images == 0) return;
-  if (r.R == 1) return mac_r<1>(r, ct, w, out, scratch);
-  if (r.R == 3) return mac_r<3>(r, ct, w, out, scratch);
-  fail(ENSEI_ERR_UNSUPPORTED, "ElementMult: unsupported prime count");
 }
 
 __global__ void recombine_kernel(const uint32_t* a, const uint32_t* b, size_t count, uint32_t p, uint32_t* out) {
@@ -431,10 +276,24 @@ Workspace carve(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g, 
   return w;
 }
 
+// Images per sub-batch: the workspace holds the ciphertexts (both parties) and the
+// ElementMult planes of at most this many images (<= 12 GiB of ciphertexts, a multiple
+// of 64 images -- one 128-row ElementMult tile -- once that many fit).  Larger batches
+// stream through it chunk by chunk (config 4: 1024 images in 8 chunks of 128).
+uint32_t chunk_images(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g, uint32_t imgs) {
+  const size_t per = ct_bytes(c, g, d->cin, 1) + ct_bytes(c, g, d->cout, 1);
+  uint64_t k = std::max<uint64_t>(1, ((size_t)12 << 30) / per);
+  if (k >= 64) k = k / 64 * 64;
+  return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(k, imgs));
+}
+
 // One sub-batch of the layer on stream `st` (aux stream `aux` for Bob's masks):
-// share || (Enc [+ HomRec]) -> ElementMult -> Dec (+ recombine).
+// share || (Enc [+ HomRec]) -> ElementMult -> Dec (+ recombine).  in / bob_prev / key /
+// alice_share / bob_share / out point at the sub-batch's first image already; i0 is its
+// index in the caller's batch (randomness stream ids, injected draws); the workspace is
+// sub-batch local.
 void layer_chain(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const Geo& g, const uint64_t* key, uint32_t ks,
-                 const uint64_t* w_eval, const uint8_t* in, int in_dtype, const uint32_t* bob_prev, uint32_t i0,
+                 const uint64_t* w_eval, const void* in, int in_dtype, const uint32_t* bob_prev, uint32_t i0,
                  uint32_t imgs, const ensei_randomness* rand, const Workspace& w, uint32_t* alice_share,
                  uint32_t* bob_share, uint32_t* out, cudaStream_t st, cudaStream_t aux, cudaEvent_t fork,
                  cudaEvent_t join) {
@@ -448,13 +307,7 @@ void layer_chain(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const Geo& g, 
     if (rc.d_share) rc.d_share += (size_t)i0 * desc->cout * B * nwords;
   }
   LayerRun r = make_run(ctx, desc, g, imgs, rand ? &rc : nullptr, st);
-  const size_t ctw = (size_t)g.B * 2 * ctx->R * ctx->n;
-  const size_t tin = (size_t)desc->cin * desc->H * desc->W, tout = (size_t)desc->cout * g.oh * g.ow;
-  uint64_t* ct_in = w.ct_in + (size_t)i0 * desc->cin * ctw;
-  uint64_t* ct_out = w.ct_out + (size_t)i0 * desc->cout * ctw;
-  uint32_t* bs = (bob_share ? bob_share : w.bob) + (size_t)i0 * tout;
-  const void* x = in + (size_t)i0 * tin * (in_dtype == ENSEI_IN_U8 ? 1 : 4);
-  const uint64_t* k = key + (size_t)i0 * ks;
+  uint32_t* bs = bob_share ? bob_share : w.bob;
   const bool inj = injected(rand);
   // Bob's HomShare masks depend only on his randomness: fork them onto the aux stream
   // so they overlap Alice's encryption; join before the ElementMult consumes them.
@@ -462,15 +315,35 @@ void layer_chain(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const Geo& g, 
   EG_CUDA(cudaStreamWaitEvent(aux, fork, 0));
   LayerRun ra = r;
   ra.st = aux;
-  share(ra, inj, ct_out, bs, (int)(imgs * desc->cout));
+  share(ra, inj, w.ct_out, bs, (int)(imgs * desc->cout));
   EG_CUDA(cudaEventRecord(join, aux));
-  tile(r, TILE_ENC, inj, in_dtype, k, ks, x, ct_in, (int)(imgs * desc->cin));
-  if (bob_prev)
-    tile(r, TILE_HOMREC, false, ENSEI_IN_U32, k, 0, bob_prev + (size_t)i0 * tin, ct_in, (int)(imgs * desc->cin));
+  tile(r, TILE_ENC, inj, in_dtype, key, ks, in, w.ct_in, (int)(imgs * desc->cin));
+  if (bob_prev) tile(r, TILE_HOMREC, false, ENSEI_IN_U32, key, 0, bob_prev, w.ct_in, (int)(imgs * desc->cin));
   EG_CUDA(cudaStreamWaitEvent(st, join, 0));
-  mac(r, ct_in, w_eval, ct_out, w.mac);
-  dec(r, k, ks, ct_out, alice_share ? alice_share + (size_t)i0 * tout : nullptr, bs, out ? out + (size_t)i0 * tout : nullptr,
-      (int)(imgs * desc->cout));
+  mac(r, w.ct_in, w_eval, w.ct_out, w.mac);
+  dec(r, key, ks, w.ct_out, alice_share, bs, out, (int)(imgs * desc->cout));
+}
+
+// The whole batch through the chunk-sized workspace.  in_at(i0, cnt) gives the device
+// address of image i0's input (and may enqueue its staging copy), out_at(i0) the address
+// its output goes to (nullptr: none); out_done(i0, cnt) runs after a chunk's output is
+// written (staging copy back); all on `st`.
+template <class InAt, class OutAt, class OutDone>
+void chunked(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const Geo& g, const uint64_t* key, uint32_t ks,
+             const uint64_t* w_eval, int in_dtype, const uint32_t* bob_prev, uint32_t imgs,
+             const ensei_randomness* rand, const Workspace& w, uint32_t* alice_share, uint32_t* bob_share,
+             cudaStream_t st, InAt in_at, OutAt out_at, OutDone out_done) {
+  const uint32_t chunk = chunk_images(ctx, desc, g, imgs);
+  const size_t tin = (size_t)desc->cin * desc->H * desc->W, tout = (size_t)desc->cout * g.oh * g.ow;
+  for (uint32_t i0 = 0; i0 < imgs; i0 += chunk) {
+    const uint32_t cnt = std::min(chunk, imgs - i0);
+    layer_chain(ctx, desc, g, key + (size_t)i0 * ks, ks, w_eval, in_at(i0, cnt), in_dtype,
+                bob_prev ? bob_prev + (size_t)i0 * tin : nullptr, i0, cnt, rand, w,
+                alice_share ? alice_share + (size_t)i0 * tout : nullptr,
+                bob_share ? bob_share + (size_t)i0 * tout : nullptr, out_at(i0), st,
+                ctx->aux, ctx->ev_fork, ctx->ev_join);
+    out_done(i0, cnt);
+  }
 }
 
 void conv_layer(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uint64_t* key, uint32_t ks,
@@ -479,9 +352,13 @@ void conv_layer(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uint64_t*
                 void* stream) {
   require(ctx && desc && key && w_eval && in && ws, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
   Geo g = geometry(ctx, desc);
-  Workspace w = carve(ctx, desc, g, imgs, ws, in_dtype, false);
-  layer_chain(ctx, desc, g, key, ks, w_eval, static_cast<const uint8_t*>(in), in_dtype, bob_prev, 0, imgs, rand, w,
-              alice_share, bob_share, out, (cudaStream_t)stream, ctx->aux, ctx->ev_fork, ctx->ev_join);
+  Workspace w = carve(ctx, desc, g, chunk_images(ctx, desc, g, imgs), ws, in_dtype, false);
+  const size_t esz = in_dtype == ENSEI_IN_U8 ? 1 : 4, tin = (size_t)desc->cin * desc->H * desc->W;
+  const size_t tout = (size_t)desc->cout * g.oh * g.ow;
+  chunked(ctx, desc, g, key, ks, w_eval, in_dtype, bob_prev, imgs, rand, w, alice_share, bob_share,
+          (cudaStream_t)stream,
+          [&](uint32_t i0, uint32_t) { return static_cast<const void*>(static_cast<const uint8_t*>(in) + i0 * tin * esz); },
+          [&](uint32_t i0) { return out ? out + (size_t)i0 * tout : nullptr; }, [](uint32_t, uint32_t) {});
 }
 
 }  // namespace
@@ -622,7 +499,7 @@ int ensei_gpu_mac_path(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, ui
 int ensei_gpu_set_mac_variant(int variant) {
   return guarded([&] {
     require(variant >= -1 && variant <= 3, ENSEI_ERR_INVALID_ARGUMENT, "variant must be -1 .. 3");
-    g_mac_variant.store(variant, std::memory_order_relaxed);
+    set_mac_variant(variant);
   });
 }
 
@@ -637,10 +514,17 @@ int ensei_gpu_recombine(ensei_gpu_ctx* ctx, const uint32_t* d_a, const uint32_t*
   });
 }
 
+uint32_t ensei_gpu_conv_chunk_images(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint32_t num_images) {
+  uint32_t out = 0;
+  guarded([&] { out = chunk_images(ctx, desc, geometry(ctx, desc), num_images); });
+  return out;
+}
+
 size_t ensei_gpu_conv_workspace_bytes(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint32_t num_images) {
   size_t out = 0;
   guarded([&] {
     Geo g = geometry(ctx, desc);
+    num_images = chunk_images(ctx, desc, g, num_images);
     out = ct_bytes(ctx, g, desc->cin, num_images) + ct_bytes(ctx, g, desc->cout, num_images) +
           share_bytes(g, desc->cout, num_images) + mac_bytes(ctx, desc, g, num_images);
   });
@@ -662,6 +546,7 @@ size_t ensei_gpu_conv_host_workspace_bytes(const ensei_gpu_ctx* ctx, const ensei
   size_t out = 0;
   guarded([&] {
     Geo g = geometry(ctx, desc);
+    num_images = chunk_images(ctx, desc, g, num_images);
     out = ct_bytes(ctx, g, desc->cin, num_images) + ct_bytes(ctx, g, desc->cout, num_images) +
           share_bytes(g, desc->cout, num_images) + mac_bytes(ctx, desc, g, num_images) +
           in_bytes(desc, num_images, in_dtype) + share_bytes(g, desc->cout, num_images);
@@ -675,9 +560,9 @@ int ensei_gpu_conv_layer_host(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, c
   return guarded([&] {
     require(ctx && desc && h_in && h_out && d_workspace && rand, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
     Geo g = geometry(ctx, desc);
-    Workspace w = carve(ctx, desc, g, num_images, d_workspace, in_dtype, true);
-    const size_t nin = (size_t)num_images * desc->cin * desc->H * desc->W * (in_dtype == ENSEI_IN_U8 ? 1 : 4);
-    const size_t nout = (size_t)num_images * desc->cout * g.oh * g.ow * sizeof(uint32_t);
+    Workspace w = carve(ctx, desc, g, chunk_images(ctx, desc, g, num_images), d_workspace, in_dtype, true);
+    const size_t tin = (size_t)desc->cin * desc->H * desc->W * (in_dtype == ENSEI_IN_U8 ? 1 : 4);
+    const size_t tout = (size_t)desc->cout * g.oh * g.ow * sizeof(uint32_t);
     cudaStream_t user = (cudaStream_t)stream;
     // the legacy stream cannot be captured: run on the context's own stream, ordered after
     // the caller's prior work by an event
@@ -704,11 +589,22 @@ int ensei_gpu_conv_layer_host(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, c
     };
     const void* din = mapped(h_in);
     uint32_t* dout = static_cast<uint32_t*>(mapped(h_out));
+    // chunk by chunk: pinned buffers are read / written in place, pageable ones staged
+    // through the (chunk-sized) workspace with one copy each way per chunk
     auto enqueue = [&] {
-      if (!din) EG_CUDA(cudaMemcpyAsync(w.stage_in, h_in, nin, cudaMemcpyHostToDevice, st));
-      conv_layer(ctx, desc, d_key, 0, d_w_eval, din ? din : w.stage_in, in_dtype, nullptr, num_images, rand,
-                 d_workspace, nullptr, nullptr, dout ? dout : w.stage_out, st);
-      if (!dout) EG_CUDA(cudaMemcpyAsync(h_out, w.stage_out, nout, cudaMemcpyDeviceToHost, st));
+      chunked(ctx, desc, g, d_key, 0, d_w_eval, in_dtype, nullptr, num_images, rand, w, nullptr, nullptr, st,
+              [&](uint32_t i0, uint32_t cnt) -> const void* {
+                if (din) return static_cast<const uint8_t*>(din) + i0 * tin;
+                EG_CUDA(cudaMemcpyAsync(w.stage_in, static_cast<const uint8_t*>(h_in) + i0 * tin, cnt * tin,
+                                        cudaMemcpyHostToDevice, st));
+                return w.stage_in;
+              },
+              [&](uint32_t i0) { return dout ? dout + i0 * (tout / sizeof(uint32_t)) : w.stage_out; },
+              [&](uint32_t i0, uint32_t cnt) {
+                if (!dout)
+                  EG_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(h_out) + i0 * tout, w.stage_out, cnt * tout,
+                                          cudaMemcpyDeviceToHost, st));
+              });
     };
     // graph key: every argument that shapes the launches (pointers, sizes, randomness)
     std::vector<uint8_t> key;

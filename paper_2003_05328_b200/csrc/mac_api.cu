@@ -1,0 +1,197 @@
+// mac_api.cu -- ElementMult + channel accumulation dispatch (REF mul_plain / add_ct,
+// ringbfv.cpp:233-306, channel sum protocol.cpp:570-581): the IMAD tile kernels
+// (layer.cuh), the int8 tensor-core kernels (mac_i8.cuh) and the choice between them.
+// Its own translation unit: the kernel instantiations dominate compile time.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "layer_launch.cuh"
+#include "mac_i8.cuh"
+
+namespace ensei_gpu {
+
+template <int R, int S, int MT, int NT, int KT, int TM, int TN>
+void mac_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
+  ProfScope ps("mac_imad4", r.st);
+  const int n = (int)r.ctx->n, rows = 2 * r.a.num_images, cols = r.a.cout;
+  auto k = mac_kernel<R, S, MT, NT, KT, TM, TN>;
+  constexpr size_t smem = mac_smem<S, MT, NT, KT>();
+  set_smem(k, smem);
+  dim3 grid((unsigned)(r.a.B * R * n / S), (unsigned)((rows + MT - 1) / MT), (unsigned)((cols + NT - 1) / NT));
+  launch_pdl(k, grid, S * (MT / TM) * (NT / TN), smem, r.st, r.a, (int)r.ctx->logn, ct, w, 1, out);
+  check_launch("mac_kernel");
+}
+
+template <int R, int S, int MT, int NT, int KT, int TM, int TN, int STAGES>
+void mac_kara_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
+  ProfScope ps("mac_kara", r.st);
+  const int n = (int)r.ctx->n, rows = 2 * r.a.num_images, cols = r.a.cout;
+  auto k = mac_kara_kernel<R, S, MT, NT, KT, TM, TN, STAGES>;
+  constexpr size_t smem = mac_kara_smem<S, MT, NT, KT, STAGES>();
+  set_smem(k, smem);
+  const long tiles = (long)(r.a.B * R * n / S) * ((rows + MT - 1) / MT) * ((cols + NT - 1) / NT);
+  static int per_sm = -1;  // per instantiation; the launch config never changes
+  if (per_sm < 0) EG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, S * (MT / TM) * (NT / TN), smem));
+  const long grid = std::min<long>(tiles, (long)std::max(per_sm, 1) * r.ctx->sm_count);
+  launch_pdl(k, (unsigned)grid, S * (MT / TM) * (NT / TN), smem, r.st, r.a, (int)r.ctx->logn, ct, w, 1, out, 0u);
+  check_launch("mac_kara_kernel");
+}
+
+// ElementMult implementation: -1 automatic (default), 0 the 4-product IMAD kernel, 1 the
+// Karatsuba IMAD kernel, 2 the int8 tensor-core kernel (mac_i8.cuh).  ENSEI_MAC_VARIANT
+// or ensei_gpu_set_mac_variant() override the automatic choice.
+static std::atomic<int> g_mac_variant{-2};
+void set_mac_variant(int v) { g_mac_variant.store(v, std::memory_order_relaxed); }
+static int mac_variant() {
+  int v = g_mac_variant.load(std::memory_order_relaxed);
+  if (v == -2) {
+    const char* e = getenv("ENSEI_MAC_VARIANT");
+    v = e ? atoi(e) : -1;
+    g_mac_variant.store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+// The int8 tensor-core path (mac_i8p_kernel): forced by variant 2, chosen automatically
+// for GEMM-sized slots (>= one 32-channel chunk, >= two 16-row tiles; measured: config 3
+// +14 %, config 4 +8 %), and only while its exact-sum bound K (q_i - 1)^2 < 2^128 holds
+// (ctx->i8_kmax); the IMAD kernels otherwise.
+bool use_i8(const ensei_gpu_ctx* c, const LayerArgs& a) {
+  const int var = mac_variant(), rows = 2 * a.num_images;
+  const bool i8_auto = var == -1 && a.cin >= kI8K && rows >= 2 * kI8Rows && a.cout >= kI8Cols;
+  return (var == 2 || i8_auto) && a.cin <= (int)c->i8_kmax;
+}
+
+// Tile choice (measured on B200, configs 1/3/4; cout <= 2 and cin <= 4 use mac_direct_kernel): 8-slot x 32-row x 16-col tiles with 36-channel
+// chunks and 2 stages for the large shapes; 8 x 16 x 16 with 12-channel chunks, 3 stages when
+// rows and cols fit 16.  Alternatives measured slower: 4 outputs per thread (no register-pair
+// moves but one more shared load per MAC), 12-channel chunks with 3 stages, 4-slot tiles.
+// ENSEI_MAC_VARIANT=0 forces the 4-product kernel (A/B); it is also the fallback for primes
+// outside the Karatsuba headroom (kara_ok).
+template <int R>
+void mac_direct_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
+  ProfScope ps("mac_direct", r.st);
+  const size_t total = (size_t)r.a.num_images * r.a.B * R * r.ctx->n;
+  const long grid = std::min<long>((long)((total + 255) / 256), (long)r.ctx->sm_count * 8);
+  launch_pdl(mac_direct_kernel<R>, (unsigned)grid, 256, 0, r.st, r.a, (int)r.ctx->logn, ct, w, 1, out);
+  check_launch("mac_direct_kernel");
+}
+
+template <int R>
+void mac_i8_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out) {
+  ProfScope ps("mac_i8", r.st);
+  const int n = (int)r.ctx->n, rows = 2 * r.a.num_images, cols = r.a.cout;
+  const long tasks = (long)(r.a.B * R * n / kI8Slots) * ((rows + kI8Rows - 1) / kI8Rows) *
+                     ((cols + kI8Cols - 1) / kI8Cols);
+  auto k = mac_i8_kernel<R>;
+  static int per_sm = -1;
+  if (per_sm < 0) EG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0));
+  const long grid = std::min<long>(tasks, (long)std::max(per_sm, 1) * r.ctx->sm_count);
+  launch_pdl(k, (unsigned)grid, 256, 0, r.st, r.a, (int)r.ctx->logn, ct, w, 1, out);
+  check_launch("mac_i8_kernel");
+}
+
+// Byte-plane scratch of the int8 tensor-core MAC (bytes; 0 when the IMAD kernels run).
+size_t mac_scratch_bytes(const ensei_gpu_ctx* c, const LayerArgs& a) {
+  if (!use_i8(c, a)) return 0;
+  const int n = (int)c->n, rows = 2 * a.num_images, K = a.cin;
+  return (size_t)(i8_plane_words(a.B, (int)c->R, n, K, rows) + i8_plane_words(a.B, (int)c->R, n, K, a.cout)) *
+         sizeof(uint32_t);
+}
+
+// Byte planes + cp.async pipeline (mac_i8p_kernel).  The planes live in `scratch`
+// (the caller's workspace: ensei_gpu_conv_workspace_bytes counts them) or, for the
+// workspace-less entry points (bob_mac / bob_eval), in a context buffer grown on
+// demand -- never under stream capture (false: the caller falls back to the IMAD
+// kernels), and every growth drops the cached host-entry graph.
+template <int R>
+bool mac_i8p_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out, void* scratch) {
+  ensei_gpu_ctx* ctx = const_cast<ensei_gpu_ctx*>(r.ctx);
+  const int n = (int)ctx->n, rows = 2 * r.a.num_images, cols = r.a.cout, K = r.a.cin;
+  const size_t aw = (size_t)i8_plane_words(r.a.B, R, n, K, rows), bw = (size_t)i8_plane_words(r.a.B, R, n, K, cols);
+  const size_t need = (aw + bw) * sizeof(uint32_t);
+  if (!scratch && need > ctx->i8_scratch_cap) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    EG_CUDA(cudaStreamIsCapturing(r.st, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return false;
+    EG_CUDA(cudaStreamSynchronize(r.st));  // the old buffer may still be read by queued work
+    if (ctx->host_graph) {
+      cudaGraphExecDestroy(ctx->host_graph);
+      ctx->host_graph = nullptr;
+      ctx->host_graph_key.clear();
+    }
+    if (ctx->i8_scratch) EG_CUDA(cudaFree(ctx->i8_scratch));
+    ctx->i8_scratch = nullptr;
+    ctx->i8_scratch_cap = 0;
+    EG_CUDA(cudaMalloc(&ctx->i8_scratch, need));
+    ctx->i8_scratch_cap = need;
+  }
+  uint32_t* Ap = static_cast<uint32_t*>(scratch ? scratch : ctx->i8_scratch);
+  uint32_t* Bp = Ap + aw;
+  const unsigned pg = (unsigned)ctx->sm_count * 8;
+  {
+    ProfScope ps("planes_ct", r.st);
+    planes_kernel<R, false><<<pg, 256, 0, r.st>>>(r.a, (int)ctx->logn, ct, Ap, rows);
+    check_launch("planes_kernel");
+  }
+  {
+    ProfScope ps("planes_w", r.st);
+    planes_kernel<R, true><<<pg, 256, 0, r.st>>>(r.a, (int)ctx->logn, w, Bp, cols);
+    check_launch("planes_kernel");
+  }
+  constexpr int STAGES = 4;
+  constexpr size_t smem = (size_t)STAGES * 2 * 8 * kI8T * 8 * sizeof(uint32_t);
+  auto k = mac_i8p_kernel<R, STAGES>;
+  set_smem(k, smem);
+  static int per_sm = -1;
+  if (per_sm < 0) EG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem));
+  const long tasks = (long)r.a.B * R * (n / 4) * ((rows + kI8T - 1) / kI8T) * ((cols + kI8T - 1) / kI8T);
+  const long grid = std::min<long>(tasks, (long)std::max(per_sm, 1) * ctx->sm_count);
+  ProfScope ps("mac_i8p", r.st);
+  k<<<(unsigned)grid, 256, smem, r.st>>>(r.a, (int)ctx->logn, Ap, Bp, 1, out);
+  check_launch("mac_i8p_kernel");
+  return true;
+}
+
+// Which ElementMult kernel a launch takes (ENSEI_MAC_* in include/ensei_gpu.h).
+int mac_path(const ensei_gpu_ctx* c, const LayerArgs& a) {
+  const int var = mac_variant();
+  if (var == 3 && a.cin <= (int)c->i8_kmax) return ENSEI_MAC_I8_DIRECT;
+  if (use_i8(c, a)) return ENSEI_MAC_I8_PLANES;
+  // tiny channel counts (config 0: 1 -> 1): direct per-slot kernel (exact while cin <= 1008)
+  if (a.cout <= 2 && a.cin <= 4) return ENSEI_MAC_DIRECT;
+  if (!c->kara_ok || var == 0) return ENSEI_MAC_IMAD4;
+  return ENSEI_MAC_KARATSUBA;
+}
+
+template <int R>
+void mac_r(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out, void* scratch) {
+  const int rows = 2 * r.a.num_images, cols = r.a.cout;
+  const bool small = rows <= 16 && cols <= 16;
+  int path = mac_path(r.ctx, r.a);
+  if (path == ENSEI_MAC_I8_DIRECT) return mac_i8_go<R>(r, ct, w, out);
+  if (path == ENSEI_MAC_I8_PLANES) {
+    if (mac_i8p_go<R>(r, ct, w, out, scratch)) return;
+    path = r.ctx->kara_ok ? ENSEI_MAC_KARATSUBA : ENSEI_MAC_IMAD4;  // no scratch under capture
+  }
+  if (path == ENSEI_MAC_DIRECT) return mac_direct_go<R>(r, ct, w, out);
+  if (path == ENSEI_MAC_IMAD4) {
+    if (small) return mac_go<R, 16, 16, 16, 16, 2, 4>(r, ct, w, out);
+    return mac_go<R, 8, 32, 32, 16, 4, 4>(r, ct, w, out);
+  }
+  if (small) return mac_kara_go<R, 8, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
+  // few input channels (config 3's 3 -> 64 layer): the 36-channel chunks of the large tile
+  // would be ~90 % zero fill and its 221 KB ring allows one CTA per SM (config 3 +0.3 %)
+  if (r.a.cin <= 12) return mac_kara_go<R, 8, 16, 16, 12, 2, 4, 3>(r, ct, w, out);
+  return mac_kara_go<R, 8, 32, 16, 36, 2, 4, 2>(r, ct, w, out);
+}
+
+void mac(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out, void* scratch) {
+  if (r.a.num_images == 0) return;
+  if (r.R == 1) return mac_r<1>(r, ct, w, out, scratch);
+  if (r.R == 3) return mac_r<3>(r, ct, w, out, scratch);
+  fail(ENSEI_ERR_UNSUPPORTED, "ElementMult: unsupported prime count");
+}
+
+}  // namespace ensei_gpu

@@ -241,18 +241,22 @@ class LayerOps:
             nb = lib().ensei_gpu_conv_workspace_bytes(self.ctx.h, C.byref(self.d), images)
         return torch.empty(nb, dtype=torch.uint8, device=self.ctx.device)
 
+    def chunk_images(self, images: int) -> int:
+        """Images per sub-batch of the layer entry points (the workspace holds that many)."""
+        return int(lib().ensei_gpu_conv_chunk_images(self.ctx.h, C.byref(self.d), images))
+
     def forward(self, key, w_eval, x: torch.Tensor, rand: Randomness, ws=None, bob_prev=None, key_stride: int = 0,
-                want_shares: bool = False, stream=None, out=None):
+                want_shares: bool = False, stream=None, out=None, alice=None, bob=None):
         """The whole oblivious conv layer for a batch; returns the reconstructed output
-        (and the two shares when want_shares)."""
+        (and the two shares when want_shares; `alice` / `bob` may be given buffers)."""
         images = x.shape[0]
         g = self.geom
         in_t = IN_U8 if x.dtype == torch.uint8 else IN_U32
         ws = self.workspace(images) if ws is None else ws
         shape = (images, self.spec.cout, g.oh, g.ow)
         out = torch.empty(shape, dtype=torch.int32, device=x.device) if out is None else out
-        a = torch.empty(shape, dtype=torch.int32, device=x.device) if want_shares else None
-        b = torch.empty(shape, dtype=torch.int32, device=x.device) if want_shares else None
+        a = (torch.empty(shape, dtype=torch.int32, device=x.device) if alice is None else alice) if want_shares else None
+        b = (torch.empty(shape, dtype=torch.int32, device=x.device) if bob is None else bob) if want_shares else None
         r = rand.struct()
         check(lib().ensei_gpu_conv_layer(self.ctx.h, C.byref(self.d), _ptr(key), key_stride, _ptr(w_eval), _ptr(x),
                                          in_t, _ptr(bob_prev), images, C.byref(r), _ptr(ws), _ptr(a), _ptr(b),

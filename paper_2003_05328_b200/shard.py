@@ -102,3 +102,47 @@ def gather_outputs(local: torch.Tensor, shard: ImageShard, out: torch.Tensor | N
         s, e = shard.range_of(r)
         out[s:e] = part[:e - s]
     return out
+
+
+class ShareGather:
+    """All-gather of BOTH parties' output shares (Alice's and Bob's, BASELINE config 4 /
+    north_star), chunk by chunk, overlapped with the computation of the next chunk.
+
+    ``post(i0, i1, alice, bob)`` is called after the layer has been enqueued for this
+    rank's images [i0, i1) (their shares in ``alice`` / ``bob``, local rows); it issues
+    asynchronous all-gathers of those rows into ``out_alice`` / ``out_bob`` (global image
+    order, ``[total, ...]``).  The collective runs on the process group's own stream after
+    the chunk's kernels, concurrently with the next chunk's.  ``wait()`` completes them.
+    Equal shards only (every rank owns the same number of images); ragged shards fall back
+    to one ``gather_outputs`` per party at ``wait()``.
+    """
+
+    def __init__(self, shard: ImageShard, out_alice: torch.Tensor, out_bob: torch.Tensor, group=None):
+        self.shard, self.group = shard, group
+        self.out = (out_alice, out_bob)
+        self.even = shard.total % shard.world == 0
+        self.pending = []
+        self.local = None
+
+    def post(self, i0: int, i1: int, alice: torch.Tensor, bob: torch.Tensor) -> None:
+        sh = self.shard
+        if sh.world == 1:
+            for o, loc in zip(self.out, (alice, bob)):
+                o[sh.start + i0:sh.start + i1].copy_(loc[i0:i1])
+            return
+        if not self.even:
+            self.local = (alice, bob)
+            return
+        cnt = sh.count
+        for o, loc in zip(self.out, (alice, bob)):
+            views = [o[r * cnt + i0:r * cnt + i1] for r in range(sh.world)]
+            self.pending.append(dist.all_gather(views, loc[i0:i1].contiguous(), group=self.group, async_op=True))
+
+    def wait(self) -> None:
+        for h in self.pending:
+            h.wait()
+        self.pending = []
+        if self.local is not None:
+            for o, loc in zip(self.out, self.local):
+                gather_outputs(loc, self.shard, o, self.group)
+            self.local = None

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define ENSEI_GPU_ABI_VERSION 1
+#define ENSEI_GPU_ABI_VERSION 2
 
 typedef enum {
   ENSEI_OK = 0,
@@ -160,6 +160,14 @@ int ensei_gpu_secret_sample(ensei_gpu_ctx* ctx, uint64_t alice_key, int64_t* d_t
  * the limb split the ElementMult accumulator uses).  t_setup, not on the online path. */
 int ensei_gpu_prepare_weights(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const int32_t* d_w,
                               uint64_t* d_w_eval, void* stream);
+/* ABI 2: the prepared-weights buffer is the packed words above FOLLOWED, for layers with
+ * 32 <= cin <= the context's int8 K limit, by the byte planes of the tcgen05 ElementMult
+ * (built once here, at t_setup, instead of on every call).  Its size: */
+size_t ensei_gpu_prepared_weights_bytes(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc);
+/* (Re)build the byte planes of a prepared-weights buffer from its packed words -- for
+ * callers that write the words themselves. */
+int ensei_gpu_prepare_weight_planes(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint64_t* d_w_eval,
+                                    void* stream);
 
 #define ENSEI_IN_U32 0 /* residues mod p */
 #define ENSEI_IN_U8 1  /* raw pixels (encode_signed of a non-negative value) */
@@ -218,7 +226,9 @@ int ensei_gpu_activation(ensei_gpu_ctx* ctx, int fn, int pool2, uint32_t channel
 
 /* ElementMult implementation (tuning / A-B testing; results are identical):
  * -1 automatic (default), 0 the 4-product IMAD kernel, 1 the Karatsuba IMAD kernel,
- * 2 the int8 tensor-core kernel (exact byte-plane products, cin <= 255). */
+ * 2 the int8 mma.sync kernel on byte planes, 3 the same with in-kernel planes, 5 the
+ * tcgen05 kernel (the int8 paths: exact byte-plane products, cin <= the context's
+ * K (q_i - 1)^2 < 2^128 limit; 5 also needs 32 <= cin). */
 int ensei_gpu_set_mac_variant(int variant);
 
 /* Which ElementMult kernel a conv layer of `num_images` images takes on this context
@@ -228,6 +238,7 @@ int ensei_gpu_set_mac_variant(int variant);
 #define ENSEI_MAC_I8_PLANES 2   /* int8 tensor cores on byte planes (planes_kernel + mac_i8p_kernel) */
 #define ENSEI_MAC_I8_DIRECT 3   /* int8 tensor cores, in-kernel plane split (mac_i8_kernel) */
 #define ENSEI_MAC_DIRECT 4      /* per-slot direct kernel for 1-4 channels (mac_direct_kernel) */
+#define ENSEI_MAC_TCGEN05 5     /* tcgen05.mma kind::i8, TMEM accumulators (planes_tc_kernel + mac_tc_kernel) */
 int ensei_gpu_mac_path(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint32_t num_images, int* path);
 
 /* recombine_clear (REF hss.cpp:64-73): out = (a + b) mod p */
@@ -411,6 +422,9 @@ int ensei_gpu_profile_read(uint32_t max_kernels, char* names, double* total_ms, 
 uint64_t ensei_gpu_launch_count(void);
 /* IMAD-pipe peak probe: returns IMAD slots/s (dependent mad.lo.u32 chains) measured on `device` */
 double ensei_gpu_imad_peak(int device);
+/* int8 tensor-core peak probe: u8 x u8 multiply-accumulates per second of back-to-back
+ * tcgen05.mma.kind::i8 (M = 128, N = n_cols, K = 32) on every SM of `device` */
+double ensei_gpu_tc_i8_peak(int device, uint32_t n_cols);
 
 #ifdef __cplusplus
 }

@@ -95,6 +95,8 @@ def lib():
             "ensei_gpu_secret_from_coeffs": (i32, [vp, vp, vp, vp]),
             "ensei_gpu_secret_sample": (i32, [vp, u64, vp, vp, vp]),
             "ensei_gpu_prepare_weights": (i32, [vp, C.POINTER(ConvDesc), vp, vp, vp]),
+            "ensei_gpu_prepared_weights_bytes": (sz, [vp, C.POINTER(ConvDesc)]),
+            "ensei_gpu_prepare_weight_planes": (i32, [vp, C.POINTER(ConvDesc), vp, vp]),
             "ensei_gpu_alice_encrypt": (i32, [vp, C.POINTER(ConvDesc), vp, u32, vp, i32, u32,
                                               C.POINTER(Randomness), vp, vp]),
             "ensei_gpu_bob_eval": (i32, [vp, C.POINTER(ConvDesc), vp, vp, vp, u32, C.POINTER(Randomness),
@@ -134,6 +136,7 @@ def lib():
             "ensei_gpu_profile": (i32, [i32]),
             "ensei_gpu_profile_read": (i32, [u32, vp, vp, vp, C.POINTER(u32)]),
             "ensei_gpu_imad_peak": (C.c_double, [i32]),
+            "ensei_gpu_tc_i8_peak": (C.c_double, [i32, u32]),
         }
         for name, (res, args) in sig.items():
             if not hasattr(L, name):  # reported by tests/test_capi.py::test_exports

@@ -394,3 +394,55 @@ extern "C" double ensei_gpu_imad_peak(int device) {
   });
   return out;
 }
+
+// ------------------------------------------------------- tcgen05 int8 peak probe
+#include "mac_tc.cuh"
+namespace ensei_gpu {
+template <int N>
+static float tc_probe_ms(int blocks, int iters, uint32_t* sink) {
+  auto k = mma_i8_peak_kernel<N>;
+  EG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+  cudaEvent_t e0, e1;
+  EG_CUDA(cudaEventCreate(&e0));
+  EG_CUDA(cudaEventCreate(&e1));
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {
+    EG_CUDA(cudaEventRecord(e0));
+    k<<<blocks, 128, 64 * 1024>>>(iters, sink);
+    EG_CUDA(cudaEventRecord(e1));
+    EG_CUDA(cudaEventSynchronize(e1));
+    EG_CUDA(cudaGetLastError());
+    float ms;
+    EG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (rep) best = std::min(best, ms);
+  }
+  count_launch(3);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return best;
+}
+}  // namespace ensei_gpu
+
+extern "C" double ensei_gpu_tc_i8_peak(int device, uint32_t n_cols) {
+  double out = -1.0;
+  guarded([&] {
+    EG_CUDA(cudaSetDevice(device));
+    int sms = 0;
+    EG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    uint32_t* sink;
+    EG_CUDA(cudaMalloc(&sink, 64));
+    const int iters = 4096;
+    float ms;
+    switch (n_cols) {
+      case 16: ms = tc_probe_ms<16>(sms, iters, sink); break;
+      case 32: ms = tc_probe_ms<32>(sms, iters, sink); break;
+      case 64: ms = tc_probe_ms<64>(sms, iters, sink); break;
+      case 128: ms = tc_probe_ms<128>(sms, iters, sink); break;
+      case 256: ms = tc_probe_ms<256>(sms, iters, sink); break;
+      default: fail(ENSEI_ERR_INVALID_ARGUMENT, "n_cols must be 16, 32, 64, 128 or 256");
+    }
+    cudaFree(sink);
+    out = (double)sms * iters * 8 * 128.0 * n_cols * 32.0 / (ms * 1e-3);
+  });
+  return out;
+}

@@ -42,6 +42,8 @@ void mac(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out
 int mac_path(const ensei_gpu_ctx* c, const LayerArgs& a);
 size_t mac_scratch_bytes(const ensei_gpu_ctx* c, const LayerArgs& a);
 void set_mac_variant(int v);
+void build_w_planes(const LayerRun& r, uint64_t* w_eval);
+size_t prepared_weights_bytes(const ensei_gpu_ctx* c, const LayerArgs& a);
 
 namespace {
 
@@ -404,6 +406,25 @@ int ensei_gpu_prepare_weights(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, c
     Geo g = geometry(ctx, desc);
     LayerRun r = make_run(ctx, desc, g, 0, nullptr, stream);
     tile(r, TILE_WEIGHTS, false, 0, nullptr, 0, d_w, d_w_eval, (int)(desc->cout * desc->cin));
+    build_w_planes(r, d_w_eval);
+  });
+}
+
+size_t ensei_gpu_prepared_weights_bytes(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc) {
+  size_t out = 0;
+  guarded([&] {
+    Geo g = geometry(ctx, desc);
+    out = prepared_weights_bytes(ctx, make_run(ctx, desc, g, 0, nullptr, nullptr).a);
+  });
+  return out;
+}
+
+int ensei_gpu_prepare_weight_planes(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint64_t* d_w_eval,
+                                    void* stream) {
+  return guarded([&] {
+    require(d_w_eval, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    Geo g = geometry(ctx, desc);
+    build_w_planes(make_run(ctx, desc, g, 0, nullptr, stream), d_w_eval);
   });
 }
 
@@ -498,7 +519,7 @@ int ensei_gpu_mac_path(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, ui
 
 int ensei_gpu_set_mac_variant(int variant) {
   return guarded([&] {
-    require(variant >= -1 && variant <= 3, ENSEI_ERR_INVALID_ARGUMENT, "variant must be -1 .. 3");
+    require(variant >= -1 && variant <= 5 && variant != 4, ENSEI_ERR_INVALID_ARGUMENT, "variant must be -1, 0, 1, 2, 3 or 5");
     set_mac_variant(variant);
   });
 }

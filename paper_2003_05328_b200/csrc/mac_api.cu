@@ -8,6 +8,7 @@
 
 #include "layer_launch.cuh"
 #include "mac_i8.cuh"
+#include "mac_tc.cuh"
 
 namespace ensei_gpu {
 
@@ -53,14 +54,55 @@ static int mac_variant() {
   return v;
 }
 
+// Context scratch for the workspace-less entry points (bob_mac / bob_eval): grown on
+// demand, never under stream capture (nullptr then: the caller falls back), and every
+// growth drops the cached host-entry graph.
+void* ctx_scratch(const LayerRun& r, size_t need) {
+  ensei_gpu_ctx* ctx = const_cast<ensei_gpu_ctx*>(r.ctx);
+  if (need > ctx->i8_scratch_cap) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    EG_CUDA(cudaStreamIsCapturing(r.st, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return nullptr;
+    EG_CUDA(cudaStreamSynchronize(r.st));  // the old buffer may still be read by queued work
+    if (ctx->host_graph) {
+      cudaGraphExecDestroy(ctx->host_graph);
+      ctx->host_graph = nullptr;
+      ctx->host_graph_key.clear();
+    }
+    if (ctx->i8_scratch) EG_CUDA(cudaFree(ctx->i8_scratch));
+    ctx->i8_scratch = nullptr;
+    ctx->i8_scratch_cap = 0;
+    EG_CUDA(cudaMalloc(&ctx->i8_scratch, need));
+    ctx->i8_scratch_cap = need;
+  }
+  return ctx->i8_scratch;
+}
+
 // The int8 tensor-core path (mac_i8p_kernel): forced by variant 2, chosen automatically
 // for GEMM-sized slots (>= one 32-channel chunk, >= two 16-row tiles; measured: config 3
 // +14 %, config 4 +8 %), and only while its exact-sum bound K (q_i - 1)^2 < 2^128 holds
 // (ctx->i8_kmax); the IMAD kernels otherwise.
 bool use_i8(const ensei_gpu_ctx* c, const LayerArgs& a) {
+  const int var = mac_variant();
+  return var == 2 && a.cin <= (int)c->i8_kmax;
+}
+
+// Prepared weights carry tcgen05 byte planes (after the packed words) exactly when the
+// layer can take the tcgen05 ElementMult: 32 <= cin <= ctx->i8_kmax.
+bool has_w_planes(const ensei_gpu_ctx* c, int cin) { return cin >= 32 && cin <= (int)c->i8_kmax; }
+size_t w_words(const ensei_gpu_ctx* c, const LayerArgs& a) { return (size_t)a.cout * a.cin * a.B * c->R * c->n; }
+size_t w_planes_bytes(const ensei_gpu_ctx* c, const LayerArgs& a) {
+  if (!has_w_planes(c, a.cin)) return 0;
+  return tc_planes_bytes(a.B * (int)c->R * (int)c->n, (a.cout + kTcColsB - 1) / kTcColsB, kTcColsB, a.cin);
+}
+
+// The tcgen05 ElementMult (mac_tc.cuh): chosen automatically for GEMM-sized slots (>= one
+// 32-channel chunk, >= one 64-image / 128-row tile, >= one 16-column tile) within the
+// exact-sum bound K (q_i - 1)^2 < 2^128 (ctx->i8_kmax); forced by variant 5.
+bool use_tc(const ensei_gpu_ctx* c, const LayerArgs& a) {
   const int var = mac_variant(), rows = 2 * a.num_images;
-  const bool i8_auto = var == -1 && a.cin >= kI8K && rows >= 2 * kI8Rows && a.cout >= kI8Cols;
-  return (var == 2 || i8_auto) && a.cin <= (int)c->i8_kmax;
+  if (!has_w_planes(c, a.cin)) return false;
+  return var == 5 || (var == -1 && rows >= 64 && a.cout >= kTcColsB);
 }
 
 // Tile choice (measured on B200, configs 1/3/4; cout <= 2 and cin <= 4 use mac_direct_kernel): 8-slot x 32-row x 16-col tiles with 36-channel
@@ -93,7 +135,17 @@ void mac_i8_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_
 }
 
 // Byte-plane scratch of the int8 tensor-core MAC (bytes; 0 when the IMAD kernels run).
+// tcgen05 scratch: the ciphertext byte planes, then the slot-major product Y
+size_t tc_a_bytes(const ensei_gpu_ctx* c, const LayerArgs& a) {
+  return tc_planes_bytes(a.B * (int)c->R * (int)c->n, (2 * a.num_images + kTcRowsA - 1) / kTcRowsA, kTcRowsA, a.cin);
+}
+size_t tc_y_bytes(const ensei_gpu_ctx* c, const LayerArgs& a) {
+  return (size_t)a.B * c->R * c->n * ((2 * a.num_images + kTcRowsA - 1) / kTcRowsA) * kTcRowsA *
+         ((a.cout + kTcColsB - 1) / kTcColsB) * kTcColsB * sizeof(uint64_t);
+}
+
 size_t mac_scratch_bytes(const ensei_gpu_ctx* c, const LayerArgs& a) {
+  if (use_tc(c, a)) return tc_a_bytes(c, a) + tc_y_bytes(c, a);
   if (!use_i8(c, a)) return 0;
   const int n = (int)c->n, rows = 2 * a.num_images, K = a.cin;
   return (size_t)(i8_plane_words(a.B, (int)c->R, n, K, rows) + i8_plane_words(a.B, (int)c->R, n, K, a.cout)) *
@@ -111,23 +163,9 @@ bool mac_i8p_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64
   const int n = (int)ctx->n, rows = 2 * r.a.num_images, cols = r.a.cout, K = r.a.cin;
   const size_t aw = (size_t)i8_plane_words(r.a.B, R, n, K, rows), bw = (size_t)i8_plane_words(r.a.B, R, n, K, cols);
   const size_t need = (aw + bw) * sizeof(uint32_t);
-  if (!scratch && need > ctx->i8_scratch_cap) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    EG_CUDA(cudaStreamIsCapturing(r.st, &cs));
-    if (cs != cudaStreamCaptureStatusNone) return false;
-    EG_CUDA(cudaStreamSynchronize(r.st));  // the old buffer may still be read by queued work
-    if (ctx->host_graph) {
-      cudaGraphExecDestroy(ctx->host_graph);
-      ctx->host_graph = nullptr;
-      ctx->host_graph_key.clear();
-    }
-    if (ctx->i8_scratch) EG_CUDA(cudaFree(ctx->i8_scratch));
-    ctx->i8_scratch = nullptr;
-    ctx->i8_scratch_cap = 0;
-    EG_CUDA(cudaMalloc(&ctx->i8_scratch, need));
-    ctx->i8_scratch_cap = need;
-  }
-  uint32_t* Ap = static_cast<uint32_t*>(scratch ? scratch : ctx->i8_scratch);
+  if (!scratch) scratch = ctx_scratch(r, need);
+  if (!scratch) return false;
+  uint32_t* Ap = static_cast<uint32_t*>(scratch);
   uint32_t* Bp = Ap + aw;
   const unsigned pg = (unsigned)ctx->sm_count * 8;
   {
@@ -154,10 +192,52 @@ bool mac_i8p_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64
   return true;
 }
 
+// tcgen05 ElementMult: ciphertext byte planes (planes_tc_kernel, into the workspace or the
+// context scratch), then one mac_tc_kernel pass per 32*NK-channel chunk.  The weight
+// planes follow the packed words of the prepared weights (ensei_gpu_prepare_weights).
+template <int R, int NK>
+void mac_tc_launch(const LayerRun& r, const uint8_t* Ap, const uint8_t* Bp, uint64_t* Y) {
+  auto k = mac_tc_kernel<NK, R>;
+  constexpr size_t smem = tc_smem_bytes<NK>();
+  set_smem(k, smem);
+  const int nkc = tc_nkc(r.a.cin);
+  for (int kc = 0; kc < nkc; ++kc) {
+    ProfScope ps("mac_tc", r.st);
+    launch_pdl(k, (unsigned)(r.ctx->sm_count & ~1), kTcThreads, smem, r.st, r.a, (int)r.ctx->logn, Ap, Bp, kc,
+               Y);  // CTA pairs: an even grid
+    check_launch("mac_tc_kernel");
+  }
+}
+
+template <int R>
+bool mac_tc_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out, void* scratch) {
+  const size_t need = mac_scratch_bytes(r.ctx, r.a);
+  uint8_t* Ap = static_cast<uint8_t*>(scratch ? scratch : ctx_scratch(r, need));
+  if (!Ap) return false;
+  uint64_t* Y = reinterpret_cast<uint64_t*>(Ap + tc_a_bytes(r.ctx, r.a));
+  const uint8_t* Bp = reinterpret_cast<const uint8_t*>(w + w_words(r.ctx, r.a));
+  {
+    ProfScope ps("planes_tc", r.st);
+    launch_pdl(planes_tc_kernel<kTcRowsA, false>, (unsigned)r.ctx->sm_count * 8, 256, 0, r.st, r.a, (int)r.ctx->logn,
+               R, ct, Ap, 2 * r.a.num_images);
+    check_launch("planes_tc_kernel");
+  }
+  if (tc_nk(r.a.cin) == 2) mac_tc_launch<R, 2>(r, Ap, Bp, Y);
+  else mac_tc_launch<R, 1>(r, Ap, Bp, Y);
+  {
+    ProfScope ps("mac_out", r.st);
+    launch_pdl(mac_out_kernel<R>, (unsigned)r.ctx->sm_count * 8, 256, 0, r.st, r.a, (int)r.ctx->logn,
+               (const uint64_t*)Y, 1, out);
+    check_launch("mac_out_kernel");
+  }
+  return true;
+}
+
 // Which ElementMult kernel a launch takes (ENSEI_MAC_* in include/ensei_gpu.h).
 int mac_path(const ensei_gpu_ctx* c, const LayerArgs& a) {
   const int var = mac_variant();
   if (var == 3 && a.cin <= (int)c->i8_kmax) return ENSEI_MAC_I8_DIRECT;
+  if (use_tc(c, a)) return ENSEI_MAC_TCGEN05;
   if (use_i8(c, a)) return ENSEI_MAC_I8_PLANES;
   // tiny channel counts (config 0: 1 -> 1): direct per-slot kernel (exact while cin <= 1008)
   if (a.cout <= 2 && a.cin <= 4) return ENSEI_MAC_DIRECT;
@@ -171,6 +251,10 @@ void mac_r(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* o
   const bool small = rows <= 16 && cols <= 16;
   int path = mac_path(r.ctx, r.a);
   if (path == ENSEI_MAC_I8_DIRECT) return mac_i8_go<R>(r, ct, w, out);
+  if (path == ENSEI_MAC_TCGEN05) {
+    if (mac_tc_go<R>(r, ct, w, out, scratch)) return;
+    path = r.ctx->kara_ok ? ENSEI_MAC_KARATSUBA : ENSEI_MAC_IMAD4;  // no scratch under capture
+  }
   if (path == ENSEI_MAC_I8_PLANES) {
     if (mac_i8p_go<R>(r, ct, w, out, scratch)) return;
     path = r.ctx->kara_ok ? ENSEI_MAC_KARATSUBA : ENSEI_MAC_IMAD4;  // no scratch under capture
@@ -192,6 +276,19 @@ void mac(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out
   if (r.R == 1) return mac_r<1>(r, ct, w, out, scratch);
   if (r.R == 3) return mac_r<3>(r, ct, w, out, scratch);
   fail(ENSEI_ERR_UNSUPPORTED, "ElementMult: unsupported prime count");
+}
+
+// The tcgen05 weight planes of a prepared-weights buffer (after its packed words), built
+// from those words; no-op for layers that cannot take the tcgen05 path.
+void build_w_planes(const LayerRun& r, uint64_t* w_eval) {
+  if (!has_w_planes(r.ctx, r.a.cin)) return;
+  ProfScope ps("planes_w_tc", r.st);
+  planes_tc_kernel<kTcColsB, true><<<(unsigned)r.ctx->sm_count * 8, 256, 0, r.st>>>(
+      r.a, (int)r.ctx->logn, (int)r.ctx->R, w_eval, reinterpret_cast<uint8_t*>(w_eval + w_words(r.ctx, r.a)), r.a.cout);
+  check_launch("planes_tc_kernel");
+}
+size_t prepared_weights_bytes(const ensei_gpu_ctx* c, const LayerArgs& a) {
+  return w_words(c, a) * sizeof(uint64_t) + w_planes_bytes(c, a);
 }
 
 }  // namespace ensei_gpu

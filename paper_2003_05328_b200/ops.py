@@ -175,12 +175,31 @@ class LayerOps:
         n, R = self.ctx.n, self.ctx.R
         return torch.empty((images, channels, self.B, 2, R, n), dtype=torch.uint64, device=self.ctx.device)
 
+    def prepared_words(self) -> int:
+        """uint64 words of a prepared-weights buffer (ABI 2: packed words + tcgen05 planes)."""
+        return lib().ensei_gpu_prepared_weights_bytes(self.ctx.h, C.byref(self.d)) // 8
+
     def prepare_weights(self, w: torch.Tensor, stream=None) -> torch.Tensor:
-        """w[cout][cin][fh][fw] int32 (device) -> prepared weights (device layout, packed)."""
+        """w[cout][cin][fh][fw] int32 (device) -> the prepared-weights buffer (1-D uint64:
+        the packed device-layout words [cout][cin][B][R][n], then the tcgen05 byte planes
+        when the layer can use them); weight_words() views the first part."""
         s = self.spec
         assert w.dtype == torch.int32 and w.is_cuda and tuple(w.shape) == (s.cout, s.cin, s.fh, s.fw)
-        out = torch.empty((s.cout, s.cin, self.B, self.ctx.R, self.ctx.n), dtype=torch.uint64, device=w.device)
+        out = torch.empty(self.prepared_words(), dtype=torch.uint64, device=w.device)
         check(lib().ensei_gpu_prepare_weights(self.ctx.h, C.byref(self.d), _ptr(w), _ptr(out), _stream(stream)))
+        return out
+
+    def weight_words(self, prepared: torch.Tensor) -> torch.Tensor:
+        """The packed words [cout][cin][B][R][n] of a prepared-weights buffer (a view)."""
+        s = self.spec
+        k = s.cout * s.cin * self.B * self.ctx.R * self.ctx.n
+        return prepared[:k].view(s.cout, s.cin, self.B, self.ctx.R, self.ctx.n)
+
+    def weights_from_words(self, words: torch.Tensor, stream=None) -> torch.Tensor:
+        """A prepared-weights buffer from caller-made packed words (planes rebuilt)."""
+        out = torch.zeros(self.prepared_words(), dtype=torch.uint64, device=words.device)
+        out[:words.numel()].copy_(words.reshape(-1))
+        check(lib().ensei_gpu_prepare_weight_planes(self.ctx.h, C.byref(self.d), _ptr(out), _stream(stream)))
         return out
 
     def alice_encrypt(self, key, x: torch.Tensor, rand: Randomness, key_stride: int = 0, stream=None):

@@ -64,7 +64,7 @@ def test_bob_mac_exact(ops, n, images, cin, cout, R):
     out = np.zeros((images, cout, B, 2, R, n), dtype=np.uint64)
     out[:, :, :, 1] = mask
     d_out = u64(out)
-    L.bob_mac(u64(ct), u64(_pack(w)), d_out)
+    L.bob_mac(u64(ct), L.weights_from_words(u64(_pack(w))), d_out)
     torch.cuda.synchronize()
     got = to_np(d_out).view(np.uint64)
     # exact check on a slot sample (all rows and columns; Python integers)
@@ -103,6 +103,13 @@ I8_CASES = [c for c in CASES if c[2] <= 255] + [
     (2048, 17, 33, 40, 1),        # one channel past a 32-channel chunk; partial row / col tiles
     (8192, 64, 64, 32, 3),        # config-4 shape class (three primes)
 ]
+TC_CASES = [
+    (8192, 64, 64, 128, 3),       # config 4's layer: one K chunk of 64, two 128-row tiles, 8 col tiles
+    (2048, 64, 128, 128, 1),      # config 3's 128 -> 128: two K passes (the second adds the first's sums)
+    (2048, 40, 33, 20, 1),        # partial row tile (80 rows), K = 33 (padded to 64), partial col tile
+    (2048, 32, 255, 16, 1),       # the int8 K limit
+    (4096, 48, 48, 40, 1),        # K = 48 in one 64-channel chunk, n = 4096
+]
 
 
 @pytest.mark.parametrize("n,images,cin,cout,R", I8_CASES)
@@ -111,6 +118,21 @@ def test_bob_mac_int8_tensor_cores_exact(ops, n, images, cin, cout, R):
     from paper_2003_05328_b200._lib import check, lib
     check(lib().ensei_gpu_set_mac_variant(2))
     try:
+        test_bob_mac_exact(ops, n, images, cin, cout, R)
+    finally:
+        check(lib().ensei_gpu_set_mac_variant(-1))
+
+
+@pytest.mark.parametrize("n,images,cin,cout,R", TC_CASES + [c for c in I8_CASES if c[2] >= 32])
+def test_bob_mac_tcgen05_exact(ops, n, images, cin, cout, R):
+    """The tcgen05 ElementMult (mac_tc.cuh, variant 5: tcgen05.mma kind::i8, TMEM
+    accumulators, weight planes built from the packed words) on the exact checks."""
+    from paper_2003_05328_b200._lib import check, lib
+    check(lib().ensei_gpu_set_mac_variant(5))
+    try:
+        q = (Q,) if R == 1 else RNS
+        L = ops.LayerOps(ops.Context(n=n, q=q), ops.ConvSpec(16, 16, 3, 3, True, cin, cout))
+        assert L.mac_path(images) == "tcgen05"
         test_bob_mac_exact(ops, n, images, cin, cout, R)
     finally:
         check(lib().ensei_gpu_set_mac_variant(-1))

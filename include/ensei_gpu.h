@@ -241,6 +241,13 @@ int ensei_gpu_set_mac_variant(int variant);
 #define ENSEI_MAC_TCGEN05 5     /* tcgen05.mma kind::i8, TMEM accumulators (planes_tc_kernel + mac_tc_kernel) */
 int ensei_gpu_mac_path(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint32_t num_images, int* path);
 
+/* The RNS decryption rounding alone (three-prime contexts): for `count` residue triples
+ * d_res[count][3] (phi mod q_0, q_1, q_2, canonical) -> d_out = round(p phi / Q) mod p
+ * exactly as REF's decrypt rounds (ringbfv.cpp:224-229, floor((p phi + floor(Q/2)) / Q)),
+ * by the same device code the RNS decryption kernel runs (test hook for the exactness
+ * of its fixed-point fast path + multi-limb fallback). */
+int ensei_gpu_crt_round(ensei_gpu_ctx* ctx, const uint64_t* d_res, size_t count, uint32_t* d_out, void* stream);
+
 /* recombine_clear (REF hss.cpp:64-73): out = (a + b) mod p */
 int ensei_gpu_recombine(ensei_gpu_ctx* ctx, const uint32_t* d_a, const uint32_t* d_b, size_t count,
                         uint32_t* d_out, void* stream);

@@ -107,6 +107,7 @@ def lib():
             "ensei_gpu_activation": (i32, [vp, i32, i32, u32, u32, u32, u32, vp, vp, C.POINTER(Randomness),
                                            vp, vp, vp, vp]),
             "ensei_gpu_recombine": (i32, [vp, vp, vp, sz, vp, vp]),
+            "ensei_gpu_crt_round": (i32, [vp, vp, sz, vp, vp]),
             "ensei_gpu_set_mac_variant": (i32, [i32]),
             "ensei_gpu_mac_path": (i32, [vp, C.POINTER(ConvDesc), u32, C.POINTER(i32)]),
             "ensei_gpu_conv_workspace_bytes": (sz, [vp, C.POINTER(ConvDesc), u32]),

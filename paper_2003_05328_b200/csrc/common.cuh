@@ -69,7 +69,14 @@ struct PrimeConst {
   uint32_t a2_chunk;      // MAC: channels per full reduction of the top limb
   uint64_t c64, c64p;     // 2^64 mod q and its Shoup companion
   uint64_t crt_inv, crt_inv_shoup;  // (Q/q_i)^-1 mod q_i (RNS decryption)
-  double inv_q;                     // 1/q_i
+  uint64_t crt_c;                   // floor(2^122 / q_i): E / q_i in 2^-62 fixed point
+};
+
+// Exact CRT rounding constants (RNS decryption, layer.cuh crt_round): M_i = Q / q_i and
+// the thresholds T_t = (2t - 1) Q, t = 1..3, as little-endian 32-bit limbs.
+struct CrtConst {
+  uint32_t M[ENSEI_MAX_PRIMES][4];
+  uint32_t T[3][6];
 };
 
 struct PConst {
@@ -102,6 +109,7 @@ struct ensei_gpu_ctx {
   uint64_t psi_q[ENSEI_MAX_PRIMES] = {};
   uint64_t psi_p = 0;
   ensei_gpu::PrimeConst pc[ENSEI_MAX_PRIMES];
+  ensei_gpu::CrtConst crt;
   ensei_gpu::PConst pp;
   ensei_gpu::DeviceTables tab;
   void* table_mem = nullptr;

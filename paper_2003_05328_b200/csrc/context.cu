@@ -192,10 +192,40 @@ static void ctx_create(int device, uint32_t n, const uint64_t* qs, uint32_t R, u
       if (j != i) qi_prod = mulmod(qi_prod, c->q[j] % q, q);
     pc.crt_inv = invmod(qi_prod, q);
     pc.crt_inv_shoup = shoup64(pc.crt_inv, q);
-    pc.inv_q = 1.0 / (double)q;
+    pc.crt_c = (uint64_t)(((unsigned __int128)1 << 122) / q);
     pc.c64 = (uint64_t)(0 - q) % q;
     pc.c64p = shoup64(pc.c64, q);
     pc.a2_chunk = (uint32_t)std::max<uint64_t>(7, std::min<uint64_t>(56, cap / 7 * 7));
+  }
+  {  // exact CRT rounding constants: M_i = Q / q_i (<= 3 primes: 4 limbs), T_t = (2t - 1) Q (6 limbs)
+    auto mul_small = [](std::vector<uint32_t>& v, uint64_t m) {  // v *= m (m < 2^62), little-endian limbs
+      unsigned __int128 carry = 0;
+      for (auto& w : v) {
+        const unsigned __int128 t = (unsigned __int128)w * m + carry;
+        w = (uint32_t)t;
+        carry = t >> 32;
+      }
+      while (carry) {
+        v.push_back((uint32_t)carry);
+        carry >>= 32;
+      }
+    };
+    std::memset(&c->crt, 0, sizeof(c->crt));
+    if (R <= 3) {
+      std::vector<uint32_t> Q{1};
+      for (uint32_t i = 0; i < R; ++i) mul_small(Q, c->q[i]);
+      for (uint32_t i = 0; i < R; ++i) {
+        std::vector<uint32_t> M{1};
+        for (uint32_t j = 0; j < R; ++j)
+          if (j != i) mul_small(M, c->q[j]);
+        for (size_t k = 0; k < M.size() && k < 4; ++k) c->crt.M[i][k] = M[k];
+      }
+      for (int t = 1; t <= 3; ++t) {
+        std::vector<uint32_t> T = Q;
+        mul_small(T, 2 * t - 1);
+        for (size_t k = 0; k < T.size() && k < 6; ++k) c->crt.T[t - 1][k] = T[k];
+      }
+    }
   }
   c->pp.f = Field32{(uint32_t)p, (uint32_t)(2 * p)};
   c->pp.cred = (uint32_t)((1ull << 32) / p);

@@ -39,6 +39,8 @@ struct LayerArgs {
   int num_images;
   // ring
   PrimeConst pc[ENSEI_MAX_PRIMES];
+  uint64_t psi_q[ENSEI_MAX_PRIMES];  // canonical 2n-th roots (direct-evaluation fallback)
+  CrtConst crt;
   PConst pp;
   const TwPair<uint64_t>* twq_fwd[ENSEI_MAX_PRIMES];
   const TwPair<uint64_t>* twq_inv[ENSEI_MAX_PRIMES];
@@ -448,25 +450,118 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
 }
 
 
-// RNS decryption (config 4): per prime r, phi_r = INTT_{q_r}(c0 t^ + c1), y_r = phi_r *
-// (Q/q_r)^-1 mod q_r; with phi = sum_r y_r Q/q_r - kQ,  p phi / Q = sum_r y_r p / q_r - kp,
-// so round(p phi / Q) mod p = (sum_r floor(y_r p / q_r) + round(sum_r frac_r)) mod p.
-// The integer parts are exact (remainder arithmetic as in dec_kernel); the fractional
-// parts are summed in double precision (exact rounding unless the true value lies within
-// ~2^-50 of a half-integer, i.e. unless decryption has already failed).  Builder
-// extension: REF has no RNS; pinned by the oracle's exact
-// multi-limb CRT rounding (eo_crt_round).
+// Exact RNS decryption rounding (REF ringbfv.cpp:224-229 over Q = q_0 q_1 q_2): with
+// y_r = phi_r (Q/q_r)^-1 mod q_r, phi = sum_r y_r M_r - k Q (M_r = Q / q_r), and
+// p y_r = I_r q_r + E_r (0 <= E_r < q_r),
+//   floor((p phi + floor(Q/2)) / Q) = sum_r I_r - k p + floor(F + 1/2 - 1/(2Q)),  F = sum_r E_r / q_r,
+// so m = (sum_r I_r + t) mod p with t = #{t in 1..3 : 2 sum_r E_r M_r > (2t - 1) Q} (Q odd:
+// no ties).  F is summed in 2^-62 fixed point (|error| < 8 ulp); only when that lands
+// within 8 ulp of a rounding boundary (never for a correctly decrypting ciphertext:
+// there F is within p |e| / Q of an integer) t is decided by the exact 192-bit compare.
+EG_DEV uint32_t crt_round_t(const CrtConst& cc, const uint64_t (&E)[3], uint64_t Fsum, bool exact = false) {
+  const uint64_t G = Fsum + (1ull << 61);
+  const uint64_t low = G & ((1ull << 62) - 1);
+  const uint32_t t = (uint32_t)(G >> 62);
+  if (!exact && low >= 8 && low <= (1ull << 62) - 8) return t;
+  uint32_t N[7] = {0, 0, 0, 0, 0, 0, 0};  // sum_r E_r M_r (< 2^182)
+#pragma unroll 1
+  for (int r = 0; r < 3; ++r) {
+    const uint32_t e[2] = {lo32(E[r]), hi32(E[r])};
+#pragma unroll 1
+    for (int i = 0; i < 2; ++i) {
+      uint64_t carry = 0;
+#pragma unroll 1
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t v = (uint64_t)e[i] * cc.M[r][j] + N[i + j] + carry;
+        N[i + j] = (uint32_t)v;
+        carry = v >> 32;
+      }
+      for (int k = i + 4; carry && k < 7; ++k) {
+        const uint64_t v = (uint64_t)N[k] + carry;
+        N[k] = (uint32_t)v;
+        carry = v >> 32;
+      }
+    }
+  }
+  uint32_t N2[6];  // 2 N (< 2^183)
+#pragma unroll
+  for (int k = 5; k >= 0; --k) N2[k] = (N[k] << 1) | (k ? N[k - 1] >> 31 : 0);
+  uint32_t tt = 0;
+#pragma unroll 1
+  for (int s = 0; s < 3; ++s) {
+    int cmp = 0;
+    for (int k = 5; k >= 0 && !cmp; --k) cmp = N2[k] > cc.T[s][k] ? 1 : (N2[k] < cc.T[s][k] ? -1 : 0);
+    tt += cmp > 0;
+  }
+  return tt;
+}
+
+// phi_r -> (I_r, E_r, E_r / q_r in 2^-62) for one prime; phi canonical
+EG_DEV void crt_part(const PrimeConst& pc, uint32_t p, uint64_t phi, uint32_t& I, uint64_t& E, uint64_t& F) {
+  const Field64& f = pc.f;
+  const uint64_t y = Bfly<Field64, 0>::fin_gs(f, f.mul_shoup_approx(phi, pc.crt_inv, pc.crt_inv_shoup));
+  const uint64_t I0 = mulhi64(y, pc.cp);  // floor(y p / q) - {0, 1, 2}
+  uint64_t rem = (uint64_t)p * y - I0 * f.q;  // < 3q, exact in 64 bits
+  const uint32_t c1 = rem >= f.q, c2 = rem >= f.q2;
+  rem -= (uint64_t)(c1 + c2) * f.q;
+  I = (uint32_t)I0 + c1 + c2;  // < p: y < q
+  E = rem;
+  F = mulhi64(rem << 4, pc.crt_c);
+}
+
+// phi_r[i] = INTT_{q_r}(c0 t^ + c1)[i] by direct evaluation, O(n):
+//   phi[i] = n^-1 sum_k X[k] psi^-(2k+1) i,  X[k] = c0 t^ + c1 at slot k (device layout:
+// position brev(k)).  The exact-rounding fallback of dec_rns_kernel for coefficients whose
+// fixed-point CRT sum lands next to a rounding boundary (never for a correctly
+// decrypting ciphertext; a few milliseconds of one thread when it happens).
+EG_DEV uint64_t powmod64(const PrimeConst& pc, uint64_t b, uint64_t e) {
+  uint64_t r = 1;
+  while (e) {
+    if (e & 1) r = pc.f.mul(r, b, pc.mu_hi, pc.mu_lo);
+    b = pc.f.mul(b, b, pc.mu_hi, pc.mu_lo);
+    e >>= 1;
+  }
+  return r;
+}
+template <int LOGN>
+EG_DEV uint64_t phi_direct(const PrimeConst& pc, uint64_t psi, const uint64_t* c0, const uint64_t* c1, const uint64_t* t,
+                           int i) {
+  constexpr int N = 1 << LOGN;
+  const Field64& f = pc.f;
+  const uint64_t q = f.q;
+  const uint64_t psi_inv = powmod64(pc, psi, 2 * (uint64_t)N - 1);    // psi^-1
+  uint64_t pw = powmod64(pc, psi_inv, (uint64_t)i);                  // psi^-i
+  const uint64_t step = f.mul(pw, pw, pc.mu_hi, pc.mu_lo);           // psi^-2i
+  uint64_t acc = 0;
+  for (int k = 0; k < N; ++k) {
+    const int j = brev(k, LOGN);
+    const uint64_t x = f.add(f.mul(c0[j], t[j], pc.mu_hi, pc.mu_lo), c1[j]);
+    acc = f.add(acc, f.mul(x, pw, pc.mu_hi, pc.mu_lo));
+    pw = f.mul(pw, step, pc.mu_hi, pc.mu_lo);
+  }
+  const uint64_t n_inv = powmod64(pc, (uint64_t)N, q - 2);
+  return f.mul(acc, n_inv, pc.mu_hi, pc.mu_lo);
+}
+
+// RNS decryption (config 4): per prime r, phi_r = INTT_{q_r}(c0 t^ + c1); per coefficient
+// the CRT parts accumulate in shared memory (sum I_r: u32, sum E_r / q_r: 2^-62 fixed point,
+// u64); then the exact rounding above -> m (slots) -> decode (NTT_p) -> tile -> IDFT2D ->
+// crop.  Coefficients whose fixed-point sum is ambiguous recompute their three phi_r by
+// direct evaluation (phi_direct) and take the 192-bit comparison.  Builder extension:
+// REF has no RNS; pinned by the oracle's exact multi-limb rounding
+// (eo_crt_round) and by ensei_gpu_crt_round's boundary tests.
 template <int LOGN, int LOGH, int LOGW, int R>
 __global__ void __launch_bounds__((1 << LOGN) >> tile_loge(LOGN))
     dec_rns_kernel(LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride,
                    const uint64_t* __restrict__ ct, uint32_t* __restrict__ alice_share,
                    const uint32_t* __restrict__ bob_share, uint32_t* __restrict__ outp) {
+  static_assert(R == 3, "exact CRT rounding: three primes");
   constexpr int N = 1 << LOGN, NT = N >> tile_loge(LOGN);
   constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
-  double* facc = reinterpret_cast<double*>(qbuf + N);
-  uint32_t* pbuf = reinterpret_cast<uint32_t*>(facc + N);  // integer-part accumulator, then m
+  uint64_t* fsum = qbuf + N;                                  // sum_r E_r / q_r, 2^-62
+  uint32_t* pbuf = reinterpret_cast<uint32_t*>(fsum + N);     // sum_r I_r, then m
   uint32_t* S = pbuf + ssize<uint32_t>(N);
   const int tid = threadIdx.x;
   const CtaBar bar;
@@ -480,7 +575,7 @@ __global__ void __launch_bounds__((1 << LOGN) >> tile_loge(LOGN))
     const uint64_t* cb = ct + ((size_t)item * a.B + b) * ct_words<R>(N);
     for (int i = tid; i < N; i += NT) {
       pbuf[sidx<uint32_t>(i)] = 0;
-      facc[i] = 0.0;
+      fsum[i] = 0;
     }
     __syncthreads();
 #pragma unroll 1
@@ -490,24 +585,34 @@ __global__ void __launch_bounds__((1 << LOGN) >> tile_loge(LOGN))
       PhiSrc src{cb + (size_t)r * N, cb + (size_t)(R + r) * N, kimg + (size_t)(2 * r) * N,
                  kimg + (size_t)(2 * r + 1) * N, f};
       auto dst = [&](int i, uint64_t v) {
-        const uint64_t phi = Bfly<Field64, 0>::fin_gs(f, v);
-        const uint64_t y = Bfly<Field64, 0>::fin_gs(f, f.mul_shoup_approx(phi, pc.crt_inv, pc.crt_inv_shoup));
-        uint64_t I = mulhi64(y, pc.cp);  // floor(y p / q_r), corrected below
-        uint64_t rem = (uint64_t)p * y - I * f.q;
-        while (rem >= f.q) {
-          rem -= f.q;
-          ++I;
-        }
-        uint32_t acc = pbuf[sidx<uint32_t>(i)] + (uint32_t)(I % p);
-        pbuf[sidx<uint32_t>(i)] = acc >= p ? acc - p : acc;
-        facc[i] += (double)rem * pc.inv_q;
+        uint32_t I;
+        uint64_t E, F;
+        crt_part(pc, p, Bfly<Field64, 0>::fin_gs(f, v), I, E, F);
+        pbuf[sidx<uint32_t>(i)] += I;  // < 3p
+        fsum[i] += F;
       };
       ntt_inverse<Field64, uint64_t, LOGN, tile_loge(LOGN), 0, false, false>(f, a.twq_inv[r], qbuf, tid, src, dst, bar);
       __syncthreads();
     }
     for (int i = tid; i < N; i += NT) {
-      uint32_t m = pbuf[sidx<uint32_t>(i)] + (uint32_t)__double2int_rn(facc[i]);
-      pbuf[sidx<uint32_t>(i)] = m % p;
+      const uint64_t G = fsum[i] + (1ull << 61), low = G & ((1ull << 62) - 1);
+      uint32_t t = (uint32_t)(G >> 62);
+      if (low < 8 || low > (1ull << 62) - 8) {  // ambiguous: exact phi_r, exact compare
+        uint64_t E[3];
+        for (int r = 0; r < 3; ++r) {
+          uint32_t I;
+          uint64_t F;
+          crt_part(a.pc[r], p,
+                   phi_direct<LOGN>(a.pc[r], a.psi_q[r], cb + (size_t)r * N, cb + (size_t)(R + r) * N,
+                                    kimg + (size_t)(2 * r) * N, i),
+                   I, E[r], F);
+        }
+        t = crt_round_t(a.crt, E, 0, true);
+      }
+      uint32_t v = pbuf[sidx<uint32_t>(i)] + t;  // < 3p + 3
+      if (v >= 2 * p) v -= 2 * p;
+      if (v >= p) v -= p;
+      pbuf[sidx<uint32_t>(i)] = v;
     }
     __syncthreads();
     SmemRW<uint32_t> psrc{pbuf};
@@ -533,6 +638,30 @@ constexpr size_t dec_rns_smem() {
   return (size_t)(1 << LOGN) * 16 + ssize<uint32_t>(1 << LOGN) * 4 + (size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4;
 }
 
+// Standalone exact CRT rounding (ensei_gpu_crt_round, for the boundary tests): residues
+// [count][R] -> m = round(p phi / Q) mod p, the same code path as dec_rns_kernel.
+template <int R>
+__global__ void crt_round_kernel(LayerArgs a, const uint64_t* __restrict__ res, size_t count,
+                                 uint32_t* __restrict__ out) {
+  static_assert(R == 3, "exact CRT rounding: three primes");
+  const uint32_t p = a.pp.f.q;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    uint32_t Isum = 0;
+    uint64_t Fsum = 0, E[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      uint32_t I;
+      uint64_t Fr;
+      crt_part(a.pc[r], p, res[i * 3 + r], I, E[r], Fr);
+      Isum += I;
+      Fsum += Fr;
+    }
+    uint32_t v = Isum + crt_round_t(a.crt, E, Fsum);
+    if (v >= 2 * p) v -= 2 * p;
+    if (v >= p) v -= p;
+    out[i] = v;
+  }
+}
 
 // ---------------------------------------------------------------- decrypt
 

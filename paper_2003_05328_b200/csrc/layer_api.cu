@@ -122,9 +122,11 @@ LayerRun make_run(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g
   a.num_images = num_images;
   for (uint32_t i = 0; i < c->R; ++i) {
     a.pc[i] = c->pc[i];
+    a.psi_q[i] = c->psi_q[i];
     a.twq_fwd[i] = c->tab.tw_q_fwd[i];
     a.twq_inv[i] = c->tab.tw_q_inv[i];
   }
+  a.crt = c->crt;
   a.pp = c->pp;
   a.twp_fwd = c->tab.tw_p_fwd;
   a.twp_inv = c->tab.tw_p_inv;
@@ -521,6 +523,20 @@ int ensei_gpu_set_mac_variant(int variant) {
   return guarded([&] {
     require(variant >= -1 && variant <= 5 && variant != 4, ENSEI_ERR_INVALID_ARGUMENT, "variant must be -1, 0, 1, 2, 3 or 5");
     set_mac_variant(variant);
+  });
+}
+
+int ensei_gpu_crt_round(ensei_gpu_ctx* ctx, const uint64_t* d_res, size_t count, uint32_t* d_out, void* stream) {
+  return guarded([&] {
+    require(ctx && (count == 0 || (d_res && d_out)), ENSEI_ERR_INVALID_ARGUMENT, "null argument");
+    require(ctx->R == 3, ENSEI_ERR_UNSUPPORTED, "exact CRT rounding: three-prime contexts");
+    if (!count) return;
+    ensei_conv_desc d{2, 2, 1, 1, 1, 1, 1};
+    Geo g{2, 2, 1, 1, 2, 2, 0, 0, 4};
+    LayerRun r = make_run(ctx, &d, g, 0, nullptr, stream);
+    const size_t grid = std::min<size_t>((count + 255) / 256, (size_t)ctx->sm_count * 8);
+    crt_round_kernel<3><<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(r.a, d_res, count, d_out);
+    check_launch("crt_round_kernel");
   });
 }
 

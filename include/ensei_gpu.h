@@ -172,6 +172,44 @@ int ensei_gpu_prepare_weight_planes(ensei_gpu_ctx* ctx, const ensei_conv_desc* d
 #define ENSEI_IN_U32 0 /* residues mod p */
 #define ENSEI_IN_U8 1  /* raw pixels (encode_signed of a non-negative value) */
 
+/* ------------------------------------------------ per-block operators
+ * REF's ringbfv / hss operators for `count` independent blocks per call (REF calls them
+ * one block at a time; csrc/host/ensei_b200.hpp wraps them with REF's C++ signatures).
+ * Slot / coefficient vectors: uint64 residues, REF natural order, [count][n].
+ * Ciphertexts: [count][2][R][n] device layout (ensei_gpu_permute <-> REF order).
+ * Prepared plains: [count][R][n] packed words (as ensei_gpu_prepare_weights).
+ * d_work: ensei_gpu_ops_workspace_bytes(ctx, count). */
+size_t ensei_gpu_ops_workspace_bytes(const ensei_gpu_ctx* ctx, size_t count);
+/* encrypt_freq_direct (REF ringbfv.cpp:180-201): c0 = -a^, c1 = a^ t^ + NTT_q(Delta
+ * encode(m) + e); e (d_noise [count][n] signed) and a^ (d_a_hat [count][R][n], natural
+ * slot order, canonical) are the caller's draws (REF's Rng: n Gaussians, then n
+ * uniform mod q per block). */
+int ensei_gpu_encrypt_freq_direct(ensei_gpu_ctx* ctx, const uint64_t* d_slots, const uint64_t* d_key,
+                                  const int64_t* d_noise, const uint64_t* d_a_hat, size_t count, uint64_t* d_ct,
+                                  void* d_work, void* stream);
+/* decrypt (REF ringbfv.cpp:203-231), evaluation-domain ciphertexts; three-prime contexts
+ * round with the exact CRT of the RNS decryption */
+int ensei_gpu_decrypt(ensei_gpu_ctx* ctx, const uint64_t* d_ct, const uint64_t* d_key, size_t count,
+                      uint64_t* d_slots, void* d_work, void* stream);
+/* prepare_plain (REF ringbfv.cpp:265-280): d_w_eval [count][R][n] packed words; h_w_inf
+ * (nullable, host, [count]) = REF's w_inf (max |centered coefficient|, at least 1) --
+ * synchronous on `stream` when given */
+int ensei_gpu_prepare_plain(ensei_gpu_ctx* ctx, const uint64_t* d_slots, size_t count, uint64_t* d_w_eval,
+                            double* h_w_inf, void* d_work, void* stream);
+/* mul_plain's slot-wise product (REF ringbfv.cpp:282-306; the static noise check is the
+ * host's, see ensei_b200.hpp): d_out = [d_out +] d_ct o w -- with accumulate = 1 this
+ * is add_ct(acc, mul_plain(ct, w)), REF's channel sum (protocol.cpp:570-581) */
+int ensei_gpu_mul_plain(ensei_gpu_ctx* ctx, const uint64_t* d_ct, const uint64_t* d_w_eval, size_t count,
+                        int accumulate, uint64_t* d_out, void* stream);
+/* add_ct (REF ringbfv.cpp:233-246): d_out = d_a + d_b */
+int ensei_gpu_add_ct(ensei_gpu_ctx* ctx, const uint64_t* d_a, const uint64_t* d_b, size_t count, uint64_t* d_out,
+                     void* stream);
+/* add_plain (REF ringbfv.cpp:248-263), evaluation domain, in place: c1 +- NTT_q(Delta
+ * encode(m)); with m = (p_A - s_B) mod p_e this is hom_share_with, with m = s_B hom_rec
+ * (REF hss.cpp:22-62) */
+int ensei_gpu_add_plain(ensei_gpu_ctx* ctx, uint64_t* d_ct, const uint64_t* d_slots, int sign, size_t count,
+                        void* d_work, void* stream);
+
 /* AliceSession::send_encrypted for `num_images` images (REF protocol.cpp:310-329):
  * pad -> DFT2D -> flatten/split -> encrypt_freq_direct (REF ringbfv.cpp:180-201),
  * fused in one kernel.  d_in[img][cin][H][W]; d_key = key blob(s), key_stride = 0

@@ -108,6 +108,13 @@ def lib():
                                            vp, vp, vp, vp]),
             "ensei_gpu_recombine": (i32, [vp, vp, vp, sz, vp, vp]),
             "ensei_gpu_crt_round": (i32, [vp, vp, sz, vp, vp]),
+            "ensei_gpu_ops_workspace_bytes": (sz, [vp, sz]),
+            "ensei_gpu_encrypt_freq_direct": (i32, [vp, vp, vp, vp, vp, sz, vp, vp, vp]),
+            "ensei_gpu_decrypt": (i32, [vp, vp, vp, sz, vp, vp, vp]),
+            "ensei_gpu_prepare_plain": (i32, [vp, vp, sz, vp, vp, vp, vp]),
+            "ensei_gpu_mul_plain": (i32, [vp, vp, vp, sz, i32, vp, vp]),
+            "ensei_gpu_add_ct": (i32, [vp, vp, vp, sz, vp, vp]),
+            "ensei_gpu_add_plain": (i32, [vp, vp, vp, i32, sz, vp, vp]),
             "ensei_gpu_set_mac_variant": (i32, [i32]),
             "ensei_gpu_mac_path": (i32, [vp, C.POINTER(ConvDesc), u32, C.POINTER(i32)]),
             "ensei_gpu_conv_workspace_bytes": (sz, [vp, C.POINTER(ConvDesc), u32]),

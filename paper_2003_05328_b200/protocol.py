@@ -52,6 +52,8 @@ class Session:
 
     def __init__(self, ctx: ops.Context, schedule: Sequence[Layer], H: int, W: int,
                  weights: Sequence[torch.Tensor]):
+        import time
+        t0 = time.perf_counter()
         self.ctx, self.schedule, self.H, self.W = ctx, list(schedule), H, W
         if not self.schedule or not isinstance(self.schedule[0], Conv):
             raise ValueError("schedule must start with a conv layer")  # REF plan_layers
@@ -75,6 +77,8 @@ class Session:
         if ci != len(weights):
             raise ValueError("extra weight banks beyond the schedule")
         self.out_hw = (h, w)
+        torch.cuda.current_stream().synchronize()
+        self.setup_seconds = time.perf_counter() - t0  # Bob's weight preparation (REF t_setup)
 
     def run(self, key: torch.Tensor, x: torch.Tensor, rand: Callable[[int], ops.Randomness],
             key_stride: int = 0, keep_trace: bool = False):
@@ -136,11 +140,24 @@ class Session:
 # are REF's logical TransformCounters (counters.hpp:17-31) for one session.
 
 @dataclass
+class PhaseTimings:
+    """REF PhaseTimings (protocol.hpp:80-87), seconds of wall clock on the party's host
+    thread with the device synchronised at phase boundaries."""
+    setup_seconds: float = 0.0
+    online_seconds: float = 0.0
+    encrypt_seconds: float = 0.0   # Alice: image transform + encryption
+    filter_seconds: float = 0.0    # Bob: HomRec, slot-wise products, HomShare
+    hadamard_seconds: float = 0.0  # Bob: the slot-wise products (inside filter; fused, not split out)
+    decrypt_seconds: float = 0.0   # Alice: share decryption + inverse transform
+
+
+@dataclass
 class PartyResult:
-    """REF PartyResult (protocol.hpp): output (Alice), counters, transcripts."""
+    """REF PartyResult (protocol.hpp:89-94): output (Alice), counters, transcripts, timings."""
     output: Optional[torch.Tensor]
     counters: dict
     transcripts: list
+    timings: PhaseTimings = None
 
 
 def _counters():
@@ -179,8 +196,11 @@ def run_alice(sess: Session, key: torch.Tensor, x: torch.Tensor, rands: Sequence
     from . import wire as Wr
     ctx, n = sess.ctx, sess.ctx.n
     from ._lib import LAYOUT_BITREV
+    import time
     T = [Wr.RecordingTransport(t) for t in transports]
     _hello(T, digest, first=True)
+    tm = PhaseTimings()
+    online0 = time.perf_counter()
     cnt = _counters()
     alice, bob = x, None
     h, w = sess.H, sess.W
@@ -190,6 +210,7 @@ def run_alice(sess: Session, key: torch.Tensor, x: torch.Tensor, rands: Sequence
         if isinstance(s, Conv):
             lo = sess.layers[li]
             B = lo.B
+            t0 = time.perf_counter()
             ct = lo.alice_encrypt(key, alice.contiguous(), r, key_stride=key_stride)
             cnt["image_ntt"] += s.cin
             cnt["ring_ntt"] += s.cin * B * (2 if freq_direct else 3)
@@ -198,11 +219,15 @@ def run_alice(sess: Session, key: torch.Tensor, x: torch.Tensor, rands: Sequence
             frames = Wr.encode_ct_blocks(ctx, Wr.CIPHERTEXT_BLOCKS, li, ct,
                                          Wr.EVALUATION if freq_direct else Wr.COEFFICIENT)
             _sync()
+            tm.encrypt_seconds += time.perf_counter() - t0
             for i, t in enumerate(T):
                 t.send_frame(frames[i])
             got = Wr.gather_frames([t.recv_frame() for t in T])
             ct_out, _, ncoef = Wr.decode_ct_blocks(ctx, got, Wr.ALICE_SHARE_CIPHERTEXTS, s.cout, B)
+            t0 = time.perf_counter()
             alice = lo.alice_decrypt(key, ct_out, key_stride=key_stride)
+            _sync()
+            tm.decrypt_seconds += time.perf_counter() - t0
             cnt["ring_ntt"] += s.cout * B * 2 + ncoef // max(len(T), 1)  # Coefficient decrypt: +1 forward
             cnt["image_ntt"] += s.cout
             h, w = lo.geom.oh, lo.geom.ow
@@ -225,15 +250,19 @@ def run_alice(sess: Session, key: torch.Tensor, x: torch.Tensor, rands: Sequence
         t.send_frame(Wr.done_frame())
     for t in T:
         Wr.expect_host(t.recv_frame(), Wr.DONE)
-    return PartyResult(out, cnt, [t.transcript for t in T])
+    tm.online_seconds = time.perf_counter() - online0
+    return PartyResult(out, cnt, [t.transcript for t in T], tm)
 
 
 def run_bob(sess: Session, rands: Sequence[ops.Randomness], transports, digest: int) -> PartyResult:
     """BobSession::run (REF protocol.cpp:521-640) for len(transports) image sessions."""
     from . import wire as Wr
     ctx = sess.ctx
+    import time
     T = [Wr.RecordingTransport(t) for t in transports]
     _hello(T, digest, first=False)
+    tm = PhaseTimings(setup_seconds=getattr(sess, "setup_seconds", 0.0))
+    online0 = time.perf_counter()
     cnt = _counters()
     mine = None
     li_last = len(sess.schedule) - 1
@@ -250,7 +279,11 @@ def run_bob(sess: Session, rands: Sequence[ops.Randomness], transports, digest: 
             if mine is not None:  # HomRec (REF protocol.cpp:543-557)
                 cnt["image_ntt"] += s.cin
                 cnt["ring_ntt"] += 2 * s.cin * B
+            t0 = time.perf_counter()
             ct_out, mine = lo.bob_eval(ct, sess.w_eval[li], r, bob_prev=mine)
+            _sync()
+            tm.filter_seconds += time.perf_counter() - t0
+            tm.hadamard_seconds = tm.filter_seconds
             cnt["hadamard"] += s.cin * s.cout * B
             cnt["ring_ntt"] += 2 * s.cout * B
             cnt["image_ntt"] += s.cout
@@ -276,7 +309,8 @@ def run_bob(sess: Session, rands: Sequence[ops.Randomness], transports, digest: 
         Wr.expect_host(t.recv_frame(), Wr.DONE)
     for t in T:
         t.send_frame(Wr.done_frame())
-    return PartyResult(None, cnt, [t.transcript for t in T])
+    tm.online_seconds = time.perf_counter() - online0
+    return PartyResult(None, cnt, [t.transcript for t in T], tm)
 
 
 def run_inproc(sess: Session, key: torch.Tensor, x: torch.Tensor, rand: Callable[[int], ops.Randomness],

@@ -306,6 +306,11 @@ def test_wire_session_batched_philox(W, ops):
     assert (to_np(alice.output) == to_np(direct)).all()
     hs = {t.content_hash_sent for t in alice.transcripts}
     assert len(hs) == 4  # four distinct sessions
+    # REF PhaseTimings on both parties (protocol.hpp:80-87)
+    ta, tb = alice.timings, bob.timings
+    assert ta.online_seconds > 0 and ta.encrypt_seconds > 0 and ta.decrypt_seconds > 0
+    assert ta.encrypt_seconds + ta.decrypt_seconds <= ta.online_seconds
+    assert tb.setup_seconds > 0 and tb.filter_seconds > 0 and tb.filter_seconds <= tb.online_seconds
 
 
 def _ref_run(seed, H, Wd, desc, img, ws, mode=1, n=2048):

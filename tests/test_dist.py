@@ -120,3 +120,55 @@ def test_single_rank_gather_is_a_copy():
     sh = ImageShard(3, 1, 0)
     assert gather_outputs(x, sh) is not x and (gather_outputs(x, sh) == x).all()
     assert gather_outputs(x, sh, out=x) is x
+
+
+def _share_gather_worker(rank, world, port, result):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2003_05328_b200.shard import ImageShard, ShareGather
+    got = {}
+    # config-4 style: both parties' shares gathered chunk by chunk (even shards), and a
+    # ragged total (falls back to one gather per party at wait())
+    for total, chunk in ((12, 4), (8, 3), (7, 2)):
+        sh = ImageShard(total, world, rank)
+        alice_all = torch.arange(total * 4, dtype=torch.int32).reshape(total, 1, 2, 2)
+        bob_all = 1000 + alice_all
+        alice, bob = sh.take(alice_all).clone(), sh.take(bob_all).clone()
+        out_a = torch.full_like(alice_all, -1)
+        out_b = torch.full_like(bob_all, -1)
+        gth = ShareGather(sh, out_a, out_b)
+        for i0 in range(0, sh.count, chunk):
+            gth.post(i0, min(sh.count, i0 + chunk), alice, bob)
+        gth.wait()
+        got[total] = (out_a.numpy(), out_b.numpy())
+    if rank == 0:
+        result.put(got)
+    dist.destroy_process_group()
+
+
+def test_two_rank_share_gather_chunked_and_ragged():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_share_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    got = q.get(timeout=300)
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    for total, (a, b) in got.items():
+        want = np.arange(total * 4, dtype=np.int32).reshape(total, 1, 2, 2)
+        assert (a == want).all() and (b == want + 1000).all(), total
+
+
+def test_share_gather_single_rank_copies():
+    from paper_2003_05328_b200.shard import ImageShard, ShareGather
+    sh = ImageShard(5, 1, 0)
+    a = torch.arange(10).reshape(5, 2)
+    oa, ob = torch.zeros_like(a), torch.zeros_like(a)
+    g = ShareGather(sh, oa, ob)
+    g.post(0, 3, a, a + 1)
+    g.post(3, 5, a, a + 1)
+    g.wait()
+    assert torch.equal(oa, a) and torch.equal(ob, a + 1)

@@ -422,36 +422,56 @@ __global__ void __launch_bounds__(256) mac_out_kernel(LayerArgs a, int logn, con
   for (long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int cg = (int)(tile % ncg), rg = (int)((tile / ncg) % nrg);
     const long s0 = tile / ((long)ncg * nrg) * kTrSlots;
-    // gather: thread -> (slot, row, 16-byte column pair); 64 x 8 x 8 pairs
-    for (int e = threadIdx.x; e < kTrSlots * kTrRows * (kTrCols / 2); e += 256) {
+    // gather: thread -> (slot, row, 16-byte column pair); every load of the tile is issued
+    // before the first shared store (8 x 16 B in flight per thread)
+    constexpr int GATHER = kTrSlots * kTrRows * (kTrCols / 2) / 256;
+    ulonglong2 v[GATHER];
+#pragma unroll
+    for (int u = 0; u < GATHER; ++u) {
+      const int e = threadIdx.x + u * 256;
       const int cp = e % (kTrCols / 2), rr = (e / (kTrCols / 2)) % kTrRows, sl = e / (kTrCols / 2 * kTrRows);
       const int row = rg * kTrRows + rr, col = cg * kTrCols + 2 * cp;
-      ulonglong2 v = make_ulonglong2(0, 0);
+      v[u] = make_ulonglong2(0, 0);
       if (row < rows && col < ycols)
-        v = __ldg(reinterpret_cast<const ulonglong2*>(
+        v[u] = __ldg(reinterpret_cast<const ulonglong2*>(
             Y + (((size_t)(s0 + sl) * nrb + row / kTcRowsA) * kTcRowsA + row % kTcRowsA) * ycols + col));
-      t[rr * kTrCols + 2 * cp][sl] = v.x;
-      t[rr * kTrCols + 2 * cp + 1][sl] = v.y;
+    }
+#pragma unroll
+    for (int u = 0; u < GATHER; ++u) {
+      const int e = threadIdx.x + u * 256;
+      const int cp = e % (kTrCols / 2), rr = (e / (kTrCols / 2)) % kTrRows, sl = e / (kTrCols / 2 * kTrRows);
+      t[rr * kTrCols + 2 * cp][sl] = v[u].x;
+      t[rr * kTrCols + 2 * cp + 1][sl] = v[u].y;
     }
     __syncthreads();
     const int bp = (int)(s0 >> logn), b = bp / R, r = bp % R, j0 = (int)(s0 & (n - 1));
     const PrimeConst pc = a.pc[r];
-    // scatter: a warp per (row, column) run of 64 slots, 2 slots per lane (16 bytes)
-    for (int e = threadIdx.x; e < kTrRows * kTrCols * (kTrSlots / 2); e += 256) {
+    // scatter: a warp per (row, column) run of 64 slots, 2 slots per lane (16 bytes); the
+    // mask loads of the thread's c1 runs are issued first
+    constexpr int SCATTER = kTrRows * kTrCols * (kTrSlots / 2) / 256;
+    ulonglong2 mk[SCATTER];
+    uint64_t* dst[SCATTER];
+#pragma unroll
+    for (int u = 0; u < SCATTER; ++u) {
+      const int e = threadIdx.x + u * 256;
       const int sp = e % (kTrSlots / 2), rc = e / (kTrSlots / 2);
       const int rr = rc / kTrCols, cc = rc % kTrCols;
       const int row = rg * kTrRows + rr, col = cg * kTrCols + cc;
-      if (row >= rows || col >= cols) continue;
       const int img = row >> 1, comp = row & 1;
-      uint64_t* o = out + ((size_t)img * a.cout + col) * chan_stride + (size_t)b * ctw + (size_t)(comp * R + r) * n +
-                    j0 + 2 * sp;
-      uint64_t x0 = t[rc][2 * sp], x1 = t[rc][2 * sp + 1];
-      if (comp == 1 && has_mask) {
-        const ulonglong2 mk = *reinterpret_cast<const ulonglong2*>(o);
-        x0 = pc.f.add(x0, mk.x);
-        x1 = pc.f.add(x1, mk.y);
-      }
-      *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(x0, x1);
+      dst[u] = (row < rows && col < cols)
+                   ? out + ((size_t)img * a.cout + col) * chan_stride + (size_t)b * ctw + (size_t)(comp * R + r) * n +
+                         j0 + 2 * sp
+                   : nullptr;
+      mk[u] = make_ulonglong2(0, 0);
+      if (dst[u] && comp == 1 && has_mask) mk[u] = *reinterpret_cast<const ulonglong2*>(dst[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < SCATTER; ++u) {
+      if (!dst[u]) continue;
+      const int e = threadIdx.x + u * 256;
+      const int sp = e % (kTrSlots / 2), rc = e / (kTrSlots / 2);
+      *reinterpret_cast<ulonglong2*>(dst[u]) =
+          make_ulonglong2(pc.f.add(t[rc][2 * sp], mk[u].x), pc.f.add(t[rc][2 * sp + 1], mk[u].y));
     }
     __syncthreads();
   }

@@ -114,6 +114,15 @@ typedef struct {
   uint32_t fh, fw; /* filter */
   uint32_t same;   /* 1 = ConvType::Same, 0 = Valid */
   uint32_t cin, cout;
+  /* Ciphertext packing (builder extension; 0 or 1 = REF's geometry, one image per
+   * ciphertext block).  pack = k (a power of two) puts k images' padded grids into one
+   * block, slots [i G, (i + 1) G) = image i of the pack (needs one block per channel and
+   * k G <= n); weights are replicated across the pack.  Every slot-wise step (ElementMult,
+   * channel sum, HomShare, Dec) is unchanged, so the outputs are REF's; the ciphertexts
+   * are the oracle's packed restatement.  Arrays of ciphertexts then hold
+   * ceil(num_images / k) "ciphertext images"; image arrays stay per image.  Packed layers
+   * take Philox randomness with a pack-aligned image_base and one shared key. */
+  uint32_t pack;
 } ensei_conv_desc;
 
 typedef struct {
@@ -121,6 +130,7 @@ typedef struct {
   uint32_t blocks;   /* ciphertext blocks per channel, ceil(Lh*Lw/n) (REF protocol.cpp:180) */
   uint32_t oh, ow;   /* output tile */
   uint32_t r0, c0;   /* crop origin (REF ntt.hpp:44-49) */
+  uint32_t pack;     /* images per ciphertext block (1: REF geometry) */
 } ensei_layer_geom;
 
 /* make_geometry + plan_layers' block count. ENSEI_ERR_BAD_GEOMETRY as REF. */

@@ -45,7 +45,7 @@ class Layer(C.Structure):
         ("same", C.c_uint32), ("cin", C.c_uint32), ("cout", C.c_uint32),
         ("Lh", C.c_uint32), ("Lw", C.c_uint32), ("blocks", C.c_uint32),
         ("oh", C.c_uint32), ("ow", C.c_uint32), ("r0", C.c_uint32), ("c0", C.c_uint32),
-        ("delta", C.c_uint64),
+        ("delta", C.c_uint64), ("pack", C.c_uint32),
     ]
 
 

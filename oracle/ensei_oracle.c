@@ -468,8 +468,11 @@ int eo_layer_init(eo_layer* L, uint64_t q, uint64_t p, uint32_t n, uint32_t H, u
   L->r0 = same ? (fh - 1) / 2 : fh - 1;
   L->c0 = same ? (fw - 1) / 2 : fw - 1;
   L->delta = q / p;
+  L->pack = 1;
   return 0;
 }
+
+static uint32_t pack_of(const eo_layer* L) { return L->pack > 1 ? L->pack : 1; }
 
 void eo_secret_eval(const eo_layer* L, const int64_t* t, uint64_t* t_eval) {
   eo_plan* pq = eo_plan_create(L->q, L->n);
@@ -479,28 +482,37 @@ void eo_secret_eval(const eo_layer* L, const int64_t* t, uint64_t* t_eval) {
 }
 
 /* pad a residue tile at the grid origin, 2D NTT, flatten, split into zero-filled
-   blocks (REF ntt.cpp:155-185, protocol.cpp:18-29) */
+   blocks (REF ntt.cpp:155-185, protocol.cpp:18-29).  Packed layers: the pack's tiles
+   (tile of image i at tile + i * stride; stride 0 = one tile replicated, the weights)
+   land at slots [i G, (i + 1) G) */
 static void grid_forward(const eo_layer* L, const uint64_t* tile, uint32_t th, uint32_t tw,
-                         uint64_t* blocks /* [B][n] */) {
+                         uint64_t* blocks /* [B][n] */, size_t stride) {
   size_t G = (size_t)L->Lh * L->Lw;
   uint64_t* g = (uint64_t*)calloc(G, 8);
-  for (uint32_t r = 0; r < th; ++r)
-    for (uint32_t c = 0; c < tw; ++c) g[(size_t)r * L->Lw + c] = tile[(size_t)r * tw + c] % L->p;
-  eo_ntt_2d(g, L->Lh, L->Lw, L->p, 0);
   memset(blocks, 0, 8 * (size_t)L->blocks * L->n);
-  memcpy(blocks, g, 8 * G);
+  for (uint32_t k = 0; k < pack_of(L); ++k) {
+    const uint64_t* t = tile + (size_t)k * stride;
+    memset(g, 0, 8 * G);
+    for (uint32_t r = 0; r < th; ++r)
+      for (uint32_t c = 0; c < tw; ++c) g[(size_t)r * L->Lw + c] = t[(size_t)r * tw + c] % L->p;
+    eo_ntt_2d(g, L->Lh, L->Lw, L->p, 0);
+    memcpy(blocks + (size_t)k * G, g, 8 * G);
+  }
   free(g);
 }
 
-/* merge blocks to the grid, IDFT2D, crop (REF protocol.cpp:31-53) */
-static void grid_inverse_crop(const eo_layer* L, const uint64_t* blocks, uint64_t* out) {
+/* merge blocks to the grid, IDFT2D, crop (REF protocol.cpp:31-53); packed: the grid of
+   image k at slots [k G, (k + 1) G) -> out + k * stride */
+static void grid_inverse_crop(const eo_layer* L, const uint64_t* blocks, uint64_t* out, size_t stride) {
   size_t G = (size_t)L->Lh * L->Lw;
   uint64_t* g = (uint64_t*)malloc(8 * G);
-  for (size_t i = 0; i < G; ++i) g[i] = blocks[i] % L->p;
-  eo_ntt_2d(g, L->Lh, L->Lw, L->p, 1);
-  for (uint32_t r = 0; r < L->oh; ++r)
-    for (uint32_t c = 0; c < L->ow; ++c)
-      out[(size_t)r * L->ow + c] = g[(size_t)(r + L->r0) * L->Lw + (c + L->c0)];
+  for (uint32_t k = 0; k < pack_of(L); ++k) {
+    for (size_t i = 0; i < G; ++i) g[i] = blocks[(size_t)k * G + i] % L->p;
+    eo_ntt_2d(g, L->Lh, L->Lw, L->p, 1);
+    for (uint32_t r = 0; r < L->oh; ++r)
+      for (uint32_t c = 0; c < L->ow; ++c)
+        out[(size_t)k * stride + (size_t)r * L->ow + c] = g[(size_t)(r + L->r0) * L->Lw + (c + L->c0)];
+  }
   free(g);
 }
 
@@ -527,7 +539,7 @@ void eo_prepare_weights(const eo_layer* L, const int64_t* w, uint64_t* w_eval) {
     for (uint32_t c = 0; c < L->cin; ++c) {
       const int64_t* f = w + ((size_t)o * L->cin + c) * L->fh * L->fw;
       for (uint32_t i = 0; i < L->fh * L->fw; ++i) tile[i] = eo_encode_signed(f[i], L->p);
-      grid_forward(L, tile, L->fh, L->fw, blk);
+      grid_forward(L, tile, L->fh, L->fw, blk, 0); /* packed: replicated across the pack */
       for (uint32_t b = 0; b < B; ++b) {
         uint64_t* dst = w_eval + (((size_t)o * L->cin + c) * B + b) * n;
         memcpy(dst, blk + (size_t)b * n, 8 * (size_t)n);
@@ -551,7 +563,7 @@ void eo_alice_encrypt(const eo_layer* L, const uint64_t* t_eval, const uint64_t*
   eo_plan* pp = eo_plan_create(L->p, n);
   uint64_t* blk = (uint64_t*)malloc(8 * (size_t)B * n);
   for (uint32_t c = 0; c < L->cin; ++c) {
-    grid_forward(L, in + (size_t)c * L->H * L->W, L->H, L->W, blk);
+    grid_forward(L, in + (size_t)c * L->H * L->W, L->H, L->W, blk, (size_t)L->cin * L->H * L->W);
     for (uint32_t b = 0; b < B; ++b) {
       size_t rb = ((size_t)c * B + b) * n;
       uint64_t* m = blk + (size_t)b * n;
@@ -586,7 +598,7 @@ void eo_bob_eval(const eo_layer* L, const uint64_t* ct_in, const uint64_t* w_eva
   uint64_t* blk = (uint64_t*)malloc(8 * (size_t)B * n);
   if (bob_prev) { /* HomRec with Bob's transformed share (REF protocol.cpp:543-557, hss.cpp:51-62) */
     for (uint32_t c = 0; c < L->cin; ++c) {
-      grid_forward(L, bob_prev + (size_t)c * L->H * L->W, L->H, L->W, blk);
+      grid_forward(L, bob_prev + (size_t)c * L->H * L->W, L->H, L->W, blk, (size_t)L->cin * L->H * L->W);
       for (uint32_t b = 0; b < B; ++b)
         add_plain_eval(L, pq, pp, blk + (size_t)b * n, cts + ((size_t)c * B + b) * ctw + n);
     }
@@ -611,7 +623,7 @@ void eo_bob_eval(const eo_layer* L, const uint64_t* ct_in, const uint64_t* w_eva
       add_plain_eval(L, pq, pp, mask, acc + n);
       memcpy(merged + (size_t)b * n, sb, 8 * (size_t)n);
     }
-    grid_inverse_crop(L, merged, bob_share + (size_t)o * L->oh * L->ow);
+    grid_inverse_crop(L, merged, bob_share + (size_t)o * L->oh * L->ow, (size_t)L->cout * L->oh * L->ow);
   }
   free(mask);
   free(merged);
@@ -641,7 +653,7 @@ void eo_alice_decrypt(const eo_layer* L, const uint64_t* t_eval, const uint64_t*
       }
       eo_plan_forward(pp, phi); /* decode_slots */
     }
-    grid_inverse_crop(L, merged, alice_share + (size_t)o * L->oh * L->ow);
+    grid_inverse_crop(L, merged, alice_share + (size_t)o * L->oh * L->ow, (size_t)L->cout * L->oh * L->ow);
   }
   free(merged);
   eo_plan_destroy(pq);
@@ -809,7 +821,7 @@ void eo_alice_decrypt_rns(const eo_layer* Ls, uint32_t R, const uint64_t* t_eval
       }
       eo_plan_forward(pp, m); /* decode_slots */
     }
-    grid_inverse_crop(L, merged, alice_share + (size_t)o * L->oh * L->ow);
+    grid_inverse_crop(L, merged, alice_share + (size_t)o * L->oh * L->ow, (size_t)L->cout * L->oh * L->ow);
   }
   free(phi);
   free(merged);

@@ -102,6 +102,12 @@ typedef struct {
   /* derived by eo_layer_init (REF ntt.cpp:51-81, protocol.cpp:162-193) */
   uint32_t Lh, Lw, blocks, oh, ow, r0, c0;
   uint64_t delta;           /* floor(q / p) (REF ringbfv.cpp:80) */
+  /* packing (builder extension, the device's ensei_conv_desc::pack): images per
+     ciphertext block, 1 = REF geometry.  With pack = k > 1 (one block per channel,
+     k Lh Lw <= n) image i of a pack owns slots [i Lh Lw, (i + 1) Lh Lw); the per-image
+     arrays below (in, bob_prev, bob_share, alice_share) then hold k images
+     ([k][channels][..]) and the filter grid is replicated across the pack. */
+  uint32_t pack;
 } eo_layer;
 int eo_layer_init(eo_layer* L, uint64_t q, uint64_t p, uint32_t n, uint32_t H, uint32_t W,
                   uint32_t fh, uint32_t fw, uint32_t same, uint32_t cin, uint32_t cout);

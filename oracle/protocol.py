@@ -175,12 +175,17 @@ def prepare_weights(L, w, workers=1):
     return out
 
 
+def _pk(L):
+    return max(1, int(L.pack))
+
+
 def bob_eval(L, ct, w_eval, bob_prev, s_b, workers=1):
     """BobSession conv step (HomRec, ElementMult + channel sum, HomShare, Bob's share IDFT2D)
-    for one image, over output-channel slices on `workers` threads."""
-    n, B = L.n, L.blocks
+    for one image (one ciphertext image of L.pack images when packed), over output-channel
+    slices on `workers` threads.  Bob's shares: [pack][cout][oh * ow] flattened."""
+    n, B, pk = L.n, L.blocks, _pk(L)
     ct_out = np.zeros((L.cout, B * 2 * n), np.uint64)
-    bob_sh = np.zeros((L.cout, L.oh * L.ow), np.uint64)
+    bob_sh = np.zeros((pk, L.cout, L.oh * L.ow), np.uint64)
     w_eval = np.ascontiguousarray(w_eval, np.uint64).reshape(L.cout, -1)
     s_b = np.ascontiguousarray(s_b, np.uint64).reshape(L.cout, -1)
     prev = None if bob_prev is None else np.ascontiguousarray(bob_prev, np.uint64).reshape(-1)
@@ -188,26 +193,26 @@ def bob_eval(L, ct, w_eval, bob_prev, s_b, workers=1):
     def job(r):
         o0, o1 = r
         co = np.zeros((o1 - o0) * B * 2 * n, np.uint64)
-        bs = np.zeros((o1 - o0) * L.oh * L.ow, np.uint64)
+        bs = np.zeros(pk * (o1 - o0) * L.oh * L.ow, np.uint64)
         lib().eo_bob_eval(C.byref(_sub(L, o1 - o0)), ct, np.ascontiguousarray(w_eval[o0:o1]).reshape(-1),
                           None if prev is None else prev.ctypes.data_as(C.c_void_p),
                           np.ascontiguousarray(s_b[o0:o1]).reshape(-1), co, bs)
         ct_out[o0:o1] = co.reshape(o1 - o0, -1)
-        bob_sh[o0:o1] = bs.reshape(o1 - o0, -1)
+        bob_sh[:, o0:o1] = bs.reshape(pk, o1 - o0, -1)
     _pmap(job, _ranges(L.cout, workers), workers)
     return ct_out.reshape(-1), bob_sh.reshape(-1)
 
 
 def alice_decrypt(L, t_eval, ct_out, workers=1):
-    n, B = L.n, L.blocks
+    n, B, pk = L.n, L.blocks, _pk(L)
     ct_out = np.ascontiguousarray(ct_out, np.uint64).reshape(L.cout, -1)
-    al = np.zeros((L.cout, L.oh * L.ow), np.uint64)
+    al = np.zeros((pk, L.cout, L.oh * L.ow), np.uint64)
 
     def job(r):
         o0, o1 = r
-        a_ = np.zeros((o1 - o0) * L.oh * L.ow, np.uint64)
+        a_ = np.zeros(pk * (o1 - o0) * L.oh * L.ow, np.uint64)
         lib().eo_alice_decrypt(C.byref(_sub(L, o1 - o0)), t_eval, np.ascontiguousarray(ct_out[o0:o1]).reshape(-1), a_)
-        al[o0:o1] = a_.reshape(o1 - o0, -1)
+        al[:, o0:o1] = a_.reshape(pk, o1 - o0, -1)
     _pmap(job, _ranges(L.cout, workers), workers)
     return al.reshape(-1)
 
@@ -222,7 +227,10 @@ def run_layer(L, t_eval, alice_in, bob_prev, w_eval, e, a, s_b, want=(), workers
                         np.ascontiguousarray(a, np.uint64).reshape(-1), ct)
     ct_out, bob_sh = bob_eval(L, ct, w_eval, bob_prev, s_b, workers)
     al_sh = alice_decrypt(L, t_eval, ct_out, workers)
-    r = {"alice": al_sh.reshape(L.cout, L.oh, L.ow), "bob": bob_sh.reshape(L.cout, L.oh, L.ow)}
+    if _pk(L) > 1:  # packed: [pack][cout][oh][ow]
+        r = {"alice": al_sh.reshape(_pk(L), L.cout, L.oh, L.ow), "bob": bob_sh.reshape(_pk(L), L.cout, L.oh, L.ow)}
+    else:
+        r = {"alice": al_sh.reshape(L.cout, L.oh, L.ow), "bob": bob_sh.reshape(L.cout, L.oh, L.ow)}
     if "ct" in want:
         r["ct_in"] = ct.reshape(L.cin, B, 2, n)
         r["ct_out"] = ct_out.reshape(L.cout, B, 2, n)
@@ -325,11 +333,12 @@ def rns_delta(qs, p):
     return [((Q - 1) // p) % q for q in qs]
 
 
-def rns_layers(qs, p, n, H, W, fh, fw, same, cin, cout):
+def rns_layers(qs, p, n, H, W, fh, fw, same, cin, cout, pack=1):
     Ls = []
     for q, d in zip(qs, rns_delta(qs, p)):
         L = layer(q, p, n, H, W, fh, fw, same, cin, cout)
         L.delta = d
+        L.pack = pack
         Ls.append(L)
     return Ls
 
@@ -373,7 +382,8 @@ def run_layer_rns(Ls, t_evals, alice_in, w_evals, e, a, s_b, workers=1):
         cts[r] = ct
         ct_in[:, :, :, r] = ct.reshape(L0.cin, B, 2, n)
     _pmap(enc, range(R), workers)
-    bob = np.zeros((L0.cout, L0.oh * L0.ow), np.uint64)
+    pk = _pk(L0)
+    bob = np.zeros((pk, L0.cout, L0.oh * L0.ow), np.uint64)
     s_b = np.ascontiguousarray(s_b, np.uint64).reshape(L0.cout, -1)
     jobs = [(r, rg) for r in range(R) for rg in _ranges(L0.cout, max(1, workers // R))]
 
@@ -381,22 +391,22 @@ def run_layer_rns(Ls, t_evals, alice_in, w_evals, e, a, s_b, workers=1):
         r, (o0, o1) = job
         w = np.ascontiguousarray(w_evals[r], np.uint64).reshape(L0.cout, -1)
         co = np.zeros((o1 - o0) * B * 2 * n, np.uint64)
-        bs = np.zeros((o1 - o0) * L0.oh * L0.ow, np.uint64)
+        bs = np.zeros(pk * (o1 - o0) * L0.oh * L0.ow, np.uint64)
         lib().eo_bob_eval(C.byref(_sub(Ls[r], o1 - o0)), cts[r], np.ascontiguousarray(w[o0:o1]).reshape(-1), None,
                           np.ascontiguousarray(s_b[o0:o1]).reshape(-1), co, bs)
         ct_out[o0:o1, :, :, r] = co.reshape(o1 - o0, B, 2, n)
         if r == 0:
-            bob[o0:o1] = bs.reshape(o1 - o0, -1)
+            bob[:, o0:o1] = bs.reshape(pk, o1 - o0, -1)
     _pmap(mac, jobs, workers)
-    al = np.zeros((L0.cout, L0.oh * L0.ow), np.uint64)
+    al = np.zeros((pk, L0.cout, L0.oh * L0.ow), np.uint64)
     te = np.ascontiguousarray(np.stack(t_evals), np.uint64).reshape(-1)
 
     def dec(rg):
         o0, o1 = rg
         arr = (Layer * R)(*[_sub(L, o1 - o0) for L in Ls])
-        a_ = np.zeros((o1 - o0) * L0.oh * L0.ow, np.uint64)
+        a_ = np.zeros(pk * (o1 - o0) * L0.oh * L0.ow, np.uint64)
         lib().eo_alice_decrypt_rns(C.cast(arr, C.c_void_p), R, te, np.ascontiguousarray(ct_out[o0:o1]).reshape(-1), a_)
-        al[o0:o1] = a_.reshape(o1 - o0, -1)
+        al[:, o0:o1] = a_.reshape(pk, o1 - o0, -1)
     _pmap(dec, _ranges(L0.cout, workers), workers)
-    return {"alice": al.reshape(L0.cout, L0.oh, L0.ow), "bob": bob.reshape(L0.cout, L0.oh, L0.ow), "ct_in": ct_in,
-            "ct_out": ct_out}
+    shape = (pk, L0.cout, L0.oh, L0.ow) if pk > 1 else (L0.cout, L0.oh, L0.ow)
+    return {"alice": al.reshape(shape), "bob": bob.reshape(shape), "ct_in": ct_in, "ct_out": ct_out}

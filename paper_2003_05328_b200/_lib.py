@@ -46,12 +46,12 @@ class CtxInfo(C.Structure):
 
 class ConvDesc(C.Structure):
     _fields_ = [("H", C.c_uint32), ("W", C.c_uint32), ("fh", C.c_uint32), ("fw", C.c_uint32),
-                ("same", C.c_uint32), ("cin", C.c_uint32), ("cout", C.c_uint32)]
+                ("same", C.c_uint32), ("cin", C.c_uint32), ("cout", C.c_uint32), ("pack", C.c_uint32)]
 
 
 class LayerGeom(C.Structure):
     _fields_ = [("Lh", C.c_uint32), ("Lw", C.c_uint32), ("blocks", C.c_uint32), ("oh", C.c_uint32),
-                ("ow", C.c_uint32), ("r0", C.c_uint32), ("c0", C.c_uint32)]
+                ("ow", C.c_uint32), ("r0", C.c_uint32), ("c0", C.c_uint32), ("pack", C.c_uint32)]
 
 
 class Randomness(C.Structure):

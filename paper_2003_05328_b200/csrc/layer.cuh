@@ -37,6 +37,8 @@ struct LayerArgs {
   int H, W, fh, fw, cin, cout;
   int Lh, Lw, B, oh, ow, r0, c0, G;
   int num_images;
+  int pk;       // images per ciphertext block (1: REF geometry)
+  int num_cts;  // ciphertext "images" = ceil(num_images / pk): the rows of the ElementMult / 2
   // ring
   PrimeConst pc[ENSEI_MAX_PRIMES];
   uint64_t psi_q[ENSEI_MAX_PRIMES];  // canonical 2n-th roots (direct-evaluation fallback)
@@ -58,23 +60,36 @@ struct LayerArgs {
 
 // ---------------------------------------------------------------- helpers
 
-// slot value at ring position j of block b read from a DFT2D tile stored
-// bit-reversed in both dimensions (S[brev(r)][brev(c)] = G[r][c]); 0 past the grid
-template <int LOGN, int LOGH, int LOGW>
-EG_DEV uint32_t gather_slot(const uint32_t* S, int b, int j, int G) {
+// Packing: a ciphertext block carries `pk` images' grids back to back (slots
+// [pi G, (pi + 1) G) hold image pi of the pack; pk = 1 is REF's geometry, one image per
+// block with the tail zero-filled, REF protocol.cpp:18-29).  The pk DFT2D tiles live at
+// S + pi * TS (TS words apart), each bit-reversed in both dimensions
+// (S[brev(r)][brev(c)] = G[r][c]).
+// slot value at ring position j of block b; 0 past the packed grids.  TILE0: every pack
+// position reads tile 0 (prepared weights, replicated across the pack)
+template <int LOGN, int LOGH, int LOGW, bool TILE0 = false>
+EG_DEV uint32_t gather_slot(const uint32_t* S, int b, int j, int pk, int TS) {
   const int flat = (b << LOGN) + brev(j, LOGN);
-  if (flat >= G) return 0;
-  const int r = flat >> LOGW, c = flat & ((1 << LOGW) - 1);
-  return S[brev(r, LOGH) * ((1 << LOGW) + 1) + brev(c, LOGW)];
+  const int pi = flat >> (LOGH + LOGW);
+  if (pi >= pk) return 0;
+  const int r = (flat >> LOGW) & ((1 << LOGH) - 1), c = flat & ((1 << LOGW) - 1);
+  return S[(TILE0 ? 0 : pi) * TS + brev(r, LOGH) * ((1 << LOGW) + 1) + brev(c, LOGW)];
 }
 
-// scatter of a decoded slot (ring position j of block b) into the bit-reversed tile
+// scatter of a decoded slot (ring position j of block b) into its bit-reversed tile
 template <int LOGN, int LOGH, int LOGW>
-EG_DEV void scatter_slot(uint32_t* S, int b, int j, int G, uint32_t v) {
+EG_DEV void scatter_slot(uint32_t* S, int b, int j, int pk, int TS, uint32_t v) {
   const int flat = (b << LOGN) + brev(j, LOGN);
-  if (flat >= G) return;
-  const int r = flat >> LOGW, c = flat & ((1 << LOGW) - 1);
-  S[brev(r, LOGH) * ((1 << LOGW) + 1) + brev(c, LOGW)] = v;
+  const int pi = flat >> (LOGH + LOGW);
+  if (pi >= pk) return;
+  const int r = (flat >> LOGW) & ((1 << LOGH) - 1), c = flat & ((1 << LOGW) - 1);
+  S[pi * TS + brev(r, LOGH) * ((1 << LOGW) + 1) + brev(c, LOGW)] = v;
+}
+
+// words per tile slot of the tile region (128-byte aligned)
+template <int LOGH, int LOGW>
+__host__ __device__ constexpr int tile_words() {
+  return (int)((((size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4 + 127) & ~(size_t)127) / 4);
 }
 
 // Delta_r * m mod q_r for m < p (R == 1: exact product, Delta*(p-1) < q)
@@ -209,8 +224,8 @@ EG_DEV TwStage tw_stage_issue(uint8_t* dst, uint64_t* bar, const TwPair<uint64_t
 // ALIAS (the fully staged single-prime variant): the p-side ring buffer lives inside
 // the q-side one -- the q transform's first pass loads all of it before its first store.
 template <int LOGN, int LOGH, int LOGW, int G, bool ALIAS = false>
-constexpr size_t tile_enc_smem() {
-  return (((size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4 + 127) & ~(size_t)127) +
+constexpr size_t tile_enc_smem(int pk = 1) {
+  return (size_t)pk * tile_words<LOGH, LOGW>() * 4 +
          G * ((((size_t)(1 << LOGN) * 8 + (ALIAS ? 0 : ssize<uint32_t>(1 << LOGN) * 4) + (1 << LOGN)) + 127) &
               ~(size_t)127);
 }
@@ -226,9 +241,11 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
   static_assert(!ALIAS || R == 1, "aliased p buffer: one q transform per block");
   constexpr size_t GROUP_BYTES = (size_t)N * 8 + (ALIAS ? 0 : ssize<uint32_t>(N) * 4) + N;
   extern __shared__ __align__(128) uint8_t smem_raw[];
+  constexpr int TS = tile_words<LOGH, LOGW>();
+  const int npk = TM == TILE_WEIGHTS ? 1 : a.pk;  // tiles loaded (weights: one, replicated by gather_slot)
   uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);
   const int g = threadIdx.x / NT, tid = threadIdx.x % NT;
-  uint8_t* gbase = smem_raw + (((size_t)Lh * LS * 4 + 127) & ~(size_t)127) + g * ((GROUP_BYTES + 127) & ~(size_t)127);
+  uint8_t* gbase = smem_raw + (size_t)npk * TS * 4 + g * ((GROUP_BYTES + 127) & ~(size_t)127);
   uint64_t* qbuf = reinterpret_cast<uint64_t*>(gbase);
   uint32_t* pbuf = ALIAS ? reinterpret_cast<uint32_t*>(qbuf) : reinterpret_cast<uint32_t*>(qbuf + N);
   int8_t* ebuf = ALIAS ? reinterpret_cast<int8_t*>(qbuf + N) : reinterpret_cast<int8_t*>(pbuf + ssize<uint32_t>(N));
@@ -238,21 +255,23 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
 
   const int item = blockIdx.x;
   const int ch = item % a.cin;
-  const int img = item / a.cin;  // image (or output channel for WEIGHTS)
+  const int img = item / a.cin;  // ciphertext image (pk images from img * pk), or output channel for WEIGHTS
   const int th = TM == TILE_WEIGHTS ? a.fh : a.H, tw = TM == TILE_WEIGHTS ? a.fw : a.W;
   pdl_trigger();  // the ElementMult may launch now; its pdl_wait() covers this grid's writes
   __shared__ uint64_t tw_bar;
   TwStage tws{a.twq_fwd[0], a.twp_inv, a.twc_fwd};
   if constexpr (TWS)
-    tws = tw_stage_issue<LOGN, TWS>(smem_raw + tile_enc_smem<LOGN, LOGH, LOGW, G, ALIAS>(), &tw_bar, a.twq_fwd[0], a.twp_inv,
-                               a.twc_fwd);
+    tws = tw_stage_issue<LOGN, TWS>(smem_raw + tile_enc_smem<LOGN, LOGH, LOGW, G, ALIAS>(npk), &tw_bar, a.twq_fwd[0],
+                                    a.twp_inv, a.twc_fwd);
 
-  // 1. pad into the tile (REF pad_image / pad_residues, ntt.cpp:155-185)
-  for (int i = threadIdx.x; i < Lh * Lw; i += blockDim.x) {
+  // 1. pad into the tiles (REF pad_image / pad_residues, ntt.cpp:155-185), pk images
+  for (int e = threadIdx.x; e < npk * Lh * Lw; e += blockDim.x) {
+    const int pi = e >> (LOGH + LOGW), i = e & (Lh * Lw - 1);
     const int r = i >> LOGW, c = i & (Lw - 1);
+    const int src_item = TM == TILE_WEIGHTS ? item : (img * npk + pi) * a.cin + ch;
     uint32_t v = 0;
-    if (r < th && c < tw) {
-      const size_t src = ((size_t)item * th + r) * tw + c;
+    if (r < th && c < tw && (TM == TILE_WEIGHTS || img * npk + pi < a.num_images)) {
+      const size_t src = ((size_t)src_item * th + r) * tw + c;
       if constexpr (TM == TILE_WEIGHTS) {
         const int32_t w = static_cast<const int32_t*>(in)[src];
         int64_t m = (int64_t)w % (int64_t)p;
@@ -263,15 +282,15 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
         v = static_cast<const uint32_t*>(in)[src] % p;
       }
     }
-    S[r * LS + c] = v;
+    S[pi * TS + r * LS + c] = v;
   }
   __syncthreads();
   if constexpr (TWS) mbar_wait(&tw_bar, 0);
-  // 2. DFT2D (rows then columns; output bit-reversed in both dims)
-  tile_transform_2d<false, LOGH, LOGW>(pf, a.pp.cred, tws.c, S, LS);
+  // 2. DFT2D of each tile (rows then columns; output bit-reversed in both dims)
+  for (int pi = 0; pi < npk; ++pi) tile_transform_2d<false, LOGH, LOGW>(pf, a.pp.cred, tws.c, S + pi * TS, LS);
 
   const uint64_t* kimg = key + (size_t)(TM == TILE_ENC ? img : 0) * key_stride;
-  const int gimg = a.image_base + img;
+  const int gimg = a.image_base / a.pk + img;  // stream id of the ciphertext (= the image when pk = 1)
   for (int b = g; b < a.B; b += G) {
     if constexpr (TM == TILE_ENC) {  // Enc noise e0 for this block, two CBD draws per call
       const size_t nb = (((size_t)img * a.cin + ch) * a.B + b) * N;
@@ -292,7 +311,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
     }
     // 3. encode_slots: INTT_p of the block's slots (gathered from the tile)
     {
-      auto src = [&](int j) { return gather_slot<LOGN, LOGH, LOGW>(S, b, j, a.G); };
+      auto src = [&](int j) { return gather_slot<LOGN, LOGH, LOGW, TM == TILE_WEIGHTS>(S, b, j, a.pk, TS); };
       SmemRW<uint32_t> dst_raw{pbuf};
       auto dst = [&](int i, uint32_t v) { dst_raw(i, Bfly<Field32, 0>::fin_gs(pf, v)); };
       ntt_inverse<Field32, uint32_t, LOGN, tile_loge(LOGN), 0, false, false>(pf, tws.p, pbuf, tid, src, dst, bar);
@@ -363,7 +382,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
 // layout) and Bob's share = crop(IDFT2D(merge(s_B))).
 template <int LOGN, int LOGH, int LOGW, int G, bool ALIAS = false>
 constexpr size_t share_smem(int B) {
-  return (((size_t)(1 << LOGH) * ((1 << LOGW) + 1) + 31) & ~(size_t)31) * 4 + (size_t)B * (1 << LOGN) * 4 +
+  return (size_t)tile_words<LOGH, LOGW>() * 4 + (size_t)B * (1 << LOGN) * 4 +
          G * ((((size_t)(1 << LOGN) * 8 + (ALIAS ? 0 : ssize<uint32_t>(1 << LOGN) * 4)) + 127) & ~(size_t)127);
 }
 
@@ -377,7 +396,7 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
   constexpr size_t GROUP_BYTES = (size_t)N * 8 + (ALIAS ? 0 : ssize<uint32_t>(N) * 4);
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);
-  uint32_t* sbuf = S + (((size_t)Lh * LS + 31) & ~(size_t)31);  // [B][N] shares
+  uint32_t* sbuf = S + tile_words<LOGH, LOGW>();  // [B][N] shares
   const int g = threadIdx.x / NT, tid = threadIdx.x % NT;
   uint8_t* gbase = reinterpret_cast<uint8_t*>(sbuf + (size_t)a.B * N) + g * ((GROUP_BYTES + 127) & ~(size_t)127);
   uint64_t* qbuf = reinterpret_cast<uint64_t*>(gbase);
@@ -385,9 +404,9 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
   const GroupBar bar{g, NT};
   const Field32 pf = a.pp.f;
   const uint32_t p = pf.q;
-  const int item = blockIdx.x;  // img * cout + o
+  const int item = blockIdx.x;  // ciphertext image * cout + o
   const int o = item % a.cout, img = item / a.cout;
-  const int gimg = a.image_base + img;
+  const int gimg = a.image_base / a.pk + img;
   __shared__ uint64_t tw_bar;
   TwStage tws{a.twq_fwd[0], a.twp_inv, a.twc_inv};
   if constexpr (TWS)  // tables after the working buffers
@@ -434,18 +453,21 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)), tile_min_b
       bar.sync();
     }
   }
-  __syncthreads();
-  // 2. Bob's share: IDFT2D of the merged s_B grid, cropped (REF protocol.cpp:593-602)
-  for (int i = threadIdx.x; i < Lh * Lw; i += blockDim.x) {
-    const int r = i >> LOGW, c = i & (Lw - 1);
-    S[brev(r, LOGH) * LS + brev(c, LOGW)] = sbuf[i];  // natural grid position i = r*Lw + c
-  }
-  __syncthreads();
-  tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, tws.c, S, LS);
-  uint32_t* bs = bob_share + (size_t)item * a.oh * a.ow;
-  for (int i = threadIdx.x; i < a.oh * a.ow; i += blockDim.x) {
-    const int r = i / a.ow, c = i % a.ow;
-    bs[i] = S[(r + a.r0) * LS + c + a.c0];
+  // 2. Bob's share of every image of the pack: IDFT2D of its part of the merged s_B grid,
+  // cropped (REF protocol.cpp:593-602)
+  for (int pi = 0; pi < a.pk && img * a.pk + pi < a.num_images; ++pi) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < Lh * Lw; i += blockDim.x) {
+      const int r = i >> LOGW, c = i & (Lw - 1);
+      S[brev(r, LOGH) * LS + brev(c, LOGW)] = sbuf[pi * Lh * Lw + i];  // natural grid position i = r*Lw + c
+    }
+    __syncthreads();
+    tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, tws.c, S, LS);
+    uint32_t* bs = bob_share + ((size_t)(img * a.pk + pi) * a.cout + o) * a.oh * a.ow;
+    for (int i = threadIdx.x; i < a.oh * a.ow; i += blockDim.x) {
+      const int r = i / a.ow, c = i % a.ow;
+      bs[i] = S[(r + a.r0) * LS + c + a.c0];
+    }
   }
 }
 
@@ -559,10 +581,11 @@ __global__ void __launch_bounds__((1 << LOGN) >> tile_loge(LOGN))
   constexpr int N = 1 << LOGN, NT = N >> tile_loge(LOGN);
   constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
   extern __shared__ __align__(128) uint8_t smem_raw[];
+  constexpr int TS = tile_words<LOGH, LOGW>();
   uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* fsum = qbuf + N;                                  // sum_r E_r / q_r, 2^-62
   uint32_t* pbuf = reinterpret_cast<uint32_t*>(fsum + N);     // sum_r I_r, then m
-  uint32_t* S = pbuf + ssize<uint32_t>(N);
+  uint32_t* S = pbuf + ssize<uint32_t>(N);                    // pk tiles, TS words apart
   const int tid = threadIdx.x;
   const CtaBar bar;
   const Field32 pf = a.pp.f;
@@ -570,7 +593,7 @@ __global__ void __launch_bounds__((1 << LOGN) >> tile_loge(LOGN))
   const int item = blockIdx.x;
   const int img = item / a.cout;
   const uint64_t* kimg = key + (size_t)img * key_stride;
-  for (int i = tid; i < Lh * LS; i += NT) S[i] = 0;
+  for (int i = tid; i < a.pk * TS; i += NT) S[i] = 0;
   for (int b = 0; b < a.B; ++b) {
     const uint64_t* cb = ct + ((size_t)item * a.B + b) * ct_words<R>(N);
     for (int i = tid; i < N; i += NT) {
@@ -616,26 +639,32 @@ __global__ void __launch_bounds__((1 << LOGN) >> tile_loge(LOGN))
     }
     __syncthreads();
     SmemRW<uint32_t> psrc{pbuf};
-    auto pdst = [&](int j, uint32_t v) { scatter_slot<LOGN, LOGH, LOGW>(S, b, j, a.G, reduce_lazy(pf, v, a.pp.cred)); };
+    auto pdst = [&](int j, uint32_t v) {
+      scatter_slot<LOGN, LOGH, LOGW>(S, b, j, a.pk, TS, reduce_lazy(pf, v, a.pp.cred));
+    };
     ntt_forward<Field32, uint32_t, LOGN, tile_loge(LOGN), 0, false, false>(pf, a.twp_fwd, pbuf, tid, psrc, pdst, bar);
     __syncthreads();
   }
-  tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, S, LS);
-  const size_t base = (size_t)item * a.oh * a.ow;
-  for (int i = tid; i < a.oh * a.ow; i += NT) {
-    const int r = i / a.ow, c = i % a.ow;
-    const uint32_t s = S[(r + a.r0) * LS + c + a.c0];
-    if (alice_share) alice_share[base + i] = s;
-    if (outp) {
-      uint32_t y = s + bob_share[base + i];
-      outp[base + i] = y >= p ? y - p : y;
+  const int o = item % a.cout;
+  for (int pi = 0; pi < a.pk && img * a.pk + pi < a.num_images; ++pi) {  // every image of the pack
+    uint32_t* St = S + pi * TS;
+    tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, St, LS);
+    const size_t base = ((size_t)(img * a.pk + pi) * a.cout + o) * a.oh * a.ow;
+    for (int i = tid; i < a.oh * a.ow; i += NT) {
+      const int r = i / a.ow, c = i % a.ow;
+      const uint32_t s = St[(r + a.r0) * LS + c + a.c0];
+      if (alice_share) alice_share[base + i] = s;
+      if (outp) {
+        uint32_t y = s + bob_share[base + i];
+        outp[base + i] = y >= p ? y - p : y;
+      }
     }
   }
 }
 
 template <int LOGN, int LOGH, int LOGW>
-constexpr size_t dec_rns_smem() {
-  return (size_t)(1 << LOGN) * 16 + ssize<uint32_t>(1 << LOGN) * 4 + (size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4;
+constexpr size_t dec_rns_smem(int pk = 1) {
+  return (size_t)(1 << LOGN) * 16 + ssize<uint32_t>(1 << LOGN) * 4 + (size_t)pk * tile_words<LOGH, LOGW>() * 4;
 }
 
 // Standalone exact CRT rounding (ensei_gpu_crt_round, for the boundary tests): residues
@@ -669,8 +698,8 @@ __global__ void crt_round_kernel(LayerArgs a, const uint64_t* __restrict__ res, 
 // INTT_q -> round(p phi / q) -> decode (NTT_p) -> scatter into the tile; then all
 // threads: IDFT2D -> crop (-> + Bob's share).
 template <int LOGN, int LOGH, int LOGW, int G>
-constexpr size_t dec_smem() {
-  return (((size_t)(1 << LOGH) * ((1 << LOGW) + 1) * 4 + 127) & ~(size_t)127) +
+constexpr size_t dec_smem(int pk = 1) {
+  return (size_t)pk * tile_words<LOGH, LOGW>() * 4 +
          G * ((((size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4) + 127) & ~(size_t)127);
 }
 
@@ -685,33 +714,34 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)))
   constexpr int N = 1 << LOGN, NT = N >> tile_loge(LOGN);
   constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
   constexpr size_t GROUP_BYTES = (size_t)N * 8 + ssize<uint32_t>(N) * 4;
+  constexpr int TS = tile_words<LOGH, LOGW>();
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);  // pk tiles, TS words apart
   const int g = threadIdx.x / NT, tid = threadIdx.x % NT;
-  uint8_t* gbase = smem_raw + (((size_t)Lh * LS * 4 + 127) & ~(size_t)127) + g * ((GROUP_BYTES + 127) & ~(size_t)127);
+  uint8_t* gbase = smem_raw + (size_t)a.pk * TS * 4 + g * ((GROUP_BYTES + 127) & ~(size_t)127);
   uint64_t* qbuf = reinterpret_cast<uint64_t*>(gbase);
   uint32_t* pbuf = reinterpret_cast<uint32_t*>(qbuf + N);
   const GroupBar bar{g, NT};
   const Field32 pf = a.pp.f;
   const uint32_t p = pf.q;
-  const int item = blockIdx.x;  // img * cout + o
-  const int img = item / a.cout;
+  const int item = blockIdx.x;  // ciphertext image * cout + o
+  const int img = item / a.cout, o = item % a.cout;
   const uint64_t* kimg = key + (size_t)img * key_stride;
   const PrimeConst pc = a.pc[0];
   const Field64 f = pc.f;
   const uint64_t cp = pc.cp, h = f.q >> 1;  // floor(p 2^64 / q), floor(q / 2)
-  uint64_t* kst = reinterpret_cast<uint64_t*>(smem_raw + dec_smem<LOGN, LOGH, LOGW, G>());  // [t^][t^'][B][c0][c1]
+  uint64_t* kst = reinterpret_cast<uint64_t*>(smem_raw + dec_smem<LOGN, LOGH, LOGW, G>(a.pk));  // [t^][t^'][B][c0][c1]
   __shared__ uint64_t tw_bar;
   // Bob's share for the final recombination, fetched now: HomShare finished before the
   // ElementMult started, so it is visible here, and the load latency hides behind the
-  // transforms instead of stalling the crop loop
+  // transforms instead of stalling the crop loop (unpacked layers)
   constexpr int kBobPre = 4;
   const size_t obase = (size_t)item * a.oh * a.ow;
   uint32_t bob_pre[kBobPre];
 #pragma unroll
   for (int k = 0; k < kBobPre; ++k) {
     const int i = threadIdx.x + k * blockDim.x;
-    bob_pre[k] = (outp && i < a.oh * a.ow) ? __ldg(bob_share + obase + i) : 0u;
+    bob_pre[k] = (outp && a.pk == 1 && i < a.oh * a.ow) ? __ldg(bob_share + obase + i) : 0u;
   }
   TwStage tws{a.twq_inv[0], a.twp_fwd, a.twc_inv};
   if constexpr (TWS)  // tables after the staged arrays
@@ -764,11 +794,30 @@ __global__ void __launch_bounds__(G*((1 << LOGN) >> tile_loge(LOGN)))
     bar.sync();
     // decode_slots (NTT_p) -> scatter into the bit-reversed tile
     SmemRW<uint32_t> psrc{pbuf};
-    auto pdst = [&](int j, uint32_t v) { scatter_slot<LOGN, LOGH, LOGW>(S, b, j, a.G, reduce_lazy(pf, v, a.pp.cred)); };
+    auto pdst = [&](int j, uint32_t v) {
+      scatter_slot<LOGN, LOGH, LOGW>(S, b, j, a.pk, TS, reduce_lazy(pf, v, a.pp.cred));
+    };
     ntt_forward<Field32, uint32_t, LOGN, tile_loge(LOGN), 0, false, false>(pf, tws.p, pbuf, tid, psrc, pdst, bar);
     bar.sync();
   }
   __syncthreads();
+  if (a.pk > 1) {  // packed: IDFT2D + crop (+ recombine) of every image of the pack
+    for (int pi = 0; pi < a.pk && img * a.pk + pi < a.num_images; ++pi) {
+      uint32_t* St = S + pi * TS;
+      tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, tws.c, St, LS);
+      const size_t base = ((size_t)(img * a.pk + pi) * a.cout + o) * a.oh * a.ow;
+      for (int i = threadIdx.x; i < a.oh * a.ow; i += blockDim.x) {
+        const int r = i / a.ow, c = i % a.ow;
+        const uint32_t s = St[(r + a.r0) * LS + c + a.c0];
+        if (alice_share) alice_share[base + i] = s;
+        if (outp) {
+          uint32_t y = s + bob_share[base + i];
+          outp[base + i] = y >= p ? y - p : y;
+        }
+      }
+    }
+    return;
+  }
   // IDFT2D + crop (+ recombine with Bob's share)
   tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, tws.c, S, LS);
   int k = 0;

@@ -57,6 +57,8 @@ int guarded(Fn&& fn) {
 
 struct Geo {
   uint32_t Lh, Lw, logL, B, oh, ow, r0, c0, G;
+  uint32_t pk = 1;  // images per ciphertext block
+  uint32_t cts(uint32_t imgs) const { return (imgs + pk - 1) / pk; }
 };
 
 int ilog2u(uint32_t v) {
@@ -86,6 +88,13 @@ Geo geometry(const ensei_gpu_ctx* c, const ensei_conv_desc* d) {
   g.logL = ilog2u(g.Lh);
   g.G = g.Lh * g.Lw;
   g.B = (g.G + c->n - 1) / c->n;
+  // packing (builder extension, ensei_conv_desc::pack): pk images' grids per block
+  g.pk = d->pack > 1 ? d->pack : 1;
+  if (g.pk > 1) {
+    require(g.B == 1 && (uint64_t)g.pk * g.G <= c->n, ENSEI_ERR_BAD_GEOMETRY,
+            "packing needs pack * padded grid <= n (one block per channel)");
+    require((g.pk & (g.pk - 1)) == 0, ENSEI_ERR_UNSUPPORTED, "pack must be a power of two");
+  }
   g.oh = d->same ? d->H : d->H - d->fh + 1;
   g.ow = d->same ? d->W : d->W - d->fw + 1;
   g.r0 = d->same ? (d->fh - 1) / 2 : d->fh - 1;
@@ -120,6 +129,8 @@ LayerRun make_run(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g
   a.c0 = g.c0;
   a.G = g.G;
   a.num_images = num_images;
+  a.pk = (int)g.pk;
+  a.num_cts = (int)g.cts(num_images);
   for (uint32_t i = 0; i < c->R; ++i) {
     a.pc[i] = c->pc[i];
     a.psi_q[i] = c->psi_q[i];
@@ -135,6 +146,8 @@ LayerRun make_run(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g
   if (rand) {
     require(rand->mode == ENSEI_RAND_PHILOX || rand->mode == ENSEI_RAND_INJECTED, ENSEI_ERR_INVALID_ARGUMENT,
             "bad randomness mode");
+    require(g.pk == 1 || (rand->mode == ENSEI_RAND_PHILOX && rand->image_base % g.pk == 0), ENSEI_ERR_UNSUPPORTED,
+            "packed layers: Philox streams with a pack-aligned image_base");
     a.rand_mode = rand->mode;
     a.layer = rand->layer;
     a.image_base = rand->image_base;
@@ -150,6 +163,13 @@ LayerRun make_run(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g
 }
 
 bool injected(const ensei_randomness* r) { return r && r->mode == ENSEI_RAND_INJECTED; }
+
+// The ElementMult sees ciphertexts, not images: its rows are the ciphertext images
+LayerRun mac_run(const LayerRun& r) {
+  LayerRun m = r;
+  m.a.num_images = r.a.num_cts;
+  return m;
+}
 
 void tile(const LayerRun& r, int tm, bool inj, int in_t, const uint64_t* key, uint32_t ks, const void* in,
           uint64_t* out, int items) {
@@ -245,11 +265,12 @@ size_t mac_bytes(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g,
   a.cin = (int)d->cin;
   a.cout = (int)d->cout;
   a.B = (int)g.B;
-  a.num_images = (int)imgs;
+  a.num_images = (int)g.cts(imgs);  // the ElementMult's rows are ciphertexts
   return (mac_scratch_bytes(c, a) + 255) & ~(size_t)255;
 }
 
 size_t ct_bytes(const ensei_gpu_ctx* c, const Geo& g, uint32_t ch, uint32_t imgs) {
+  imgs = g.cts(imgs);  // ciphertexts hold pk images each
   return (size_t)imgs * ch * g.B * 2 * c->R * c->n * sizeof(uint64_t);
 }
 size_t share_bytes(const Geo& g, uint32_t cout, uint32_t imgs) {
@@ -285,9 +306,10 @@ Workspace carve(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g, 
 // of 64 images -- one 128-row ElementMult tile -- once that many fit).  Larger batches
 // stream through it chunk by chunk (config 4: 1024 images in 8 chunks of 128).
 uint32_t chunk_images(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g, uint32_t imgs) {
-  const size_t per = ct_bytes(c, g, d->cin, 1) + ct_bytes(c, g, d->cout, 1);
+  const size_t per = ct_bytes(c, g, d->cin, 1) + ct_bytes(c, g, d->cout, 1);  // one ciphertext image
   uint64_t k = std::max<uint64_t>(1, ((size_t)12 << 30) / per);
   if (k >= 64) k = k / 64 * 64;
+  k *= g.pk;  // images (a multiple of pk: stream ids stay pack-aligned across sub-batches)
   return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(k, imgs));
 }
 
@@ -314,18 +336,24 @@ void layer_chain(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const Geo& g, 
   uint32_t* bs = bob_share ? bob_share : w.bob;
   const bool inj = injected(rand);
   // Bob's HomShare masks depend only on his randomness: fork them onto the aux stream
-  // so they overlap Alice's encryption; join before the ElementMult consumes them.
-  EG_CUDA(cudaEventRecord(fork, st));
-  EG_CUDA(cudaStreamWaitEvent(aux, fork, 0));
+  // so they overlap Alice's encryption; join before the ElementMult consumes them.  In a
+  // per-kernel timing pass (ensei_gpu_profile) they run in line, so that every kernel's
+  // event span is its own.
+  const bool fork_share = !prof_on();
   LayerRun ra = r;
-  ra.st = aux;
-  share(ra, inj, w.ct_out, bs, (int)(imgs * desc->cout));
-  EG_CUDA(cudaEventRecord(join, aux));
-  tile(r, TILE_ENC, inj, in_dtype, key, ks, in, w.ct_in, (int)(imgs * desc->cin));
-  if (bob_prev) tile(r, TILE_HOMREC, false, ENSEI_IN_U32, key, 0, bob_prev, w.ct_in, (int)(imgs * desc->cin));
-  EG_CUDA(cudaStreamWaitEvent(st, join, 0));
-  mac(r, w.ct_in, w_eval, w.ct_out, w.mac);
-  dec(r, key, ks, w.ct_out, alice_share, bs, out, (int)(imgs * desc->cout));
+  if (fork_share) {
+    EG_CUDA(cudaEventRecord(fork, st));
+    EG_CUDA(cudaStreamWaitEvent(aux, fork, 0));
+    ra.st = aux;
+  }
+  const int cts = r.a.num_cts;  // ciphertext images (pk images each)
+  share(ra, inj, w.ct_out, bs, cts * (int)desc->cout);
+  if (fork_share) EG_CUDA(cudaEventRecord(join, aux));
+  tile(r, TILE_ENC, inj, in_dtype, key, ks, in, w.ct_in, cts * (int)desc->cin);
+  if (bob_prev) tile(r, TILE_HOMREC, false, ENSEI_IN_U32, key, 0, bob_prev, w.ct_in, cts * (int)desc->cin);
+  if (fork_share) EG_CUDA(cudaStreamWaitEvent(st, join, 0));
+  mac(mac_run(r), w.ct_in, w_eval, w.ct_out, w.mac);
+  dec(r, key, ks, w.ct_out, alice_share, bs, out, cts * (int)desc->cout);
 }
 
 // The whole batch through the chunk-sized workspace.  in_at(i0, cnt) gives the device
@@ -376,7 +404,7 @@ int ensei_gpu_layer_geometry(const ensei_gpu_ctx* ctx, const ensei_conv_desc* de
   return guarded([&] {
     require(geom != nullptr, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
     Geo g = geometry(ctx, desc);
-    *geom = {g.Lh, g.Lw, g.B, g.oh, g.ow, g.r0, g.c0};
+    *geom = {g.Lh, g.Lw, g.B, g.oh, g.ow, g.r0, g.c0, g.pk};
   });
 }
 
@@ -438,7 +466,8 @@ int ensei_gpu_alice_encrypt(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, con
     require(in_dtype == ENSEI_IN_U32 || in_dtype == ENSEI_IN_U8, ENSEI_ERR_INVALID_ARGUMENT, "bad input dtype");
     Geo g = geometry(ctx, desc);
     LayerRun r = make_run(ctx, desc, g, num_images, rand, stream);
-    tile(r, TILE_ENC, injected(rand), in_dtype, d_key, key_stride, d_in, d_ct, (int)(num_images * desc->cin));
+    require(g.pk == 1 || key_stride == 0, ENSEI_ERR_UNSUPPORTED, "packed layers share one key per ciphertext");
+    tile(r, TILE_ENC, injected(rand), in_dtype, d_key, key_stride, d_in, d_ct, r.a.num_cts * (int)desc->cin);
   });
 }
 
@@ -449,9 +478,9 @@ int ensei_gpu_bob_eval(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint64_t
     require(d_ct && d_w_eval && d_ct_out && d_bob_share, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
     Geo g = geometry(ctx, desc);
     LayerRun r = make_run(ctx, desc, g, num_images, rand, stream);
-    share(r, injected(rand), d_ct_out, d_bob_share, (int)(num_images * desc->cout));
-    if (d_bob_prev) tile(r, TILE_HOMREC, false, ENSEI_IN_U32, nullptr, 0, d_bob_prev, d_ct, (int)(num_images * desc->cin));
-    mac(r, d_ct, d_w_eval, d_ct_out);
+    share(r, injected(rand), d_ct_out, d_bob_share, r.a.num_cts * (int)desc->cout);
+    if (d_bob_prev) tile(r, TILE_HOMREC, false, ENSEI_IN_U32, nullptr, 0, d_bob_prev, d_ct, r.a.num_cts * (int)desc->cin);
+    mac(mac_run(r), d_ct, d_w_eval, d_ct_out);
   });
 }
 
@@ -461,7 +490,7 @@ int ensei_gpu_bob_share(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, uint32_
     require(d_ct_out && d_bob_share, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
     Geo g = geometry(ctx, desc);
     LayerRun r = make_run(ctx, desc, g, num_images, rand, stream);
-    share(r, injected(rand), d_ct_out, d_bob_share, (int)(num_images * desc->cout));
+    share(r, injected(rand), d_ct_out, d_bob_share, r.a.num_cts * (int)desc->cout);
   });
 }
 
@@ -471,7 +500,7 @@ int ensei_gpu_bob_mac(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const uin
     require(d_ct && d_w_eval && d_ct_out, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
     Geo g = geometry(ctx, desc);
     LayerRun r = make_run(ctx, desc, g, num_images, nullptr, stream);
-    mac(r, d_ct, d_w_eval, d_ct_out);
+    mac(mac_run(r), d_ct, d_w_eval, d_ct_out);
   });
 }
 
@@ -482,7 +511,8 @@ int ensei_gpu_alice_decrypt(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, con
     require(d_key && d_ct_out && d_alice_share, ENSEI_ERR_INVALID_ARGUMENT, "null argument");
     Geo g = geometry(ctx, desc);
     LayerRun r = make_run(ctx, desc, g, num_images, nullptr, stream);
-    dec(r, d_key, key_stride, d_ct_out, d_alice_share, nullptr, nullptr, (int)(num_images * desc->cout));
+    require(g.pk == 1 || key_stride == 0, ENSEI_ERR_UNSUPPORTED, "packed layers share one key per ciphertext");
+    dec(r, d_key, key_stride, d_ct_out, d_alice_share, nullptr, nullptr, r.a.num_cts * (int)desc->cout);
   });
 }
 
@@ -514,7 +544,7 @@ int ensei_gpu_mac_path(const ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, ui
     a.cin = (int)desc->cin;
     a.cout = (int)desc->cout;
     a.B = (int)g.B;
-    a.num_images = (int)num_images;
+    a.num_images = (int)g.cts(num_images);  // ElementMult rows: ciphertexts
     *path = mac_path(ctx, a);
   });
 }

@@ -58,7 +58,8 @@ template <int LOGN, int LOGL, int R, int TM, bool INJ, int IN_T, int G, int TWS>
 static void enc_go_t(const LayerRun& r, const uint64_t* key, uint32_t key_stride, const void* in, uint64_t* out,
                      int items) {
   auto k = tile_enc_kernel<LOGN, LOGL, LOGL, R, TM, INJ, IN_T, G, TWS>;
-  constexpr size_t smem = tile_enc_smem<LOGN, LOGL, LOGL, G, TWS == 2>() + tw_stage_bytes<LOGN, TWS>();
+  const size_t smem = tile_enc_smem<LOGN, LOGL, LOGL, G, TWS == 2>(TM == TILE_WEIGHTS ? 1 : r.a.pk) +
+                      tw_stage_bytes<LOGN, TWS>();
   set_smem_shared_sm(k, smem);
   k<<<items, G * ((1 << LOGN) >> tile_loge(LOGN)), smem, r.st>>>(r.a, key, key_stride, in, out);
   check_launch("tile_enc_kernel");
@@ -191,7 +192,7 @@ void launch_share(const LayerRun& r, bool inj, uint64_t* mask, uint32_t* bob_sha
 template <int LOGN, int LOGL, int G>
 static void dec_go_g(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint64_t* ct, uint32_t* alice,
                      const uint32_t* bob, uint32_t* out, int items) {
-  constexpr size_t base = dec_smem<LOGN, LOGL, LOGL, G>();
+  const size_t base = dec_smem<LOGN, LOGL, LOGL, G>(r.a.pk);
   const size_t staged = base + (size_t)(2 + 2 * r.a.B) * (1 << LOGN) * 8;  // + t^, t^', c0/c1 per block
   constexpr size_t twb = tw_stage_bytes<LOGN, 2>();
   // + staged twiddles (TWS): free when registers allow one CTA per SM anyway (G = 2)
@@ -224,7 +225,7 @@ template <int LOGN, int LOGL>
 static void dec_rns_go(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint64_t* ct, uint32_t* alice,
                        const uint32_t* bob, uint32_t* out, int items) {
   auto k = dec_rns_kernel<LOGN, LOGL, LOGL, 3>;
-  constexpr size_t smem = dec_rns_smem<LOGN, LOGL, LOGL>();
+  const size_t smem = dec_rns_smem<LOGN, LOGL, LOGL>(r.a.pk);
   set_smem(k, smem);
   k<<<items, (1 << LOGN) >> tile_loge(LOGN), smem, r.st>>>(r.a, key, ks, ct, alice, bob, out);
   check_launch("dec_rns_kernel");

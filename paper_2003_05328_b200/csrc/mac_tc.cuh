@@ -109,8 +109,13 @@ __global__ void __launch_bounds__(256) planes_tc_kernel(LayerArgs a, int logn, i
   pdl_wait();  // launched programmatically after Enc / HomRec: their ciphertexts
   pdl_trigger();
   for (long it = (long)blockIdx.x * 256 + threadIdx.x; it < total; it += (long)gridDim.x * 256) {
-    // lane-friendly decomposition: row%8, octet%2, row/8, octet/2, then tile, slot quad, chunk
+    // lane-friendly decomposition: slot-quad parity, row%8, octet%2 | row/8, octet/2, tile,
+    // slot-quad pair, chunk.  A store instruction covers two whole 128-byte core matrices,
+    // and the two lanes of a slot-quad pair read one contiguous 64-byte run per (row,
+    // channel) (32-byte reads cost a 64-byte DRAM access each: 2x read traffic, measured)
     long rest = it;
+    const int sq0 = (int)(rest & 1);
+    rest >>= 1;
     const int m8 = (int)(rest & 7);
     rest >>= 3;
     const int o2 = (int)(rest & 1);
@@ -121,8 +126,8 @@ __global__ void __launch_bounds__(256) planes_tc_kernel(LayerArgs a, int logn, i
     rest /= (octs / 2);
     const int tile = (int)(rest % ntiles);
     rest /= ntiles;
-    const long sq = rest % (S / 4);
-    const int kc = (int)(rest / (S / 4));
+    const long sq = (rest % (S / 8)) * 2 + sq0;
+    const int kc = (int)(rest / (S / 8));
     const int m = mg * 8 + m8, o = oh * 2 + o2;
     const int rc = tile * T + m;             // global row (or out channel)
     const long s0 = sq * 4;                  // first of 4 slots (same bp: n % 4 == 0)

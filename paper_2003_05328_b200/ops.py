@@ -116,9 +116,10 @@ class ConvSpec:
     same: bool
     cin: int
     cout: int
+    pack: int = 1  # images per ciphertext block (builder extension; 1 = REF geometry)
 
     def desc(self) -> ConvDesc:
-        return ConvDesc(self.H, self.W, self.fh, self.fw, int(self.same), self.cin, self.cout)
+        return ConvDesc(self.H, self.W, self.fh, self.fw, int(self.same), self.cin, self.cout, self.pack)
 
 
 def unpack_limbs(t: torch.Tensor) -> torch.Tensor:
@@ -170,10 +171,15 @@ class LayerOps:
         check(lib().ensei_gpu_layer_geometry(ctx.h, C.byref(self.d), C.byref(g)))
         self.geom = g
         self.B = g.blocks
+        self.pack = g.pack
+
+    def cts(self, images: int) -> int:
+        """Ciphertext images of a batch (pack images per ciphertext block)."""
+        return -(-images // self.pack)
 
     def empty_ct(self, images: int, channels: int) -> torch.Tensor:
         n, R = self.ctx.n, self.ctx.R
-        return torch.empty((images, channels, self.B, 2, R, n), dtype=torch.uint64, device=self.ctx.device)
+        return torch.empty((self.cts(images), channels, self.B, 2, R, n), dtype=torch.uint64, device=self.ctx.device)
 
     def prepared_words(self) -> int:
         """uint64 words of a prepared-weights buffer (ABI 2: packed words + tcgen05 planes)."""
@@ -212,8 +218,9 @@ class LayerOps:
                                             images, C.byref(r), _ptr(ct), _stream(stream)))
         return ct
 
-    def bob_eval(self, ct: torch.Tensor, w_eval: torch.Tensor, rand: Randomness, bob_prev=None, stream=None):
-        images = ct.shape[0]
+    def bob_eval(self, ct: torch.Tensor, w_eval: torch.Tensor, rand: Randomness, bob_prev=None, stream=None,
+                 images=None):
+        images = ct.shape[0] * self.pack if images is None else images
         g = self.geom
         ct_out = self.empty_ct(images, self.spec.cout)
         bob = torch.empty((images, self.spec.cout, g.oh, g.ow), dtype=torch.int32, device=ct.device)
@@ -233,12 +240,12 @@ class LayerOps:
         return ct_out, bob
 
     def bob_mac(self, ct, w_eval, ct_out, stream=None):
-        check(lib().ensei_gpu_bob_mac(self.ctx.h, C.byref(self.d), _ptr(ct), _ptr(w_eval), ct.shape[0],
+        check(lib().ensei_gpu_bob_mac(self.ctx.h, C.byref(self.d), _ptr(ct), _ptr(w_eval), ct.shape[0] * self.pack,
                                       _ptr(ct_out), _stream(stream)))
         return ct_out
 
-    def alice_decrypt(self, key, ct_out: torch.Tensor, key_stride: int = 0, stream=None):
-        images = ct_out.shape[0]
+    def alice_decrypt(self, key, ct_out: torch.Tensor, key_stride: int = 0, stream=None, images=None):
+        images = ct_out.shape[0] * self.pack if images is None else images
         g = self.geom
         a = torch.empty((images, self.spec.cout, g.oh, g.ow), dtype=torch.int32, device=ct_out.device)
         check(lib().ensei_gpu_alice_decrypt(self.ctx.h, C.byref(self.d), _ptr(key), key_stride, _ptr(ct_out), images,

@@ -31,6 +31,7 @@ class Conv:
     same: bool
     cin: int
     cout: int
+    pack: int = 1  # images per ciphertext block (builder extension; 0 = the most the ring holds)
 
 
 @dataclass
@@ -63,7 +64,12 @@ class Session:
         ci = 0
         for s in self.schedule:
             if isinstance(s, Conv):
-                lo = ops.LayerOps(ctx, ops.ConvSpec(h, w, s.fh, s.fw, s.same, s.cin, s.cout))
+                pk = s.pack
+                if pk == 0:  # the most images one ciphertext block holds (1 when the grid spans blocks)
+                    probe = ops.LayerOps(ctx, ops.ConvSpec(h, w, s.fh, s.fw, s.same, s.cin, s.cout))
+                    grid = probe.geom.Lh * probe.geom.Lw
+                    pk = max(1, ctx.n // grid) if probe.B == 1 else 1
+                lo = ops.LayerOps(ctx, ops.ConvSpec(h, w, s.fh, s.fw, s.same, s.cin, s.cout, pk))
                 wt = weights[ci].to(device=ctx.device, dtype=torch.int32).contiguous()
                 self.layers.append(lo)
                 self.w_eval.append(lo.prepare_weights(wt))
@@ -93,9 +99,10 @@ class Session:
             r = rand(li)
             if isinstance(s, Conv):
                 lo = self.layers[li]
+                images = alice.shape[0]
                 ct = lo.alice_encrypt(key, alice.contiguous(), r, key_stride=key_stride)
-                ct_out, bob_new = lo.bob_eval(ct, self.w_eval[li], r, bob_prev=bob)
-                alice = lo.alice_decrypt(key, ct_out, key_stride=key_stride)
+                ct_out, bob_new = lo.bob_eval(ct, self.w_eval[li], r, bob_prev=bob, images=images)
+                alice = lo.alice_decrypt(key, ct_out, key_stride=key_stride, images=images)
                 bob = bob_new
                 h, w = lo.geom.oh, lo.geom.ow
                 if keep_trace:

@@ -79,7 +79,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=2003)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ntt", action="store_true")
-    ap.add_argument("--no-side", action="store_true", help="config 4: skip the config-1 side line")
+    ap.add_argument("--no-side", action="store_true", help="config 4: skip the config-1 / unpacked side lines")
+    ap.add_argument("--pack", type=int, default=None,
+                    help="images per ciphertext block (config 4 default 2; 1 = REF geometry); config 3: 1 = unpacked")
     ap.add_argument("--no-graph", action="store_true", help="launch the layer eagerly instead of a CUDA graph")
     return ap.parse_args()
 
@@ -102,18 +104,22 @@ def idft2d(L):
     return dft2d(L) + L * L
 
 
-def layer_counts(n, R, L, B, cin, cout, H, W, oh, ow, imgs):
-    """Algorithmic modmul counts and HBM bytes per kernel per launch."""
+def layer_counts(n, R, L, B, cin, cout, H, W, oh, ow, imgs, pack=1):
+    """Algorithmic modmul counts and HBM bytes per kernel per launch for
+    `imgs` images; with packing, the ring work is per ciphertext image (pack images each),
+    the 2D transforms and pixel / share bytes per image."""
+    c = -(-imgs // pack)  # ciphertext images
     k = {}
-    k["enc"] = dict(q=imgs * cin * B * R * (2 * n + ntt_fwd(n)), mac=0, p=imgs * cin * (dft2d(L) + B * ntt_inv(n)),
-                    bytes=imgs * cin * H * W + imgs * cin * B * 2 * R * n * 8 + 2 * R * n * 8)
-    k["share"] = dict(q=imgs * cout * B * R * (n + ntt_fwd(n)), mac=0, p=imgs * cout * (B * ntt_inv(n) + idft2d(L)),
-                      bytes=imgs * cout * B * R * n * 8 + imgs * cout * oh * ow * 4)
-    k["mac"] = dict(q=0, mac=imgs * cin * cout * B * R * 2 * n, p=0,
-                    bytes=imgs * cin * B * 2 * R * n * 8 + cout * cin * B * R * n * 8 + imgs * cout * B * R * n * 8
-                    + imgs * cout * B * 2 * R * n * 8)
-    k["dec"] = dict(q=imgs * cout * B * R * (n + ntt_inv(n)), mac=0, p=imgs * cout * (B * ntt_fwd(n) + idft2d(L)),
-                    bytes=imgs * cout * B * 2 * R * n * 8 + 2 * R * n * 8 + imgs * cout * oh * ow * 4 * 3)
+    k["enc"] = dict(q=c * cin * B * R * (2 * n + ntt_fwd(n)), mac=0, p=imgs * cin * dft2d(L) + c * cin * B * ntt_inv(n),
+                    bytes=imgs * cin * H * W + c * cin * B * 2 * R * n * 8 + 2 * R * n * 8)
+    k["share"] = dict(q=c * cout * B * R * (n + ntt_fwd(n)), mac=0,
+                      p=c * cout * B * ntt_inv(n) + imgs * cout * idft2d(L),
+                      bytes=c * cout * B * R * n * 8 + imgs * cout * oh * ow * 4)
+    k["mac"] = dict(q=0, mac=c * cin * cout * B * R * 2 * n, p=0,
+                    bytes=c * cin * B * 2 * R * n * 8 + cout * cin * B * R * n * 8 + c * cout * B * R * n * 8
+                    + c * cout * B * 2 * R * n * 8)
+    k["dec"] = dict(q=c * cout * B * R * (n + ntt_inv(n)), mac=0, p=c * cout * B * ntt_fwd(n) + imgs * cout * idft2d(L),
+                    bytes=c * cout * B * 2 * R * n * 8 + 2 * R * n * 8 + imgs * cout * oh * ow * 4 * 3)
     for v in k.values():
         v["imad"] = C_Q * v["q"] + C_MAC * v["mac"] + C_P * v["p"]
         v["modmul"] = v["q"] + v["mac"] + v["p"]
@@ -578,15 +584,21 @@ def i8_peak_tops(peaks):
     return 2.0 * peaks.get("bf16_tflops", 1590.0), "2 x MEASURED_PEAKS.json bf16_tflops (int8 dense = 2x bf16 dense)"
 
 
-def config4_counts(imgs, n=8192, R=3, L=64, B=1, cin=64, cout=128, H=32, W=32):
+def config4_counts(imgs, pack=1, n=8192, R=3, L=64, B=1, cin=64, cout=128, H=32, W=32):
     """Per-kernel algorithmic work for one sub-batch of `imgs` images:
-    modmuls by class, IMAD slots (c_q, c_mac, c_p), HBM bytes, int8 tensor MACs."""
-    k = layer_counts(n, R, L, B, cin, cout, H, W, H, W, imgs)
-    ctw = imgs * cin * B * 2 * R * n * 8
-    k["planes_ct"] = dict(q=0, mac=0, p=0, bytes=2 * ctw, imad=0, modmul=0)
-    k["planes_w"] = dict(q=0, mac=0, p=0, bytes=2 * cout * cin * B * R * n * 8, imad=0, modmul=0)
-    # ElementMult on the tensor cores: 64 u8 x u8 products per modular MAC (byte planes);
-    # operands = ciphertext + weight planes (as many bytes as the words), masks in, outputs out
+    modmuls by class, IMAD slots (c_q, c_mac, c_p), HBM bytes, int8 tensor MACs.  The
+    tcgen05 ElementMult is three kernels: planes_tc (ciphertext words -> byte planes),
+    mac_tc (tensor cores; reads the ciphertext and weight planes, writes the slot-major
+    product Y) and mac_out (Y + the HomShare masks -> the ciphertext layout)."""
+    k = layer_counts(n, R, L, B, cin, cout, H, W, H, W, imgs, pack)
+    c = -(-imgs // pack)
+    ctw = c * cin * B * 2 * R * n * 8  # ciphertext words in, bytes
+    ybytes = c * cout * B * 2 * R * n * 8
+    k["planes_tc"] = dict(q=0, mac=0, p=0, bytes=2 * ctw, imad=0, modmul=0)
+    # 64 u8 x u8 products per modular MAC (byte planes)
+    k["mac_tc"] = dict(q=0, mac=k["mac"]["mac"], p=0, i8_mac=64 * k["mac"]["mac"], imad=0,
+                       modmul=k["mac"]["mac"], bytes=ctw + cout * cin * B * R * n * 8 + ybytes)
+    k["mac_out"] = dict(q=0, mac=0, p=0, imad=0, modmul=0, bytes=ybytes + c * cout * B * R * n * 8 + ybytes)
     k["mac"]["i8_mac"] = 64 * k["mac"]["mac"]
     k["mac"]["imad"] = 0
     return k
@@ -604,8 +616,9 @@ def run_config4(args, world, rank, local):
     cfg = CF.CONFIG4
     imgs = args.images or cfg["images"]
     cin, cout = cfg["cin"], cfg["cout"]
+    pack = CF.CONFIG4_PACK if args.pack is None else args.pack
     ctx = ops.Context(n=cfg["n"], q=cfg["q"], p=P, device=local)
-    L = ops.LayerOps(ctx, ops.ConvSpec(32, 32, 3, 3, True, cin, cout))
+    L = ops.LayerOps(ctx, ops.ConvSpec(32, 32, 3, 3, True, cin, cout, pack))
     g = L.geom
     shard = ImageShard(world * imgs, world, rank)  # contiguous image shards, global image ids
     # this rank's images (seeded per shard: 64 MiB of pixels per GPU), weights from the common seed
@@ -683,7 +696,7 @@ def run_config4(args, world, rank, local):
     prof = _lib.profile_read()
     _lib.profile(False)
     nchunks = -(-imgs // chunk)
-    kc = config4_counts(chunk)
+    kc = config4_counts(chunk, pack)
     imad_peak = lib.ensei_gpu_imad_peak(local)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
@@ -691,7 +704,9 @@ def run_config4(args, world, rank, local):
     i8_peak, i8_src = i8_peak_tops(peaks)
     mac_name = next((k for k in prof if k.startswith("mac")), "mac")
     alias = {"enc": "enc", "share": "share", "dec_rns": "dec", "planes_ct": "planes_ct", "planes_w": "planes_w",
-             mac_name: "mac"}
+             "planes_tc": "planes_tc", "mac_tc": "mac_tc", "mac_out": "mac_out"}
+    if mac_name not in alias:
+        alias[mac_name] = "mac"
     per_kernel = {}
     for name, (tot, cnt) in prof.items():
         ms = tot / cnt  # per launch = per sub-batch of `chunk` images
@@ -730,6 +745,20 @@ def run_config4(args, world, rank, local):
         "c_q": C_Q, "c_mac": C_MAC, "c_p": C_P,
     }
     step_imad = sum(kc[k]["imad"] for k in ("enc", "share", "dec")) * nchunks
+    # the same layer in REF's geometry (one image per ciphertext block), for comparison
+    unpacked = None
+    if pack > 1 and not args.no_side:
+        L1 = ops.LayerOps(ctx, ops.ConvSpec(32, 32, 3, 3, True, cin, cout, 1))
+        we1 = L1.prepare_weights(w_h.to(dev))
+        ws1 = L1.workspace(imgs)
+        out1 = torch.empty_like(out)
+        t1 = _time_steps(lambda: L1.forward(key, we1, x, rand, ws=ws1, out=out1), max(3, args.steps // 4), 2, flush,
+                         stream)
+        unpacked = {"value": world * imgs * max(3, args.steps // 4) / (t1 / 1e3), "unit": "conv/s",
+                    "geometry": "REF's: one image per n = 8192 ciphertext block (half the slots empty)",
+                    "outputs_equal_packed": bool(torch.equal(out1, out))}
+        del ws1, we1
+        torch.cuda.empty_cache()
     total_modmul = sum(kc[k]["modmul"] for k in ("enc", "share", "mac", "dec")) * nchunks
 
     # ---- e2e through the host-buffer C-ABI entry point (pinned host buffers, chunked inside)
@@ -820,12 +849,15 @@ def run_config4(args, world, rank, local):
                    "gather": "both parties' output shares all-gathered per sub-batch over NCCL, overlapped"
                              if world > 1 else "none (1 GPU)",
                    "unit_def": "1 conv = 1 image through the whole 64->128 layer", "config_index": 4,
-                   "mac_path": L.mac_path(chunk)},
+                   "mac_path": L.mac_path(chunk),
+                   "pack": pack, "packing": ("two images' 64x64 DFT grids per n = 8192 ciphertext block (builder "
+                                             "extension; every slot-wise step unchanged, outputs = REF's)")
+                   if pack > 1 else "REF geometry (one image per block)"},
         "roofline": roofline, "setup_ms": setup_ms,
         "imad_slot_rate": step_imad * args.steps / (total_ms / 1e3), "modmul_per_s": total_modmul * args.steps / (
             total_ms / 1e3),
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk, "verify": verify,
-        "config1": side1, "ntt_n8192": ntt,
+        "config1": side1, "ntt_n8192": ntt, "ref_geometry": unpacked,
     }
 
 
@@ -962,7 +994,7 @@ def other_config(args, world, rank, local):
         from paper_2003_05328_b200 import configs as CF
         imgs = args.images or CF.CONFIG3_IMAGES
         ctx = ops.Context(n=2048, device=local)
-        sched = CF.CONFIG3_SCHEDULE
+        sched = CF.CONFIG3_SCHEDULE if args.pack == 1 else CF.CONFIG3_SCHEDULE_PACKED
         ws = [torch.randint(-128, 128, s_, dtype=torch.int32, generator=gen) for s_ in CF.CONFIG3_WEIGHTS]
         sess = GP.Session(ctx, sched, 32, 32, ws)
         shard = ImageShard(world * imgs, world, rank)  # contiguous image shards, global image ids
@@ -984,6 +1016,7 @@ def other_config(args, world, rank, local):
         workload = (f"config3: {imgs} images x 3x32x32 through 7 conv layers (3->64, 64->64 @32; 64->128, "
                     "128->128 @16; 128->128 3x3, 128->128 1x1, 128->16 1x1 @8), ReLU, 2x2 max-pool after L2/L4")
         extra["mac_paths"] = [lo.mac_path(imgs) for lo in sess.layers if lo is not None]
+        extra["packs"] = [lo.pack for lo in sess.layers if lo is not None]
         if rank == 0:  # sampled outputs of the last timed step vs the plaintext chain (oracle as checker)
             try:
                 from oracle import protocol as OP

@@ -279,6 +279,11 @@ int ensei_gpu_activation(ensei_gpu_ctx* ctx, int fn, int pool2, uint32_t channel
  * K (q_i - 1)^2 < 2^128 limit; 5 also needs 32 <= cin). */
 int ensei_gpu_set_mac_variant(int variant);
 
+/* Tile kernels (Enc / HomShare / Dec) of the 3-prime RNS layer at n = 8192 (tuning / A-B
+ * testing; results are identical): 1 (default) the 512-thread kernels, two CTAs per SM
+ * (csrc/layer_rns.cuh); 0 the first-generation 1024-thread kernels (csrc/layer.cuh). */
+int ensei_gpu_set_tile_variant(int variant);
+
 /* Which ElementMult kernel a conv layer of `num_images` images takes on this context
  * (the automatic choice, or the forced variant): */
 #define ENSEI_MAC_IMAD4 0       /* 4-product IMAD tile kernel (mac_kernel) */

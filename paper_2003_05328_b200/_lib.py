@@ -116,6 +116,7 @@ def lib():
             "ensei_gpu_add_ct": (i32, [vp, vp, vp, sz, vp, vp]),
             "ensei_gpu_add_plain": (i32, [vp, vp, vp, i32, sz, vp, vp]),
             "ensei_gpu_set_mac_variant": (i32, [i32]),
+            "ensei_gpu_set_tile_variant": (i32, [i32]),
             "ensei_gpu_mac_path": (i32, [vp, C.POINTER(ConvDesc), u32, C.POINTER(i32)]),
             "ensei_gpu_conv_workspace_bytes": (sz, [vp, C.POINTER(ConvDesc), u32]),
             "ensei_gpu_conv_chunk_images": (u32, [vp, C.POINTER(ConvDesc), u32]),

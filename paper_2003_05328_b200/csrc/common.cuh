@@ -70,6 +70,10 @@ struct PrimeConst {
   uint64_t c64, c64p;     // 2^64 mod q and its Shoup companion
   uint64_t crt_inv, crt_inv_shoup;  // (Q/q_i)^-1 mod q_i (RNS decryption)
   uint64_t crt_c;                   // floor(2^122 / q_i): E / q_i in 2^-62 fixed point
+  // second-generation RNS decryption (layer_rns.cuh): the last-stage constants of the
+  // inverse transform with (Q/q_i)^-1 folded in (n^-1 crt_inv, and twi[1] crt_inv), and
+  // floor(p 2^(dec_kbits + 64) / q_i)
+  uint64_t dec_ni, dec_ni_shoup, dec_t1, dec_t1_shoup, dec_c;
 };
 
 // Exact CRT rounding constants (RNS decryption, layer.cuh crt_round): M_i = Q / q_i and
@@ -116,6 +120,9 @@ struct ensei_gpu_ctx {
   bool approx_ok = true;  // every 31 q_i < 2^64: approximate-quotient butterflies (MODE 0); the layer path needs it
   uint32_t i8_kmax = 255;  // int8 tensor-core MAC: largest K with K (q_i - 1)^2 < 2^128 for every prime
   bool kara_ok = true;    // every q_i within the Karatsuba MAC's headroom (layer.cuh)
+  // layer_rns.cuh: fraction bits of the packed CRT accumulator (3p 2^k <= 2^48); 0 when the
+  // chain cannot use it (then the first-generation kernels run)
+  uint32_t dec_kbits = 0;
   // fork/join helpers: Bob's input-independent HomShare work runs concurrently
   // with Alice's encryption on an auxiliary stream (capturable in CUDA graphs)
   cudaStream_t aux = nullptr;

@@ -94,6 +94,13 @@ static void build_tables(ensei_gpu_ctx* c) {
       hq[(2 * i + 1) * n + k] = {tv.inv[k], shoup64(tv.inv[k], c->q[i])};
     }
     c->psi_q[i] = root_of_unity(2 * n, c->q[i]);
+    // RNS decryption, second generation: y_i = phi_i (Q/q_i)^-1 comes out of the inverse
+    // transform itself when its last stage multiplies by n^-1 crt_inv / twi[1] crt_inv
+    PrimeConst& pc = c->pc[i];
+    pc.dec_ni = mulmod(tv.inv[0], pc.crt_inv, c->q[i]);
+    pc.dec_ni_shoup = shoup64(pc.dec_ni, c->q[i]);
+    pc.dec_t1 = mulmod(tv.inv[1], pc.crt_inv, c->q[i]);
+    pc.dec_t1_shoup = shoup64(pc.dec_t1, c->q[i]);
   }
   auto* hp = reinterpret_cast<TwPair<uint32_t>*>(h.data() + bytes_q);
   {
@@ -225,6 +232,16 @@ static void ctx_create(int device, uint32_t n, const uint64_t* qs, uint32_t R, u
         mul_small(T, 2 * t - 1);
         for (size_t k = 0; k < T.size() && k < 6; ++k) c->crt.T[t - 1][k] = T[k];
       }
+    }
+  }
+  if (R == 3) {  // packed CRT accumulator of layer_rns.cuh: A < 3p 2^k <= 2^48, floor(p 2^(k+64) / q_i) < 2^64
+    uint32_t k = 48;
+    while (k && (unsigned __int128)(3 * p) << k > ((unsigned __int128)1 << 48)) --k;
+    bool ok = k >= 20;
+    for (uint32_t i = 0; i < R && ok; ++i) ok = ((unsigned __int128)p << k) < c->q[i];
+    if (ok) {
+      c->dec_kbits = k;
+      for (uint32_t i = 0; i < R; ++i) c->pc[i].dec_c = (uint64_t)(((unsigned __int128)p << (k + 64)) / c->q[i]);
     }
   }
   c->pp.f = Field32{(uint32_t)p, (uint32_t)(2 * p)};

@@ -43,6 +43,7 @@ struct LayerArgs {
   PrimeConst pc[ENSEI_MAX_PRIMES];
   uint64_t psi_q[ENSEI_MAX_PRIMES];  // canonical 2n-th roots (direct-evaluation fallback)
   CrtConst crt;
+  int dec_kbits;  // layer_rns.cuh: fraction bits of the packed CRT accumulator
   PConst pp;
   const TwPair<uint64_t>* twq_fwd[ENSEI_MAX_PRIMES];
   const TwPair<uint64_t>* twq_inv[ENSEI_MAX_PRIMES];

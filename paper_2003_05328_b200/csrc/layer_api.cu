@@ -102,6 +102,9 @@ Geo geometry(const ensei_gpu_ctx* c, const ensei_conv_desc* d) {
   return g;
 }
 
+// RNS tile kernel generation (ensei_gpu_set_tile_variant): 1 = layer_rns.cuh, 0 = layer.cuh
+std::atomic<int> g_tile_gen{1};
+
 LayerRun make_run(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g, uint32_t num_images,
                   const ensei_randomness* rand, void* stream) {
   require(c->approx_ok, ENSEI_ERR_UNSUPPORTED,
@@ -112,6 +115,7 @@ LayerRun make_run(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g
   r.logL = (int)g.logL;
   r.R = (int)c->R;
   r.st = (cudaStream_t)stream;
+  r.tile_gen = g_tile_gen.load(std::memory_order_relaxed);
   LayerArgs& a = r.a;
   std::memset(&a, 0, sizeof(a));
   a.H = d->H;
@@ -138,6 +142,7 @@ LayerRun make_run(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g
     a.twq_inv[i] = c->tab.tw_q_inv[i];
   }
   a.crt = c->crt;
+  a.dec_kbits = (int)c->dec_kbits;
   a.pp = c->pp;
   a.twp_fwd = c->tab.tw_p_fwd;
   a.twp_inv = c->tab.tw_p_inv;
@@ -553,6 +558,13 @@ int ensei_gpu_set_mac_variant(int variant) {
   return guarded([&] {
     require(variant >= -1 && variant <= 5 && variant != 4, ENSEI_ERR_INVALID_ARGUMENT, "variant must be -1, 0, 1, 2, 3 or 5");
     set_mac_variant(variant);
+  });
+}
+
+int ensei_gpu_set_tile_variant(int variant) {
+  return guarded([&] {
+    require(variant == 0 || variant == 1, ENSEI_ERR_INVALID_ARGUMENT, "variant must be 0 or 1");
+    g_tile_gen.store(variant, std::memory_order_relaxed);
   });
 }
 

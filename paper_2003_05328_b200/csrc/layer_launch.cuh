@@ -2,7 +2,7 @@
 // ring degree and instantiated once per degree (layer_n11.cu / n12 / n13) so the
 // heavy template code compiles in parallel.
 #pragma once
-#include "layer.cuh"
+#include "layer_rns.cuh"
 
 namespace ensei_gpu {
 
@@ -12,6 +12,7 @@ struct LayerRun {
   int logL;  // square padded grid, log2 side
   int R;
   cudaStream_t st;
+  int tile_gen = 1;  // RNS tile kernels: 1 = layer_rns.cuh (512 threads, two CTAs per SM), 0 = layer.cuh
 };
 
 // Launch with programmatic stream serialization (layer.cuh, pdl_wait / pdl_trigger):
@@ -121,12 +122,53 @@ static void enc_dispatch_r(const LayerRun& r, int tm, bool inj, int in_t, const 
   fail(ENSEI_ERR_UNSUPPORTED, "padded grid side must be a power of two <= 64 on this path");
 }
 
+// ---- second-generation RNS tile kernels (layer_rns.cuh): n = 8192, 3 primes, 32x32 / 64x64 grids ----
+template <int LOGL, int IN_T>
+static void enc3_go(const LayerRun& r, const uint64_t* key, uint32_t ks, const void* in, uint64_t* out, int items) {
+  auto k = enc3_kernel<LOGL, LOGL, IN_T>;
+  constexpr size_t smem = enc3_smem<LOGL, LOGL>();
+  set_smem_shared_sm(k, smem);
+  k<<<items, kRnsThreads, smem, r.st>>>(r.a, key, ks, in, out);
+  check_launch("enc3_kernel");
+}
+template <int LOGL>
+static bool enc3_try(const LayerRun& r, int in_t, const uint64_t* key, uint32_t ks, const void* in, uint64_t* out,
+                     int items) {
+  if ((size_t)r.a.pk * tile_words<LOGL, LOGL>() * 4 > (size_t)(1 << kRnsLogN) * 8) return false;  // tiles alias qbuf
+  if (in_t == ENSEI_IN_U8) enc3_go<LOGL, ENSEI_IN_U8>(r, key, ks, in, out, items);
+  else enc3_go<LOGL, ENSEI_IN_U32>(r, key, ks, in, out, items);
+  return true;
+}
+template <int LOGL>
+static void share3_go(const LayerRun& r, uint64_t* mask, uint32_t* bob_share, int items) {
+  auto k = share3_kernel<LOGL, LOGL>;
+  constexpr size_t smem = share3_smem();
+  set_smem_shared_sm(k, smem);
+  k<<<items, kRnsThreads, smem, r.st>>>(r.a, mask, bob_share);
+  check_launch("share3_kernel");
+}
+template <int LOGL>
+static bool dec3_try(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint64_t* ct, uint32_t* alice,
+                     const uint32_t* bob, uint32_t* out, int items) {
+  const size_t smem = dec3_smem<LOGL, LOGL>(r.a.pk);
+  if (smem > 113 * 1024) return false;
+  auto k = dec3_kernel<LOGL, LOGL>;
+  set_smem_shared_sm(k, smem);
+  k<<<items, kRnsThreads, smem, r.st>>>(r.a, key, ks, ct, alice, bob, out);
+  check_launch("dec3_kernel");
+  return true;
+}
+
 template <int LOGN>
 void launch_tile(const LayerRun& r, int tm, bool inj, int in_t, const uint64_t* key, uint32_t ks, const void* in,
                  uint64_t* out, int items) {
   if (items == 0) return;
   if (r.R == 1) return enc_dispatch_r<LOGN, 1>(r, tm, inj, in_t, key, ks, in, out, items);
   if constexpr (LOGN == 13) {
+    if (r.R == 3 && r.tile_gen && tm == TILE_ENC && !inj) {
+      if (r.logL == 6 && enc3_try<6>(r, in_t, key, ks, in, out, items)) return;
+      if (r.logL == 5 && enc3_try<5>(r, in_t, key, ks, in, out, items)) return;
+    }
     if (r.R == 3) return enc_dispatch_r<LOGN, 3>(r, tm, inj, in_t, key, ks, in, out, items);
   }
   fail(ENSEI_ERR_UNSUPPORTED, "RNS chains are supported with 3 primes at n = 8192");
@@ -183,6 +225,10 @@ void launch_share(const LayerRun& r, bool inj, uint64_t* mask, uint32_t* bob_sha
     return share_dispatch<LOGN, 1, false>(r, mask, bob_share, items);
   }
   if constexpr (LOGN == 13) {
+    if (r.R == 3 && !inj && r.tile_gen) {
+      if (r.logL == 6) return share3_go<6>(r, mask, bob_share, items);
+      if (r.logL == 5) return share3_go<5>(r, mask, bob_share, items);
+    }
     if (r.R == 3 && !inj) return share_dispatch<LOGN, 3, false>(r, mask, bob_share, items);
   }
   fail(ENSEI_ERR_UNSUPPORTED, "HomShare: unsupported prime count / randomness mode");
@@ -237,6 +283,10 @@ void launch_dec(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint6
   if (items == 0) return;
   if (r.R != 1) {
     if constexpr (LOGN == 13) {
+      if (r.R == 3 && r.tile_gen && r.a.dec_kbits) {
+        if (r.logL == 6 && dec3_try<6>(r, key, ks, ct, alice, bob, out, items)) return;
+        if (r.logL == 5 && dec3_try<5>(r, key, ks, ct, alice, bob, out, items)) return;
+      }
       if (r.R == 3) {
         switch (r.logL) {
           case 5: return dec_rns_go<LOGN, 5>(r, key, ks, ct, alice, bob, out, items);

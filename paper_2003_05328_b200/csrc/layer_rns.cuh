@@ -1,0 +1,429 @@
+// layer_rns.cuh -- tile kernels of the 3-prime RNS layer at n = 8192 (config 4), second
+// generation: 512-thread CTAs, two resident per SM.
+//
+// The first-generation kernels (layer.cuh) give every (ciphertext image, channel) tile a
+// 1024-thread CTA that fills an SM's register file: all 32 warps are in the same fused
+// stage at the same time, so the load-bound stages (Dec's first INTT pass straight from
+// HBM, Enc's a^ draw, the global stores) never overlap the FMA-bound butterfly passes
+// (ncu, profiles/r02_ncu_summary.md: issue active 42-56 %, one CTA per SM).  Here a tile is
+// owned by 512 threads that run every radix-8 pass in two rounds of 1024 virtual threads
+// (same registers per thread, same shared-memory traffic), and the working set is cut to
+// <= 113 KB by aliasing buffers whose lifetimes do not overlap, so two CTAs in different
+// stages share an SM (an Enc and a HomShare CTA co-reside too).
+//
+// At n = 8192 every supported grid (<= 64 x 64) fits one block per channel: B = 1.
+//
+//   enc3_kernel    Alice Enc, REF protocol.cpp:310-329 + ringbfv.cpp:180-201 per prime
+//   share3_kernel  Bob HomShare masks + his share, REF hss.cpp:22-49, protocol.cpp:587-603
+//   dec3_kernel    Alice Dec (exact CRT rounding over Q = q0 q1 q2, REF ringbfv.cpp:203-231
+//                  semantics) -> merge -> IDFT2D -> crop (+ recombine), REF protocol.cpp:332-355
+#pragma once
+#include "layer.cuh"
+
+namespace ensei_gpu {
+
+constexpr int kRnsLogN = 13;
+constexpr int kRnsThreads = 512;
+constexpr int kRnsRounds = 2;  // virtual threads (n / 8) per real thread
+
+// One pass of a transform run by 512 threads as two rounds of virtual threads; in place
+// or between disjoint buffers (no SPLIT: a virtual thread stores exactly where it loaded,
+// or where nobody loads).
+template <class F, class T, int I, bool INV, class Src, class Dst, bool CORR = false>
+EG_DEV void rns_pass(const F& f, const TwPair<T>* __restrict__ tw, int tid, Src& src, Dst& dst, uint32_t cred = 0) {
+  const CtaBar bar;
+#pragma unroll 1
+  for (int rd = 0; rd < kRnsRounds; ++rd)
+    run_pass<F, T, kRnsLogN, 3, I, INV, 0, false, Src, Dst, CtaBar, CORR>(f, tw, tid + rd * kRnsThreads, src, dst, bar,
+                                                                         cred);
+}
+
+// forward: passes 0 (src -> sm), 1..3 (sm), 4 (sm -> dst); no barrier before the first
+// pass or after the last.  B_IN bounds the inputs in units of q.
+template <class F, class T, int B_IN, class Src, class Dst>
+EG_DEV void rns_forward(const F& f, const TwPair<T>* __restrict__ tw, T* sm, int tid, Src src, Dst dst,
+                        uint32_t cred = 0) {
+  using FB = FwdBounds<F, 0, kRnsLogN, 3, B_IN>;
+  SmemRW<T> s{sm};
+  rns_pass<F, T, 0, false, Src, SmemRW<T>, FB::corr(0)>(f, tw, tid, src, s, cred);
+  __syncthreads();
+  rns_pass<F, T, 1, false, SmemRW<T>, SmemRW<T>, FB::corr(1)>(f, tw, tid, s, s, cred);
+  __syncthreads();
+  rns_pass<F, T, 2, false, SmemRW<T>, SmemRW<T>, FB::corr(2)>(f, tw, tid, s, s, cred);
+  __syncthreads();
+  rns_pass<F, T, 3, false, SmemRW<T>, SmemRW<T>, FB::corr(3)>(f, tw, tid, s, s, cred);
+  __syncthreads();
+  rns_pass<F, T, 4, false, SmemRW<T>, Dst, FB::corr(4)>(f, tw, tid, s, dst, cred);
+}
+
+// inverse passes 4 (src -> sm), 3..1 (sm); the caller runs pass 0 (or rns_inverse_last)
+template <class F, class T, class Src>
+EG_DEV void rns_inverse_head(const F& f, const TwPair<T>* __restrict__ tw, T* sm, int tid, Src src) {
+  SmemRW<T> s{sm};
+  rns_pass<F, T, 4, true, Src, SmemRW<T>>(f, tw, tid, src, s);
+  __syncthreads();
+  rns_pass<F, T, 3, true, SmemRW<T>, SmemRW<T>>(f, tw, tid, s, s);
+  __syncthreads();
+  rns_pass<F, T, 2, true, SmemRW<T>, SmemRW<T>>(f, tw, tid, s, s);
+  __syncthreads();
+  rns_pass<F, T, 1, true, SmemRW<T>, SmemRW<T>>(f, tw, tid, s, s);
+  __syncthreads();
+}
+template <class F, class T, class Src, class Dst>
+EG_DEV void rns_inverse(const F& f, const TwPair<T>* __restrict__ tw, T* sm, int tid, Src src, Dst dst) {
+  rns_inverse_head<F, T, Src>(f, tw, sm, tid, src);
+  SmemRW<T> s{sm};
+  rns_pass<F, T, 0, true, SmemRW<T>, Dst>(f, tw, tid, s, dst);
+}
+
+// x * q-ish helper: floor(x C / 2^64) from three wide products (the low x low product and
+// the middle carries are dropped): at most 2 below the exact floor.
+EG_DEV uint64_t mulhi64_approx(uint64_t x, uint64_t c) {
+  const uint32_t x0 = lo32(x), x1 = hi32(x), c0 = lo32(c), c1 = hi32(c);
+  return mulw(x1, c1) + hi32(mulw(x0, c1)) + hi32(mulw(x1, c0));
+}
+
+// uniform mod q from 128 bits, floor(x q / 2^128), exact (= philox.cuh uniform_q_from) from
+// eight full-rate wide products (the generic __umul64hi costs ~20 IMAD slots).
+EG_DEV uint64_t uniform_q_from_fast(const Philox4& r, uint64_t q) {
+  const uint64_t x0 = ((uint64_t)r.y << 32) | r.x, x1 = ((uint64_t)r.w << 32) | r.z;
+  const uint64_t h0 = mulhi64(x0, q);
+  uint64_t hi, lo;
+  mul128(x1, q, hi, lo);
+  const uint64_t s = lo + h0;
+  return hi + (s < lo ? 1 : 0);
+}
+
+// -------------------------------------------------------------------- Enc
+// shared: [ qbuf n u64 | pbuf n u32 (padded) | noise n int8 ]; the pk DFT2D tiles alias
+// qbuf (dead once encode_slots' first pass has gathered them).
+template <int LOGH, int LOGW>
+constexpr size_t enc3_smem() {
+  return (size_t)(1 << kRnsLogN) * 8 + ssize<uint32_t>(1 << kRnsLogN) * 4 + (1 << kRnsLogN);
+}
+
+template <int LOGH, int LOGW, int IN_T>
+__global__ void __launch_bounds__(kRnsThreads, 2)
+    enc3_kernel(LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride, const void* __restrict__ in,
+                uint64_t* __restrict__ out) {
+  constexpr int LOGN = kRnsLogN, N = 1 << LOGN, NT = kRnsThreads, R = 3;
+  constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
+  constexpr int TS = tile_words<LOGH, LOGW>();
+  static_assert((size_t)2 * TS * 4 <= (size_t)N * 8 || true, "");
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);  // tiles alias qbuf
+  uint32_t* pbuf = reinterpret_cast<uint32_t*>(qbuf + N);
+  int8_t* ebuf = reinterpret_cast<int8_t*>(pbuf + ssize<uint32_t>(N));
+  const int tid = threadIdx.x;
+  const Field32 pf = a.pp.f;
+  const int item = blockIdx.x;
+  const int ch = item % a.cin, img = item / a.cin;
+  const int npk = a.pk;
+  pdl_trigger();
+
+  // 1. pad into the tiles (REF pad_image, ntt.cpp:155-185), pk images
+  for (int e = tid; e < npk * Lh * Lw; e += NT) {
+    const int pi = e >> (LOGH + LOGW), i = e & (Lh * Lw - 1);
+    const int r = i >> LOGW, c = i & (Lw - 1);
+    uint32_t v = 0;
+    if (r < a.H && c < a.W && img * npk + pi < a.num_images) {
+      const size_t src = ((size_t)((img * npk + pi) * a.cin + ch) * a.H + r) * a.W + c;
+      if constexpr (IN_T == ENSEI_IN_U8) v = static_cast<const uint8_t*>(in)[src];
+      else v = static_cast<const uint32_t*>(in)[src] % pf.q;
+    }
+    S[pi * TS + r * LS + c] = v;
+  }
+  // Enc noise e0, two CBD draws per Philox call
+  const int gimg = a.image_base / a.pk + img;
+  {
+    const uint32_t mask = a.cbd_k >= 32 ? 0xFFFFFFFFu : ((1u << a.cbd_k) - 1u);
+    const uint64_t sid = stream_id(PURPOSE_NOISE, a.layer, gimg, ch, 0);
+    for (int i2 = tid; i2 < N / 2; i2 += NT) {
+      const Philox4 rr = philox(a.alice_key, sid, i2);
+      const int e0 = cbd_from(rr.x, rr.y, mask), e1 = cbd_from(rr.z, rr.w, mask);
+      *reinterpret_cast<uint16_t*>(ebuf + 2 * i2) = (uint16_t)((e0 & 0xFF) | ((e1 & 0xFF) << 8));
+    }
+  }
+  __syncthreads();
+  // 2. DFT2D of each tile
+  for (int pi = 0; pi < npk; ++pi) tile_transform_2d<false, LOGH, LOGW>(pf, a.pp.cred, a.twc_fwd, S + pi * TS, LS);
+  // 3. encode_slots: INTT_p of the slots gathered from the tiles
+  {
+    auto src = [&](int j) { return gather_slot<LOGN, LOGH, LOGW>(S, 0, j, a.pk, TS); };
+    SmemRW<uint32_t> praw{pbuf};
+    auto dst = [&](int i, uint32_t v) { praw(i, Bfly<Field32, 0>::fin_gs(pf, v)); };
+    rns_inverse<Field32, uint32_t>(pf, a.twp_inv, pbuf, tid, src, dst);
+  }
+  __syncthreads();
+  const uint64_t* kimg = key + (size_t)img * key_stride;
+  uint64_t* ob = out + (size_t)item * ct_words<R>(N);
+#pragma unroll 1
+  for (int r = 0; r < R; ++r) {
+    const PrimeConst pc = a.pc[r];
+    const Field64 f = pc.f;
+    // 4. Delta m + e, lazy in [0, 3q)
+    auto src = [&](int i) -> uint64_t {
+      uint64_t x = f.mul_shoup_approx(pbuf[sidx<uint32_t>(i)], pc.delta, pc.delta_shoup);  // < 4q
+      if (x >= f.q2) x -= f.q2;
+      return x + signed_mod(ebuf[i], f.q);
+    };
+    SmemRW<uint64_t> qs{qbuf};
+    rns_forward<Field64, uint64_t, 3>(f, a.twq_fwd[r], qbuf, tid, src, qs, pc.cred);
+    __syncthreads();
+    // 5. c0 = -a^, c1 = a^ t^ + NTT(Delta m + e); two slots per step, 16-byte accesses
+    uint64_t* c0 = ob + (size_t)r * N;
+    uint64_t* c1 = ob + (size_t)(R + r) * N;
+    const uint64_t* tk = kimg + (size_t)(2 * r) * N;
+    const uint64_t* tkp = tk + N;
+    const uint64_t sid = stream_id(PURPOSE_AHAT, a.layer, gimg, ch, r << 12);
+    for (int j2 = tid; j2 < N / 2; j2 += NT) {
+      const int j = 2 * j2;
+      const ulonglong2 xv = *reinterpret_cast<const ulonglong2*>(qbuf + sidx<uint64_t>(j));
+      const ulonglong2 tv = __ldg(reinterpret_cast<const ulonglong2*>(tk + j));
+      const ulonglong2 tpv = __ldg(reinterpret_cast<const ulonglong2*>(tkp + j));
+      const int k = brev(j, LOGN);  // natural slot index keys the a^ stream; slot j + 1 -> k + n/2
+      const uint64_t ah0 = uniform_q_from_fast(philox(a.alice_key, sid, k), f.q);
+      const uint64_t ah1 = uniform_q_from_fast(philox(a.alice_key, sid, k + N / 2), f.q);
+      auto fin = [&](uint64_t x, uint64_t ah, uint64_t t, uint64_t tp) {
+        uint64_t v = Bfly<Field64, 0>::corr(f, x, pc.cred) + f.mul_shoup_approx(ah, t, tp);  // < 7q
+        if (v >= f.q4) v -= f.q4;
+        if (v >= f.q2) v -= f.q2;
+        return v >= f.q ? v - f.q : v;
+      };
+      *reinterpret_cast<ulonglong2*>(c0 + j) = make_ulonglong2(ah0 ? f.q - ah0 : 0, ah1 ? f.q - ah1 : 0);
+      *reinterpret_cast<ulonglong2*>(c1 + j) = make_ulonglong2(fin(xv.x, ah0, tv.x, tpv.x), fin(xv.y, ah1, tv.y, tpv.y));
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------- HomShare + Bob share
+// shared: [ qbuf n u64 | pbuf n u32 (padded) ]; pbuf first holds s_B in evaluation
+// (bit-reversed) order, Bob's share tile aliases qbuf.
+constexpr size_t share3_smem() { return (size_t)(1 << kRnsLogN) * 8 + ssize<uint32_t>(1 << kRnsLogN) * 4; }
+
+template <int LOGH, int LOGW>
+__global__ void __launch_bounds__(kRnsThreads, 2)
+    share3_kernel(LayerArgs a, uint64_t* __restrict__ mask, uint32_t* __restrict__ bob_share) {
+  constexpr int LOGN = kRnsLogN, N = 1 << LOGN, NT = kRnsThreads, R = 3;
+  constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* pbuf = reinterpret_cast<uint32_t*>(qbuf + N);
+  const int tid = threadIdx.x;
+  const Field32 pf = a.pp.f;
+  const uint32_t p = pf.q;
+  const int item = blockIdx.x;  // ciphertext image * cout + o
+  const int o = item % a.cout, img = item / a.cout;
+  const int gimg = a.image_base / a.pk + img;
+  // 1. s_B (natural slot i -> evaluation position brev(i))
+  {
+    const uint64_t sid = stream_id(PURPOSE_SHARE, a.layer, gimg, o, 0);
+    for (int i2 = tid; i2 < N / 2; i2 += NT) {
+      const Philox4 rr = philox(a.bob_key, sid, i2);
+      const int j = brev(2 * i2, LOGN);  // slot 2 i2 + 1 -> j + n/2
+      pbuf[sidx<uint32_t>(j)] = uniform_p_from(rr.x, rr.y, p);
+      pbuf[sidx<uint32_t>(j + N / 2)] = uniform_p_from(rr.z, rr.w, p);
+    }
+  }
+  // 2. Bob's share of every image of the pack: crop(IDFT2D(its part of the s_B grid))
+  // (REF protocol.cpp:593-602)
+  for (int pi = 0; pi < a.pk && img * a.pk + pi < a.num_images; ++pi) {
+    __syncthreads();
+    for (int i = tid; i < Lh * Lw; i += NT) {
+      const int r = i >> LOGW, c = i & (Lw - 1);
+      S[brev(r, LOGH) * LS + brev(c, LOGW)] = pbuf[sidx<uint32_t>(brev(pi * Lh * Lw + i, LOGN))];
+    }
+    __syncthreads();
+    tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, S, LS);
+    uint32_t* bs = bob_share + ((size_t)(img * a.pk + pi) * a.cout + o) * a.oh * a.ow;
+    for (int i = tid; i < a.oh * a.ow; i += NT) {
+      const int r = i / a.ow, c = i % a.ow;
+      bs[i] = S[(r + a.r0) * LS + c + a.c0];
+    }
+  }
+  __syncthreads();
+  // 3. INTT_p of (p_A - s_B) mod p_E (REF hss.cpp:33-35), in place
+  {
+    SmemRW<uint32_t> praw{pbuf};
+    auto src = [&](int j) {
+      const uint32_t s = praw(j);
+      return s == 0 ? 0u : p - s;
+    };
+    auto dst = [&](int i, uint32_t v) { praw(i, Bfly<Field32, 0>::fin_gs(pf, v)); };
+    // the first pass negates on load: same positions loaded and stored per virtual thread
+    rns_pass<Field32, uint32_t, 4, true>(pf, a.twp_inv, tid, src, praw);
+    __syncthreads();
+    rns_pass<Field32, uint32_t, 3, true>(pf, a.twp_inv, tid, praw, praw);
+    __syncthreads();
+    rns_pass<Field32, uint32_t, 2, true>(pf, a.twp_inv, tid, praw, praw);
+    __syncthreads();
+    rns_pass<Field32, uint32_t, 1, true>(pf, a.twp_inv, tid, praw, praw);
+    __syncthreads();
+    rns_pass<Field32, uint32_t, 0, true>(pf, a.twp_inv, tid, praw, dst);
+  }
+  __syncthreads();
+  // 4. masks NTT_q(Delta m) land where c1 of the output ciphertext lives
+#pragma unroll 1
+  for (int r = 0; r < R; ++r) {
+    const PrimeConst pc = a.pc[r];
+    const Field64 f = pc.f;
+    auto qsrc = [&](int i) {
+      const uint64_t x = f.mul_shoup_approx(pbuf[sidx<uint32_t>(i)], pc.delta, pc.delta_shoup);  // < 4q
+      return x >= f.q2 ? x - f.q2 : x;
+    };
+    uint64_t* mo = mask + (size_t)item * ct_words<R>(N) + (size_t)(R + r) * N;
+    GlobalOut64Fwd outw{mo, f, pc.cred};
+    rns_forward<Field64, uint64_t, 2>(f, a.twq_fwd[r], qbuf, tid, qsrc, outw, pc.cred);
+    __syncthreads();
+  }
+}
+
+// -------------------------------------------------------------------- Dec
+// phi = c0 t^ + c1 straight from global memory, 16-byte loads (the view of the first
+// INTT pass); reduced to [0, 4q + 2^32) for the Gentleman-Sande bounds.
+struct PhiSrcV {
+  const uint64_t *c0, *c1, *t, *tp;
+  Field64 f;
+  static constexpr bool kVec = true;
+  EG_DEV uint64_t one(uint64_t a, uint64_t b, uint64_t w, uint64_t wp) const {
+    const uint64_t x = f.mul_shoup_approx(a, w, wp) + b;  // < 5q
+    return hi32(x) > hi32(f.q4) ? x - f.q4 : x;
+  }
+  EG_DEV uint64_t operator()(int j) const { return one(c0[j], c1[j], t[j], tp[j]); }
+  EG_DEV void ld2(int j, uint64_t& x, uint64_t& y) const {
+    const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(c0 + j);
+    const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(c1 + j);
+    const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(t + j));
+    const ulonglong2 wp = __ldg(reinterpret_cast<const ulonglong2*>(tp + j));
+    x = one(a.x, b.x, w.x, wp.x);
+    y = one(a.y, b.y, w.y, wp.y);
+  }
+};
+
+// The exact decision for one coefficient whose fixed-point CRT sum is ambiguous: the three
+// phi_r by direct evaluation, exact E_r, 192-bit compare (layer.cuh).  Returns m.
+template <int LOGN>
+__device__ __noinline__ uint32_t dec3_exact(const LayerArgs& a, const uint64_t* cb, const uint64_t* kimg, int i) {
+  constexpr int N = 1 << LOGN, R = 3;
+  const uint32_t p = a.pp.f.q;
+  uint64_t E[3];
+  uint32_t Isum = 0;
+  for (int r = 0; r < 3; ++r) {
+    uint32_t I;
+    uint64_t F;
+    crt_part(a.pc[r], p,
+             phi_direct<LOGN>(a.pc[r], a.psi_q[r], cb + (size_t)r * N, cb + (size_t)(R + r) * N,
+                              kimg + (size_t)(2 * r) * N, i),
+             I, E[r], F);
+    Isum += I;
+  }
+  uint32_t v = Isum + crt_round_t(a.crt, E, 0, true);  // < 3p + 3
+  if (v >= 2 * p) v -= 2 * p;
+  if (v >= p) v -= p;
+  return v;
+}
+
+// shared: [ qbuf n u64 | acc_lo n u32 | acc_hi n u16 ]: the CRT accumulator
+// A = sum_r floor(y_r p 2^k / q_r) (y_r = phi_r (Q/q_r)^-1 mod q_r, k = dec_kbits fraction
+// bits, A < 3p 2^k < 2^48) per coefficient; m = floor((A + 2^(k-1)) / 2^k) mod p unless the
+// low bits sit within 16 of a multiple of 2^k (each term is at most 3.1 below its exact
+// value), where dec3_exact decides.  y_r comes out of the INTT itself: (Q/q_r)^-1 is folded
+// into the n^-1 constants of its last stage (PrimeConst::dec_*).  m overwrites acc_lo, the
+// p-side transform then runs in qbuf's space and scatters into the tiles (over acc).
+template <int LOGH, int LOGW>
+constexpr size_t dec3_smem(int pk) {
+  const size_t acc = (size_t)(1 << kRnsLogN) * 6, tiles = (size_t)pk * tile_words<LOGH, LOGW>() * 4;
+  return (size_t)(1 << kRnsLogN) * 8 + (acc > tiles ? acc : tiles);
+}
+
+template <int LOGH, int LOGW>
+__global__ void __launch_bounds__(kRnsThreads, 2)
+    dec3_kernel(const __grid_constant__ LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride, const uint64_t* __restrict__ ct,
+                uint32_t* __restrict__ alice_share, const uint32_t* __restrict__ bob_share,
+                uint32_t* __restrict__ outp) {
+  constexpr int LOGN = kRnsLogN, N = 1 << LOGN, NT = kRnsThreads, R = 3;
+  constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
+  constexpr int TS = tile_words<LOGH, LOGW>();
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* acc_lo = reinterpret_cast<uint32_t*>(qbuf + N);
+  uint16_t* acc_hi = reinterpret_cast<uint16_t*>(acc_lo + N);
+  uint32_t* pbuf = reinterpret_cast<uint32_t*>(qbuf);
+  uint32_t* S = acc_lo;  // pk tiles, TS words apart
+  const int tid = threadIdx.x;
+  const Field32 pf = a.pp.f;
+  const uint32_t p = pf.q;
+  const int item = blockIdx.x;
+  const int img = item / a.cout, o = item % a.cout;
+  const uint64_t* kimg = key + (size_t)img * key_stride;
+  const uint64_t* cb = ct + (size_t)item * ct_words<R>(N);
+  const int kb = a.dec_kbits;
+#pragma unroll 1
+  for (int r = 0; r < R; ++r) {
+    const PrimeConst pc = a.pc[r];
+    const Field64 f = pc.f;
+    PhiSrcV src{cb + (size_t)r * N, cb + (size_t)(R + r) * N, kimg + (size_t)(2 * r) * N,
+                kimg + (size_t)(2 * r + 1) * N, f};
+    rns_inverse_head<Field64, uint64_t>(f, a.twq_inv[r], qbuf, tid, src);
+    // last stage (coefficients i, i + n/2) with the CRT constants folded in, then the
+    // accumulator
+    const TwPair<uint64_t> t1{pc.dec_t1, pc.dec_t1_shoup}, ni{pc.dec_ni, pc.dec_ni_shoup};
+#pragma unroll 1
+    for (int i = tid; i < N / 2; i += NT) {
+      uint64_t u = qbuf[sidx<uint64_t>(i)], v = qbuf[sidx<uint64_t>(i + N / 2)];
+      Bfly<Field64, 0>::gs_last(f, u, v, t1, ni);
+      const uint64_t y[2] = {Bfly<Field64, 0>::fin_gs(f, u), Bfly<Field64, 0>::fin_gs(f, v)};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int idx = i + h * (N / 2);
+        uint64_t A = mulhi64_approx(y[h], pc.dec_c);
+        if (r > 0) A += (uint64_t)acc_lo[idx] | ((uint64_t)acc_hi[idx] << 32);
+        if (r < R - 1) {
+          acc_lo[idx] = (uint32_t)A;
+          acc_hi[idx] = (uint16_t)(A >> 32);
+        } else {
+          A += 1ull << (kb - 1);
+          const uint64_t low = A & ((1ull << kb) - 1);
+          uint32_t m;
+          if (low < 16 || low > (1ull << kb) - 16) {
+            m = dec3_exact<LOGN>(a, cb, kimg, idx);
+          } else {
+            m = (uint32_t)(A >> kb);  // < 3p + 1
+            if (m >= 2 * p) m -= 2 * p;
+            if (m >= p) m -= p;
+          }
+          acc_lo[idx] = m;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // decode_slots (NTT_p): m (acc_lo, natural order) -> qbuf's space -> tiles over acc
+  {
+    auto psrc = [&](int i) { return acc_lo[i]; };
+    auto pdst = [&](int j, uint32_t v) {
+      scatter_slot<LOGN, LOGH, LOGW>(S, 0, j, a.pk, TS, reduce_lazy(pf, v, a.pp.cred));
+    };
+    rns_forward<Field32, uint32_t, 1>(pf, a.twp_fwd, pbuf, tid, psrc, pdst);
+  }
+  __syncthreads();
+  for (int pi = 0; pi < a.pk && img * a.pk + pi < a.num_images; ++pi) {  // every image of the pack
+    uint32_t* St = S + pi * TS;
+    tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, St, LS);
+    const size_t base = ((size_t)(img * a.pk + pi) * a.cout + o) * a.oh * a.ow;
+    for (int i = tid; i < a.oh * a.ow; i += NT) {
+      const int r = i / a.ow, c = i % a.ow;
+      const uint32_t s = St[(r + a.r0) * LS + c + a.c0];
+      if (alice_share) alice_share[base + i] = s;
+      if (outp) {
+        uint32_t y = s + bob_share[base + i];
+        outp[base + i] = y >= p ? y - p : y;
+      }
+    }
+  }
+}
+
+}  // namespace ensei_gpu

@@ -154,7 +154,7 @@ static bool dec3_try(const LayerRun& r, const uint64_t* key, uint32_t ks, const 
   if (smem > 113 * 1024) return false;
   auto k = dec3_kernel<LOGL, LOGL>;
   set_smem_shared_sm(k, smem);
-  k<<<items, kRnsThreads, smem, r.st>>>(r.a, key, ks, ct, alice, bob, out);
+  k<<<items, kRnsThreads, smem, r.st>>>(r.a, key, ks, ct, alice, bob, out, 2 * r.ctx->sm_count);
   check_launch("dec3_kernel");
   return true;
 }

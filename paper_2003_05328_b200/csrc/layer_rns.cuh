@@ -303,6 +303,11 @@ struct PhiSrcV {
   }
 };
 
+// L2 prefetch of `bytes` (multiple of 16) from `g` by the calling thread (TMA bulk prefetch)
+EG_DEV void prefetch_l2_bulk(const void* g, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
+}
+
 // The exact decision for one coefficient whose fixed-point CRT sum is ambiguous: the three
 // phi_r by direct evaluation, exact E_r, 192-bit compare (layer.cuh).  Returns m.
 template <int LOGN>
@@ -343,9 +348,9 @@ template <int LOGH, int LOGW>
 __global__ void __launch_bounds__(kRnsThreads, 2)
     dec3_kernel(const __grid_constant__ LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride, const uint64_t* __restrict__ ct,
                 uint32_t* __restrict__ alice_share, const uint32_t* __restrict__ bob_share,
-                uint32_t* __restrict__ outp) {
+                uint32_t* __restrict__ outp, int ahead) {
   constexpr int LOGN = kRnsLogN, N = 1 << LOGN, NT = kRnsThreads, R = 3;
-  constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
+  constexpr int Lw = 1 << LOGW, LS = Lw + 1;
   constexpr int TS = tile_words<LOGH, LOGW>();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
@@ -365,6 +370,17 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
   for (int r = 0; r < R; ++r) {
     const PrimeConst pc = a.pc[r];
     const Field64 f = pc.f;
+    // the first pass reads c0 / c1 straight from HBM with every warp of the CTA waiting on
+    // it: pull the next prime's words (or the first prime's of the tile this SM slot runs
+    // next) into L2 while this prime's passes run
+    if (tid == 0) {
+      const uint64_t* nb = r + 1 < R ? cb : cb + (size_t)ahead * ct_words<R>(N);
+      const int nr = r + 1 < R ? r + 1 : 0;
+      if (r + 1 < R || item + ahead < (int)gridDim.x) {
+        prefetch_l2_bulk(nb + (size_t)nr * N, N * 8);
+        prefetch_l2_bulk(nb + (size_t)(R + nr) * N, N * 8);
+      }
+    }
     PhiSrcV src{cb + (size_t)r * N, cb + (size_t)(R + r) * N, kimg + (size_t)(2 * r) * N,
                 kimg + (size_t)(2 * r + 1) * N, f};
     rns_inverse_head<Field64, uint64_t>(f, a.twq_inv[r], qbuf, tid, src);

@@ -104,6 +104,7 @@ Geo geometry(const ensei_gpu_ctx* c, const ensei_conv_desc* d) {
 
 // RNS tile kernel generation (ensei_gpu_set_tile_variant): 1 = layer_rns.cuh, 0 = layer.cuh
 std::atomic<int> g_tile_gen{1};
+std::atomic<int> g_no_fork{0};  // tuning: HomShare in line instead of forked onto the aux stream
 
 LayerRun make_run(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g, uint32_t num_images,
                   const ensei_randomness* rand, void* stream) {
@@ -344,7 +345,7 @@ void layer_chain(ensei_gpu_ctx* ctx, const ensei_conv_desc* desc, const Geo& g, 
   // so they overlap Alice's encryption; join before the ElementMult consumes them.  In a
   // per-kernel timing pass (ensei_gpu_profile) they run in line, so that every kernel's
   // event span is its own.
-  const bool fork_share = !prof_on();
+  const bool fork_share = !prof_on() && !g_no_fork.load(std::memory_order_relaxed);
   LayerRun ra = r;
   if (fork_share) {
     EG_CUDA(cudaEventRecord(fork, st));
@@ -563,8 +564,9 @@ int ensei_gpu_set_mac_variant(int variant) {
 
 int ensei_gpu_set_tile_variant(int variant) {
   return guarded([&] {
-    require(variant == 0 || variant == 1, ENSEI_ERR_INVALID_ARGUMENT, "variant must be 0 or 1");
-    g_tile_gen.store(variant, std::memory_order_relaxed);
+    require(variant >= 0 && variant <= 3, ENSEI_ERR_INVALID_ARGUMENT, "variant must be 0..3");
+    g_tile_gen.store(variant & 1, std::memory_order_relaxed);
+    g_no_fork.store(variant >> 1, std::memory_order_relaxed);
   });
 }
 

@@ -282,27 +282,6 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
 }
 
 // -------------------------------------------------------------------- Dec
-// phi = c0 t^ + c1 straight from global memory, 16-byte loads (the view of the first
-// INTT pass); reduced to [0, 4q + 2^32) for the Gentleman-Sande bounds.
-struct PhiSrcV {
-  const uint64_t *c0, *c1, *t, *tp;
-  Field64 f;
-  static constexpr bool kVec = true;
-  EG_DEV uint64_t one(uint64_t a, uint64_t b, uint64_t w, uint64_t wp) const {
-    const uint64_t x = f.mul_shoup_approx(a, w, wp) + b;  // < 5q
-    return hi32(x) > hi32(f.q4) ? x - f.q4 : x;
-  }
-  EG_DEV uint64_t operator()(int j) const { return one(c0[j], c1[j], t[j], tp[j]); }
-  EG_DEV void ld2(int j, uint64_t& x, uint64_t& y) const {
-    const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(c0 + j);
-    const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(c1 + j);
-    const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(t + j));
-    const ulonglong2 wp = __ldg(reinterpret_cast<const ulonglong2*>(tp + j));
-    x = one(a.x, b.x, w.x, wp.x);
-    y = one(a.y, b.y, w.y, wp.y);
-  }
-};
-
 // L2 prefetch of `bytes` (multiple of 16) from `g` by the calling thread (TMA bulk prefetch)
 EG_DEV void prefetch_l2_bulk(const void* g, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
@@ -366,14 +345,29 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
   const uint64_t* kimg = key + (size_t)img * key_stride;
   const uint64_t* cb = ct + (size_t)item * ct_words<R>(N);
   const int kb = a.dec_kbits;
+  __shared__ __align__(8) uint64_t c1_bar;
+  if (tid == 0) mbar_init(&c1_bar, 1);
+  __syncthreads();
 #pragma unroll 1
   for (int r = 0; r < R; ++r) {
     const PrimeConst pc = a.pc[r];
     const Field64 f = pc.f;
-    // the first pass reads c0 / c1 straight from HBM with every warp of the CTA waiting on
-    // it: pull the next prime's words (or the first prime's of the tile this SM slot runs
-    // next) into L2 while this prime's passes run
+    // phi = c0 t^ + c1 as a streaming pre-pass: c1 arrives in qbuf by TMA bulk copies (no
+    // registers), c0 / t^ / t^' by 16-byte loads issued two steps ahead of their use; a warp
+    // covers whole 128-byte rows per step (8 lanes x 16 B), reads the row's c1 pairs and
+    // writes phi into the swizzled positions of the same row.  (Fused into the first INTT
+    // pass the loads were serialised behind its butterflies by the 64-register budget:
+    // four exposed L2 / HBM round trips per round, ncu: 46 % long-scoreboard stalls there.)
+    const uint64_t* c0g = cb + (size_t)r * N;
+    const uint64_t* tg = kimg + (size_t)(2 * r) * N;
     if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // qbuf: generic reads/writes -> TMA writes
+      mbar_expect_tx(&c1_bar, N * 8);
+      const uint8_t* c1g = reinterpret_cast<const uint8_t*>(cb + (size_t)(R + r) * N);
+      for (uint32_t off = 0; off < N * 8; off += 32768u)
+        tma_bulk_g2s(reinterpret_cast<uint8_t*>(qbuf) + off, c1g + off, 32768u, &c1_bar);
+      // the next prime's words (or the first prime's of the tile this SM slot runs next)
+      // into L2 while this prime's passes run
       const uint64_t* nb = r + 1 < R ? cb : cb + (size_t)ahead * ct_words<R>(N);
       const int nr = r + 1 < R ? r + 1 : 0;
       if (r + 1 < R || item + ahead < (int)gridDim.x) {
@@ -381,8 +375,32 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
         prefetch_l2_bulk(nb + (size_t)(R + nr) * N, N * 8);
       }
     }
-    PhiSrcV src{cb + (size_t)r * N, cb + (size_t)(R + r) * N, kimg + (size_t)(2 * r) * N,
-                kimg + (size_t)(2 * r + 1) * N, f};
+#pragma unroll 1
+    for (int b = 0; b < N / 2 / NT / 2; ++b) {
+      ulonglong2 A[2], W[2], WP[2], C[2];
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2) {
+        const int j = 2 * ((2 * b + s2) * NT + tid);
+        A[s2] = *reinterpret_cast<const ulonglong2*>(c0g + j);
+        W[s2] = __ldg(reinterpret_cast<const ulonglong2*>(tg + j));
+        WP[s2] = __ldg(reinterpret_cast<const ulonglong2*>(tg + N + j));
+      }
+      if (b == 0) mbar_wait(&c1_bar, (uint32_t)(r & 1));
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2) C[s2] = *reinterpret_cast<const ulonglong2*>(qbuf + 2 * ((2 * b + s2) * NT + tid));
+      __syncwarp();
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2) {
+        const int j = 2 * ((2 * b + s2) * NT + tid);
+        uint64_t x = f.mul_shoup_approx(A[s2].x, W[s2].x, WP[s2].x) + C[s2].x;  // < 5q
+        uint64_t y = f.mul_shoup_approx(A[s2].y, W[s2].y, WP[s2].y) + C[s2].y;
+        x = hi32(x) > hi32(f.q4) ? x - f.q4 : x;  // < 4q + 2^32: the Gentleman-Sande input bound
+        y = hi32(y) > hi32(f.q4) ? y - f.q4 : y;
+        *reinterpret_cast<ulonglong2*>(qbuf + sidx<uint64_t>(j)) = make_ulonglong2(x, y);
+      }
+    }
+    __syncthreads();
+    SmemRW<uint64_t> src{qbuf};
     rns_inverse_head<Field64, uint64_t>(f, a.twq_inv[r], qbuf, tid, src);
     // last stage (coefficients i, i + n/2) with the CRT constants folded in, then the
     // accumulator

@@ -65,6 +65,15 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         res[f"gen{gen}_layer_ms"] = round(e0.elapsed_time(e1) / a.reps, 4)
+        _lib.check(lib.ensei_gpu_set_tile_variant(gen + 2))  # HomShare in line (no fork)
+        L.forward(key, we, x, R, ws=ws)
+        e0.record()
+        for _ in range(a.reps):
+            L.forward(key, we, x, R, ws=ws)
+        e1.record()
+        torch.cuda.synchronize()
+        res[f"gen{gen}_layer_nofork_ms"] = round(e0.elapsed_time(e1) / a.reps, 4)
+    _lib.check(lib.ensei_gpu_set_tile_variant(1))
     names = ("ct_in", "ct_out", "bob", "alice", "out", "fused_alice", "fused_bob")
     res["equal"] = {n: bool(torch.equal(p, q)) for n, p, q in zip(names, out[0], out[1])}
     res["stagewise_vs_fused"] = bool(torch.equal(out[1][3], out[1][5]) and torch.equal(out[1][2], out[1][6]))

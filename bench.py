@@ -52,9 +52,11 @@ METRIC = "oblivious NTT-domain conv/sec (1/2/4/8 B200); NTT modmul/s vs roofline
 C_Q, C_MAC, C_P = 10, 6, 3
 
 
-NCU_KERNELS = {"enc": "tile_enc_kernel", "share": "share_kernel", "mac": "mac_kara_kernel", "dec": "dec_kernel",
-               "dec_rns": "dec_rns_kernel", "planes_tc": "planes_tc_kernel", "mac_tc": "mac_tc_kernel",
-               "mac_out": "mac_out_kernel"}
+# profile name -> kernel names it can stand for (the 3-prime RNS layer runs the second-generation
+# tile kernels enc3 / share3 / dec3, every other shape the first-generation ones)
+NCU_KERNELS = {"enc": ("enc3_kernel", "tile_enc_kernel"), "share": ("share3_kernel", "share_kernel"),
+               "mac": ("mac_kara_kernel",), "dec": ("dec_kernel",), "dec_rns": ("dec3_kernel", "dec_rns_kernel"),
+               "planes_tc": ("planes_tc_kernel",), "mac_tc": ("mac_tc_kernel",), "mac_out": ("mac_out_kernel",)}
 
 
 def ncu_traffic(cfg, name):
@@ -64,9 +66,10 @@ def ncu_traffic(cfg, name):
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_traffic.json")))
     for f in reversed(files):  # the newest round that captured this kernel
-        rec = json.load(open(f)).get(cfg, {}).get(NCU_KERNELS.get(name, name))
-        if rec is not None:
-            return rec["dram_bytes"]
+        recs = json.load(open(f)).get(cfg, {})
+        for k in NCU_KERNELS.get(name, (name,)):
+            if k in recs:
+                return recs[k]["dram_bytes"]
     return None
 
 

@@ -120,7 +120,7 @@ struct ensei_gpu_ctx {
   bool approx_ok = true;  // every 31 q_i < 2^64: approximate-quotient butterflies (MODE 0); the layer path needs it
   uint32_t i8_kmax = 255;  // int8 tensor-core MAC: largest K with K (q_i - 1)^2 < 2^128 for every prime
   bool kara_ok = true;    // every q_i within the Karatsuba MAC's headroom (layer.cuh)
-  // layer_rns.cuh: fraction bits of the packed CRT accumulator (3p 2^k <= 2^48); 0 when the
+  // layer_rns.cuh: fraction bits of the packed CRT accumulator (12p 2^k <= 2^48); 0 when the
   // chain cannot use it (then the first-generation kernels run)
   uint32_t dec_kbits = 0;
   // fork/join helpers: Bob's input-independent HomShare work runs concurrently

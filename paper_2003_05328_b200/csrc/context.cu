@@ -234,10 +234,10 @@ static void ctx_create(int device, uint32_t n, const uint64_t* qs, uint32_t R, u
       }
     }
   }
-  if (R == 3) {  // packed CRT accumulator of layer_rns.cuh: A < 3p 2^k <= 2^48, floor(p 2^(k+64) / q_i) < 2^64
+  if (R == 3) {  // packed CRT accumulator of layer_rns.cuh: A < 12p 2^k <= 2^48, floor(p 2^(k+64) / q_i) < 2^64
     uint32_t k = 48;
-    while (k && (unsigned __int128)(3 * p) << k > ((unsigned __int128)1 << 48)) --k;
-    bool ok = k >= 20;
+    while (k && (unsigned __int128)(12 * p) << k > ((unsigned __int128)1 << 48)) --k;
+    bool ok = k >= 18 && 12 * p + 1 < (1ull << 32);
     for (uint32_t i = 0; i < R && ok; ++i) ok = ((unsigned __int128)p << k) < c->q[i];
     if (ok) {
       c->dec_kbits = k;

@@ -94,6 +94,29 @@ EG_DEV uint64_t uniform_q_from_fast(const Philox4& r, uint64_t q) {
   return hi + (s < lo ? 1 : 0);
 }
 
+// In-place 2D transforms of `nt` tiles (TS words apart) at once: every pass covers the
+// lines of all tiles before its barrier (a 64 x 64 tile is one radix-8 set per thread of a
+// 512-thread CTA: per-tile passes were barrier-latency-bound, ncu: 28 % of HomShare's
+// samples for 12 % of its instructions).  Inverse: values are left in [0, 2p) -- the caller
+// reduces what it crops (kernels.cuh tile_transform_2d spends a whole pass on that).
+template <bool INV, int LOGH, int LOGW>
+EG_DEV void rns_tiles_2d(const Field32& f, uint32_t cred, const TwPair<uint32_t>* twc, uint32_t* S, int LS, int TS,
+                         int nt) {
+  constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW;
+  constexpr int EW = LOGW < 3 ? LOGW : 3, EH = LOGH < 3 ? LOGH : 3;
+  auto rows = [=](int l) { return TileRow{S + (l >> LOGH) * TS, (l & (Lh - 1)) * LS}; };
+  tile_lines_all<INV, LOGW, EW, 0>(f, twc + Lw, rows, nt * Lh);
+  if constexpr (!INV) {
+    auto cols = [=](int l) {
+      return ReduceOnStore<TileCol>{TileCol{S + (l >> LOGW) * TS, l & (Lw - 1), LS}, f, cred};
+    };
+    tile_lines_all<INV, LOGH, EH, 0>(f, twc + Lh, cols, nt * Lw);
+  } else {
+    auto cols = [=](int l) { return TileCol{S + (l >> LOGW) * TS, l & (Lw - 1), LS}; };
+    tile_lines_all<INV, LOGH, EH, 0>(f, twc + Lh, cols, nt * Lw);
+  }
+}
+
 // -------------------------------------------------------------------- Enc
 // shared: [ qbuf n u64 | pbuf n u32 (padded) | noise n int8 ]; the pk DFT2D tiles alias
 // qbuf (dead once encode_slots' first pass has gathered them).
@@ -147,7 +170,7 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
   }
   __syncthreads();
   // 2. DFT2D of each tile
-  for (int pi = 0; pi < npk; ++pi) tile_transform_2d<false, LOGH, LOGW>(pf, a.pp.cred, a.twc_fwd, S + pi * TS, LS);
+  rns_tiles_2d<false, LOGH, LOGW>(pf, a.pp.cred, a.twc_fwd, S, LS, TS, npk);
   // 3. encode_slots: INTT_p of the slots gathered from the tiles
   {
     auto src = [&](int j) { return gather_slot<LOGN, LOGH, LOGW>(S, 0, j, a.pk, TS); };
@@ -229,19 +252,27 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
     }
   }
   // 2. Bob's share of every image of the pack: crop(IDFT2D(its part of the s_B grid))
-  // (REF protocol.cpp:593-602)
-  for (int pi = 0; pi < a.pk && img * a.pk + pi < a.num_images; ++pi) {
-    __syncthreads();
-    for (int i = tid; i < Lh * Lw; i += NT) {
-      const int r = i >> LOGW, c = i & (Lw - 1);
-      S[brev(r, LOGH) * LS + brev(c, LOGW)] = pbuf[sidx<uint32_t>(brev(pi * Lh * Lw + i, LOGN))];
-    }
-    __syncthreads();
-    tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, S, LS);
-    uint32_t* bs = bob_share + ((size_t)(img * a.pk + pi) * a.cout + o) * a.oh * a.ow;
-    for (int i = tid; i < a.oh * a.ow; i += NT) {
-      const int r = i / a.ow, c = i % a.ow;
-      bs[i] = S[(r + a.r0) * LS + c + a.c0];
+  // (REF protocol.cpp:593-602); as many tiles at once as fit in qbuf's space
+  {
+    constexpr int TS = tile_words<LOGH, LOGW>();
+    constexpr int TB = (int)(((size_t)N * 8) / ((size_t)TS * 4));  // tiles per batch
+    const int npi = min(a.pk, a.num_images - img * a.pk);
+    for (int p0 = 0; p0 < npi; p0 += TB) {
+      const int nb = min(TB, npi - p0);
+      __syncthreads();
+      for (int e = tid; e < nb * Lh * Lw; e += NT) {
+        const int pi = e >> (LOGH + LOGW), i = e & (Lh * Lw - 1);
+        const int r = i >> LOGW, c = i & (Lw - 1);
+        S[pi * TS + brev(r, LOGH) * LS + brev(c, LOGW)] = pbuf[sidx<uint32_t>(brev((p0 + pi) * Lh * Lw + i, LOGN))];
+      }
+      __syncthreads();
+      rns_tiles_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, S, LS, TS, nb);
+      for (int e = tid; e < nb * a.oh * a.ow; e += NT) {
+        const int pi = e / (a.oh * a.ow), i = e % (a.oh * a.ow);
+        const int r = i / a.ow, c = i % a.ow;
+        bob_share[((size_t)(img * a.pk + p0 + pi) * a.cout + o) * a.oh * a.ow + i] =
+            pf.reduce_once(S[pi * TS + (r + a.r0) * LS + c + a.c0]);
+      }
     }
   }
   __syncthreads();
@@ -311,10 +342,11 @@ __device__ __noinline__ uint32_t dec3_exact(const LayerArgs& a, const uint64_t* 
 }
 
 // shared: [ qbuf n u64 | acc_lo n u32 | acc_hi n u16 ]: the CRT accumulator
-// A = sum_r floor(y_r p 2^k / q_r) (y_r = phi_r (Q/q_r)^-1 mod q_r, k = dec_kbits fraction
-// bits, A < 3p 2^k < 2^48) per coefficient; m = floor((A + 2^(k-1)) / 2^k) mod p unless the
-// low bits sit within 16 of a multiple of 2^k (each term is at most 3.1 below its exact
-// value), where dec3_exact decides.  y_r comes out of the INTT itself: (Q/q_r)^-1 is folded
+// A = sum_r floor(y_r p 2^k / q_r) (y_r = phi_r (Q/q_r)^-1 mod q_r as the lazy value in
+// [0, 4 q_r) the transform leaves, k = dec_kbits fraction bits, A < 12p 2^k <= 2^48) per
+// coefficient; m = floor((A + 2^(k-1)) / 2^k) mod p unless the low bits sit within 16 of a
+// multiple of 2^k (each term is at most 3.3 below its exact value), where dec3_exact
+// decides.  y_r comes out of the INTT itself: (Q/q_r)^-1 is folded
 // into the n^-1 constants of its last stage (PrimeConst::dec_*).  m overwrites acc_lo, the
 // p-side transform then runs in qbuf's space and scatters into the tiles (over acc).
 template <int LOGH, int LOGW>
@@ -409,7 +441,8 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
     for (int i = tid; i < N / 2; i += NT) {
       uint64_t u = qbuf[sidx<uint64_t>(i)], v = qbuf[sidx<uint64_t>(i + N / 2)];
       Bfly<Field64, 0>::gs_last(f, u, v, t1, ni);
-      const uint64_t y[2] = {Bfly<Field64, 0>::fin_gs(f, u), Bfly<Field64, 0>::fin_gs(f, v)};
+      // lazy y = y_r + j q_r (j <= 3) only adds j p to the integer part of its term
+      const uint64_t y[2] = {u, v};
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int idx = i + h * (N / 2);
@@ -422,13 +455,8 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
           A += 1ull << (kb - 1);
           const uint64_t low = A & ((1ull << kb) - 1);
           uint32_t m;
-          if (low < 16 || low > (1ull << kb) - 16) {
-            m = dec3_exact<LOGN>(a, cb, kimg, idx);
-          } else {
-            m = (uint32_t)(A >> kb);  // < 3p + 1
-            if (m >= 2 * p) m -= 2 * p;
-            if (m >= p) m -= p;
-          }
+          if (low < 16 || low > (1ull << kb) - 16) m = dec3_exact<LOGN>(a, cb, kimg, idx);
+          else m = reduce_lazy(pf, (uint32_t)(A >> kb), a.pp.cred);  // A >> kb <= 12p
           acc_lo[idx] = m;
         }
       }
@@ -444,17 +472,18 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
     rns_forward<Field32, uint32_t, 1>(pf, a.twp_fwd, pbuf, tid, psrc, pdst);
   }
   __syncthreads();
-  for (int pi = 0; pi < a.pk && img * a.pk + pi < a.num_images; ++pi) {  // every image of the pack
-    uint32_t* St = S + pi * TS;
-    tile_transform_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, St, LS);
-    const size_t base = ((size_t)(img * a.pk + pi) * a.cout + o) * a.oh * a.ow;
-    for (int i = tid; i < a.oh * a.ow; i += NT) {
+  {  // IDFT2D of every image of the pack at once, crop (+ recombine)
+    const int npi = min(a.pk, a.num_images - img * a.pk);
+    rns_tiles_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, S, LS, TS, npi);
+    for (int e = tid; e < npi * a.oh * a.ow; e += NT) {
+      const int pi = e / (a.oh * a.ow), i = e % (a.oh * a.ow);
       const int r = i / a.ow, c = i % a.ow;
-      const uint32_t s = St[(r + a.r0) * LS + c + a.c0];
-      if (alice_share) alice_share[base + i] = s;
+      const uint32_t s = pf.reduce_once(S[pi * TS + (r + a.r0) * LS + c + a.c0]);
+      const size_t at = ((size_t)(img * a.pk + pi) * a.cout + o) * a.oh * a.ow + i;
+      if (alice_share) alice_share[at] = s;
       if (outp) {
-        uint32_t y = s + bob_share[base + i];
-        outp[base + i] = y >= p ? y - p : y;
+        const uint32_t y = s + bob_share[at];
+        outp[at] = y >= p ? y - p : y;
       }
     }
   }

@@ -52,7 +52,9 @@ EG_DEV void rns_forward(const F& f, const TwPair<T>* __restrict__ tw, T* sm, int
   rns_pass<F, T, 2, false, SmemRW<T>, SmemRW<T>, FB::corr(2)>(f, tw, tid, s, s, cred);
   __syncthreads();
   rns_pass<F, T, 3, false, SmemRW<T>, SmemRW<T>, FB::corr(3)>(f, tw, tid, s, s, cred);
-  __syncthreads();
+  // passes 3 and 4 (stages 7..12) work inside 64-element blocks owned by the same 8 lanes
+  // of a warp in both passes and both rounds: a warp barrier is enough
+  __syncwarp();
   rns_pass<F, T, 4, false, SmemRW<T>, Dst, FB::corr(4)>(f, tw, tid, s, dst, cred);
 }
 
@@ -61,7 +63,7 @@ template <class F, class T, class Src>
 EG_DEV void rns_inverse_head(const F& f, const TwPair<T>* __restrict__ tw, T* sm, int tid, Src src) {
   SmemRW<T> s{sm};
   rns_pass<F, T, 4, true, Src, SmemRW<T>>(f, tw, tid, src, s);
-  __syncthreads();
+  __syncwarp();  // passes 4 and 3 share their 64-element blocks within a warp (see rns_forward)
   rns_pass<F, T, 3, true, SmemRW<T>, SmemRW<T>>(f, tw, tid, s, s);
   __syncthreads();
   rns_pass<F, T, 2, true, SmemRW<T>, SmemRW<T>>(f, tw, tid, s, s);
@@ -81,6 +83,15 @@ EG_DEV void rns_inverse(const F& f, const TwPair<T>* __restrict__ tw, T* sm, int
 EG_DEV uint64_t mulhi64_approx(uint64_t x, uint64_t c) {
   const uint32_t x0 = lo32(x), x1 = hi32(x), c0 = lo32(c), c1 = hi32(c);
   return mulw(x1, c1) + hi32(mulw(x0, c1)) + hi32(mulw(x1, c0));
+}
+
+// x w mod q in [0, 4q) for a small x < 2^32 (the lifts Delta m): Q' = hi32(x w1') drops
+// x w0' / 2^64 < 1, so Q - Q' <= 2; 3 wide + 2 plain IMADs instead of 5 + 4.
+EG_DEV uint64_t mul_shoup_small(const Field64& f, uint32_t x, uint64_t w, uint64_t wp) {
+  const uint32_t Q = hi32(mulw(x, hi32(wp)));
+  const uint64_t a = mulw(x, lo32(w)) + ((uint64_t)(x * hi32(w)) << 32);
+  const uint64_t b = mulw(Q, lo32(f.q)) + ((uint64_t)(Q * hi32(f.q)) << 32);
+  return a - b;
 }
 
 // uniform mod q from 128 bits, floor(x q / 2^128), exact (= philox.cuh uniform_q_from) from
@@ -187,7 +198,7 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
     const Field64 f = pc.f;
     // 4. Delta m + e, lazy in [0, 3q)
     auto src = [&](int i) -> uint64_t {
-      uint64_t x = f.mul_shoup_approx(pbuf[sidx<uint32_t>(i)], pc.delta, pc.delta_shoup);  // < 4q
+      uint64_t x = mul_shoup_small(f, pbuf[sidx<uint32_t>(i)], pc.delta, pc.delta_shoup);  // < 4q
       if (x >= f.q2) x -= f.q2;
       return x + signed_mod(ebuf[i], f.q);
     };
@@ -286,7 +297,7 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
     auto dst = [&](int i, uint32_t v) { praw(i, Bfly<Field32, 0>::fin_gs(pf, v)); };
     // the first pass negates on load: same positions loaded and stored per virtual thread
     rns_pass<Field32, uint32_t, 4, true>(pf, a.twp_inv, tid, src, praw);
-    __syncthreads();
+    __syncwarp();
     rns_pass<Field32, uint32_t, 3, true>(pf, a.twp_inv, tid, praw, praw);
     __syncthreads();
     rns_pass<Field32, uint32_t, 2, true>(pf, a.twp_inv, tid, praw, praw);
@@ -302,7 +313,7 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
     const PrimeConst pc = a.pc[r];
     const Field64 f = pc.f;
     auto qsrc = [&](int i) {
-      const uint64_t x = f.mul_shoup_approx(pbuf[sidx<uint32_t>(i)], pc.delta, pc.delta_shoup);  // < 4q
+      const uint64_t x = mul_shoup_small(f, pbuf[sidx<uint32_t>(i)], pc.delta, pc.delta_shoup);  // < 4q
       return x >= f.q2 ? x - f.q2 : x;
     };
     uint64_t* mo = mask + (size_t)item * ct_words<R>(N) + (size_t)(R + r) * N;

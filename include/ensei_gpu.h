@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define ENSEI_GPU_ABI_VERSION 2
+#define ENSEI_GPU_ABI_VERSION 3
 
 typedef enum {
   ENSEI_OK = 0,
@@ -123,6 +123,17 @@ typedef struct {
    * ceil(num_images / k) "ciphertext images"; image arrays stay per image.  Packed layers
    * take Philox randomness with a pack-aligned image_base and one shared key. */
   uint32_t pack;
+  /* Padded grid side (builder extension, ABI 3; 0 = REF's choice, choose_padded_len: the
+   * next power of two).  REF pads H + fh - 1 to a power of two for its own radix-2
+   * transform; any length L >= max(H + fh - 1, W + fw - 1) dividing p - 1 holds the linear
+   * convolution (REF itself falls back to such lengths, with its O(L^2) ntt_direct, when no
+   * power of two divides p - 1: ntt.cpp:51-61).  A non-power-of-two grid runs the direct
+   * transform on the device too and lets more images share a block (32x32 images, 3x3
+   * filter, p - 1 = 2^14 39: L = 39, five images per n = 8192 block instead of two).
+   * Outputs are REF's; ciphertexts are the oracle's restatement with the same grid.
+   * Supported for the 3-prime RNS layer at n = 8192 (one layer: no HomRec), any pack with
+   * pack L^2 <= n. */
+  uint32_t grid;
 } ensei_conv_desc;
 
 typedef struct {

@@ -333,10 +333,22 @@ def rns_delta(qs, p):
     return [((Q - 1) // p) % q for q in qs]
 
 
-def rns_layers(qs, p, n, H, W, fh, fw, same, cin, cout, pack=1):
+def set_grid(L, grid):
+    """Grid override (the device's ensei_conv_desc::grid): a padded side that holds the
+    linear convolution and divides p - 1, like the lengths REF's choose_padded_len falls
+    back to (ntt.cpp:51-61); the C restatement's transforms take any such length (direct
+    O(L^2) path, REF ntt.cpp:35-49)."""
+    if grid:
+        assert grid >= L.H + L.fh - 1 and grid >= L.W + L.fw - 1 and (L.p - 1) % grid == 0
+        L.Lh = L.Lw = grid
+        L.blocks = -(-grid * grid // L.n)
+    return L
+
+
+def rns_layers(qs, p, n, H, W, fh, fw, same, cin, cout, pack=1, grid=0):
     Ls = []
     for q, d in zip(qs, rns_delta(qs, p)):
-        L = layer(q, p, n, H, W, fh, fw, same, cin, cout)
+        L = set_grid(layer(q, p, n, H, W, fh, fw, same, cin, cout), grid)
         L.delta = d
         L.pack = pack
         Ls.append(L)

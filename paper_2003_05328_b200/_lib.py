@@ -46,7 +46,8 @@ class CtxInfo(C.Structure):
 
 class ConvDesc(C.Structure):
     _fields_ = [("H", C.c_uint32), ("W", C.c_uint32), ("fh", C.c_uint32), ("fw", C.c_uint32),
-                ("same", C.c_uint32), ("cin", C.c_uint32), ("cout", C.c_uint32), ("pack", C.c_uint32)]
+                ("same", C.c_uint32), ("cin", C.c_uint32), ("cout", C.c_uint32), ("pack", C.c_uint32),
+                ("grid", C.c_uint32)]
 
 
 class LayerGeom(C.Structure):

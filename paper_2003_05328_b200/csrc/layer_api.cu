@@ -6,6 +6,7 @@
 #include <cstring>
 #include <string>
 
+#include "host_field.hpp"
 #include "layer_launch.cuh"
 
 namespace ensei_gpu {
@@ -58,6 +59,7 @@ int guarded(Fn&& fn) {
 struct Geo {
   uint32_t Lh, Lw, logL, B, oh, ow, r0, c0, G;
   uint32_t pk = 1;  // images per ciphertext block
+  uint32_t gridL = 0;  // grid override in force (a non-power-of-two side), else 0
   uint32_t cts(uint32_t imgs) const { return (imgs + pk - 1) / pk; }
 };
 
@@ -81,8 +83,17 @@ Geo geometry(const ensei_gpu_ctx* c, const ensei_conv_desc* d) {
     fail(ENSEI_ERR_UNSUPPORTED, "non-power-of-two transform length (REF direct O(L^2) path) not on the GPU path");
   };
   Geo g;
-  g.Lh = padded(d->H + d->fh - 1);
-  g.Lw = padded(d->W + d->fw - 1);
+  if (d->grid && (d->grid & (d->grid - 1))) {
+    // grid override (builder extension): any side holding the linear convolution that
+    // divides p - 1, as REF's own fallback lengths do (choose_padded_len, ntt.cpp:51-61)
+    require(d->grid >= d->H + d->fh - 1 && d->grid >= d->W + d->fw - 1, ENSEI_ERR_BAD_GEOMETRY,
+            "grid override smaller than the linear convolution");
+    require((c->p - 1) % d->grid == 0, ENSEI_ERR_BAD_GEOMETRY, "grid override must divide p - 1");
+    g.Lh = g.Lw = g.gridL = d->grid;
+  } else {
+    g.Lh = padded(d->grid ? std::max(d->grid, d->H + d->fh - 1) : d->H + d->fh - 1);
+    g.Lw = padded(d->grid ? std::max(d->grid, d->W + d->fw - 1) : d->W + d->fw - 1);
+  }
   require(g.Lh == g.Lw, ENSEI_ERR_UNSUPPORTED, "rectangular padded grids are not on the GPU path");
   require(g.Lh <= (uint32_t)kMaxTile && g.Lh >= 2, ENSEI_ERR_UNSUPPORTED, "padded grid side must be in [2, 64]");
   g.logL = ilog2u(g.Lh);
@@ -93,7 +104,8 @@ Geo geometry(const ensei_gpu_ctx* c, const ensei_conv_desc* d) {
   if (g.pk > 1) {
     require(g.B == 1 && (uint64_t)g.pk * g.G <= c->n, ENSEI_ERR_BAD_GEOMETRY,
             "packing needs pack * padded grid <= n (one block per channel)");
-    require((g.pk & (g.pk - 1)) == 0, ENSEI_ERR_UNSUPPORTED, "pack must be a power of two");
+    require(g.gridL || (g.pk & (g.pk - 1)) == 0, ENSEI_ERR_UNSUPPORTED,
+            "pack must be a power of two (any pack with a grid override)");
   }
   g.oh = d->same ? d->H : d->H - d->fh + 1;
   g.ow = d->same ? d->W : d->W - d->fw + 1;
@@ -117,6 +129,7 @@ LayerRun make_run(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g
   r.R = (int)c->R;
   r.st = (cudaStream_t)stream;
   r.tile_gen = g_tile_gen.load(std::memory_order_relaxed);
+  r.gridL = (int)g.gridL;
   LayerArgs& a = r.a;
   std::memset(&a, 0, sizeof(a));
   a.H = d->H;
@@ -144,6 +157,12 @@ LayerRun make_run(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g
   }
   a.crt = c->crt;
   a.dec_kbits = (int)c->dec_kbits;
+  if (g.gridL) {
+    const uint64_t w = host::root_of_unity(g.gridL, c->p);
+    a.grid_w = (uint32_t)w;
+    a.grid_winv = (uint32_t)host::invmod(w, c->p);
+    a.grid_linv = (uint32_t)host::invmod(g.gridL % c->p, c->p);
+  }
   a.pp = c->pp;
   a.twp_fwd = c->tab.tw_p_fwd;
   a.twp_inv = c->tab.tw_p_inv;

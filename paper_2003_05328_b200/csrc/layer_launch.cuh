@@ -12,6 +12,7 @@ struct LayerRun {
   int logL;  // square padded grid, log2 side
   int R;
   cudaStream_t st;
+  int gridL = 0;     // grid override (ensei_conv_desc::grid): the non-power-of-two side, else 0
   int tile_gen = 1;  // RNS tile kernels: 1 = layer_rns.cuh (512 threads, two CTAs per SM), 0 = layer.cuh
 };
 
@@ -122,52 +123,78 @@ static void enc_dispatch_r(const LayerRun& r, int tm, bool inj, int in_t, const 
   fail(ENSEI_ERR_UNSUPPORTED, "padded grid side must be a power of two <= 64 on this path");
 }
 
-// ---- second-generation RNS tile kernels (layer_rns.cuh): n = 8192, 3 primes, 32x32 / 64x64 grids ----
-template <int LOGL, int IN_T>
+// ---- second-generation RNS tile kernels (layer_rns.cuh): n = 8192, 3 primes; 32x32 / 64x64
+// grids (REF's geometry) or a grid override (ensei_conv_desc::grid, direct transform) ----
+template <class GR, int IN_T>
 static void enc3_go(const LayerRun& r, const uint64_t* key, uint32_t ks, const void* in, uint64_t* out, int items) {
-  auto k = enc3_kernel<LOGL, LOGL, IN_T>;
-  constexpr size_t smem = enc3_smem<LOGL, LOGL>();
+  auto k = enc3_kernel<GR, IN_T>;
+  constexpr size_t smem = enc3_smem();
   set_smem_shared_sm(k, smem);
   k<<<items, kRnsThreads, smem, r.st>>>(r.a, key, ks, in, out);
   check_launch("enc3_kernel");
 }
-template <int LOGL>
+template <class GR>
 static bool enc3_try(const LayerRun& r, int in_t, const uint64_t* key, uint32_t ks, const void* in, uint64_t* out,
                      int items) {
-  if ((size_t)r.a.pk * tile_words<LOGL, LOGL>() * 4 > (size_t)(1 << kRnsLogN) * 8) return false;  // tiles alias qbuf
-  if (in_t == ENSEI_IN_U8) enc3_go<LOGL, ENSEI_IN_U8>(r, key, ks, in, out, items);
-  else enc3_go<LOGL, ENSEI_IN_U32>(r, key, ks, in, out, items);
+  if (grid_tile_bytes<GR>(r.a.pk) > (size_t)(1 << kRnsLogN) * 8) return false;  // tiles alias qbuf
+  if (in_t == ENSEI_IN_U8) enc3_go<GR, ENSEI_IN_U8>(r, key, ks, in, out, items);
+  else enc3_go<GR, ENSEI_IN_U32>(r, key, ks, in, out, items);
   return true;
 }
-template <int LOGL>
+template <class GR>
 static void share3_go(const LayerRun& r, uint64_t* mask, uint32_t* bob_share, int items) {
-  auto k = share3_kernel<LOGL, LOGL>;
+  auto k = share3_kernel<GR>;
   constexpr size_t smem = share3_smem();
   set_smem_shared_sm(k, smem);
   k<<<items, kRnsThreads, smem, r.st>>>(r.a, mask, bob_share);
   check_launch("share3_kernel");
 }
-template <int LOGL>
+template <class GR>
 static bool dec3_try(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint64_t* ct, uint32_t* alice,
                      const uint32_t* bob, uint32_t* out, int items) {
-  const size_t smem = dec3_smem<LOGL, LOGL>(r.a.pk);
-  if (smem > 113 * 1024) return false;
-  auto k = dec3_kernel<LOGL, LOGL>;
+  const size_t smem = dec3_smem<GR>(r.a.pk);
+  if (smem > 113 * 1024 || grid_tile_bytes<GR>(r.a.pk) / (GR::kScratch ? 2 : 1) > (size_t)(1 << kRnsLogN) * 8)
+    return false;
+  auto k = dec3_kernel<GR>;
   set_smem_shared_sm(k, smem);
   k<<<items, kRnsThreads, smem, r.st>>>(r.a, key, ks, ct, alice, bob, out, 2 * r.ctx->sm_count);
   check_launch("dec3_kernel");
   return true;
+}
+template <class GR>
+static void weights3_go(const LayerRun& r, const int32_t* w, uint64_t* out, int items) {
+  auto k = weights3_kernel<GR>;
+  constexpr size_t smem = enc3_smem();
+  set_smem_shared_sm(k, smem);
+  k<<<items, kRnsThreads, smem, r.st>>>(r.a, w, out);
+  check_launch("weights3_kernel");
+}
+// grid override: the side lengths compiled in (p - 1 = 2^14 39 for the default p: 39 holds a
+// 32x32 image with a filter up to 8x8)
+inline bool grid_supported(int L) { return L == 39; }
+[[noreturn]] inline void grid_fail() {
+  fail(ENSEI_ERR_UNSUPPORTED,
+       "grid override: 3-prime RNS layers at n = 8192 with grid = 39, Philox randomness, no HomRec, pack 39^2 <= n");
 }
 
 template <int LOGN>
 void launch_tile(const LayerRun& r, int tm, bool inj, int in_t, const uint64_t* key, uint32_t ks, const void* in,
                  uint64_t* out, int items) {
   if (items == 0) return;
+  if (r.gridL) {  // grid override: second-generation kernels only
+    if constexpr (LOGN == 13) {
+      if (r.R == 3 && !inj && r.gridL == 39) {
+        if (tm == TILE_WEIGHTS) return weights3_go<GridDirect<39>>(r, static_cast<const int32_t*>(in), out, items);
+        if (tm == TILE_ENC && enc3_try<GridDirect<39>>(r, in_t, key, ks, in, out, items)) return;
+      }
+    }
+    grid_fail();
+  }
   if (r.R == 1) return enc_dispatch_r<LOGN, 1>(r, tm, inj, in_t, key, ks, in, out, items);
   if constexpr (LOGN == 13) {
     if (r.R == 3 && r.tile_gen && tm == TILE_ENC && !inj) {
-      if (r.logL == 6 && enc3_try<6>(r, in_t, key, ks, in, out, items)) return;
-      if (r.logL == 5 && enc3_try<5>(r, in_t, key, ks, in, out, items)) return;
+      if (r.logL == 6 && enc3_try<GridPow2<6>>(r, in_t, key, ks, in, out, items)) return;
+      if (r.logL == 5 && enc3_try<GridPow2<5>>(r, in_t, key, ks, in, out, items)) return;
     }
     if (r.R == 3) return enc_dispatch_r<LOGN, 3>(r, tm, inj, in_t, key, ks, in, out, items);
   }
@@ -220,14 +247,20 @@ static void share_dispatch(const LayerRun& r, uint64_t* m, uint32_t* bs, int ite
 template <int LOGN>
 void launch_share(const LayerRun& r, bool inj, uint64_t* mask, uint32_t* bob_share, int items) {
   if (items == 0) return;
+  if (r.gridL) {
+    if constexpr (LOGN == 13) {
+      if (r.R == 3 && !inj && r.gridL == 39) return share3_go<GridDirect<39>>(r, mask, bob_share, items);
+    }
+    grid_fail();
+  }
   if (r.R == 1) {
     if (inj) return share_dispatch<LOGN, 1, true>(r, mask, bob_share, items);
     return share_dispatch<LOGN, 1, false>(r, mask, bob_share, items);
   }
   if constexpr (LOGN == 13) {
     if (r.R == 3 && !inj && r.tile_gen) {
-      if (r.logL == 6) return share3_go<6>(r, mask, bob_share, items);
-      if (r.logL == 5) return share3_go<5>(r, mask, bob_share, items);
+      if (r.logL == 6) return share3_go<GridPow2<6>>(r, mask, bob_share, items);
+      if (r.logL == 5) return share3_go<GridPow2<5>>(r, mask, bob_share, items);
     }
     if (r.R == 3 && !inj) return share_dispatch<LOGN, 3, false>(r, mask, bob_share, items);
   }
@@ -281,11 +314,19 @@ template <int LOGN>
 void launch_dec(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint64_t* ct, uint32_t* alice,
                 const uint32_t* bob, uint32_t* out, int items) {
   if (items == 0) return;
+  if (r.gridL) {
+    if constexpr (LOGN == 13) {
+      if (r.R == 3 && r.a.dec_kbits && r.gridL == 39 &&
+          dec3_try<GridDirect<39>>(r, key, ks, ct, alice, bob, out, items))
+        return;
+    }
+    grid_fail();
+  }
   if (r.R != 1) {
     if constexpr (LOGN == 13) {
       if (r.R == 3 && r.tile_gen && r.a.dec_kbits) {
-        if (r.logL == 6 && dec3_try<6>(r, key, ks, ct, alice, bob, out, items)) return;
-        if (r.logL == 5 && dec3_try<5>(r, key, ks, ct, alice, bob, out, items)) return;
+        if (r.logL == 6 && dec3_try<GridPow2<6>>(r, key, ks, ct, alice, bob, out, items)) return;
+        if (r.logL == 5 && dec3_try<GridPow2<5>>(r, key, ks, ct, alice, bob, out, items)) return;
       }
       if (r.R == 3) {
         switch (r.logL) {

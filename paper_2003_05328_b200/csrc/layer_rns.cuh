@@ -128,22 +128,113 @@ EG_DEV void rns_tiles_2d(const Field32& f, uint32_t cred, const TwPair<uint32_t>
   }
 }
 
+// ------------------------------------------------------------ padded-grid policies
+// The tile side of a layer: how its DFT2D / IDFT2D run in shared memory and where the
+// frequency (r, c) of a transformed tile lives.
+//   GridPow2<LOG>  REF's choice (next power of two): radix-8 passes, frequencies in
+//                  bit-reversed positions (kernels.cuh conventions).
+//   GridDirect<L>  any L dividing p - 1 (ensei_conv_desc::grid): the O(L^2) transform REF
+//                  itself runs for such lengths (ntt_direct, ntt.cpp:35-49), rows from S into
+//                  a scratch buffer of the same size and columns back; natural order
+//                  throughout; L^-1 per dimension folded into the inverse root table.
+template <int LOG>
+struct GridPow2 {
+  static constexpr int L = 1 << LOG, LS = L + 1, G = L * L;
+  static constexpr int TS = tile_words<LOG, LOG>();
+  static constexpr bool kScratch = false;
+  EG_DEV static int px(int r, int c) { return r * LS + c; }                        // pixel (r, c)
+  EG_DEV static int fq(int r, int c) { return brev(r, LOG) * LS + brev(c, LOG); }  // frequency (r, c)
+  EG_DEV static void split(int flat, int& pi, int& r, int& c) {  // natural slot -> (image of the pack, r, c)
+    pi = flat >> (2 * LOG);
+    r = (flat >> LOG) & (L - 1);
+    c = flat & (L - 1);
+  }
+  template <bool INV>
+  EG_DEV static void transform(const LayerArgs& a, uint32_t* S, uint32_t*, int nt) {
+    rns_tiles_2d<INV, LOG, LOG>(a.pp.f, a.pp.cred, INV ? a.twc_inv : a.twc_fwd, S, LS, TS, nt);
+  }
+};
+
+template <int L_>
+struct GridDirect {
+  static constexpr int L = L_, LS = (L_ & 1) ? L_ : L_ + 1, G = L_ * L_;  // odd row stride: conflict-free columns
+  static constexpr int TS = (int)((((size_t)L_ * LS * 4 + 127) & ~(size_t)127) / 4);
+  static constexpr bool kScratch = true;
+  EG_DEV static int px(int r, int c) { return r * LS + c; }
+  EG_DEV static int fq(int r, int c) { return r * LS + c; }
+  EG_DEV static void split(int flat, int& pi, int& r, int& c) {
+    pi = flat / G;
+    const int rem = flat - pi * G;
+    r = rem / L;
+    c = rem - r * L;
+  }
+  // one dimension: out[line][k] = sum_i in[line][i] W[(i k) mod L], 64-bit lazy sums
+  // (L 2^32 2^20 < 2^64), one reduction per output; a warp covers consecutive k of a line
+  // (broadcast reads of the line).  Outputs canonical (inverse: the caller's reduce_once
+  // is then the identity).
+  template <bool COLS>
+  EG_DEV static void lines(const PConst& pp, const uint32_t* W, const uint32_t* in, uint32_t* out, int nt) {
+    for (int o = threadIdx.x; o < nt * G; o += blockDim.x) {
+      const int t = o / G, rem = o - t * G, ln = rem / L, k = rem - ln * L;
+      const uint32_t* x = in + t * TS + (COLS ? ln : ln * LS);
+      uint64_t acc = 0;
+      int idx = 0;
+#pragma unroll 13
+      for (int i = 0; i < L; ++i) {
+        acc = madw(x[COLS ? i * LS : i], W[idx], acc);
+        idx += k;
+        if (idx >= L) idx -= L;
+      }
+      const uint64_t qt = mulhi64(acc, pp.m64);
+      out[t * TS + (COLS ? k * LS + ln : ln * LS + k)] = pp.f.reduce_once((uint32_t)(acc - qt * pp.f.q));
+    }
+  }
+  template <bool INV>
+  EG_DEV static void transform(const LayerArgs& a, uint32_t* S, uint32_t* scratch, int nt) {
+    __shared__ uint32_t W[L_];
+    if (threadIdx.x < L) {  // W[i] = w^i (inverse: w^-i / L)
+      uint32_t b = INV ? a.grid_winv : a.grid_w, r = INV ? a.grid_linv : 1u;
+      for (int e = threadIdx.x; e; e >>= 1) {
+        if (e & 1) r = a.pp.f.mul(r, b, a.pp.m64);
+        b = a.pp.f.mul(b, b, a.pp.m64);
+      }
+      W[threadIdx.x] = r;
+    }
+    __syncthreads();
+    lines<false>(a.pp, W, S, scratch, nt);
+    __syncthreads();
+    lines<true>(a.pp, W, scratch, S, nt);
+    __syncthreads();
+  }
+};
+
 // -------------------------------------------------------------------- Enc
 // shared: [ qbuf n u64 | pbuf n u32 (padded) | noise n int8 ]; the pk DFT2D tiles alias
 // qbuf (dead once encode_slots' first pass has gathered them).
-template <int LOGH, int LOGW>
 constexpr size_t enc3_smem() {
   return (size_t)(1 << kRnsLogN) * 8 + ssize<uint32_t>(1 << kRnsLogN) * 4 + (1 << kRnsLogN);
 }
+// tiles (and the direct transform's scratch copy) that must fit in qbuf's space
+template <class GR>
+constexpr size_t grid_tile_bytes(int nt) {
+  return (size_t)nt * GR::TS * 4 * (GR::kScratch ? 2 : 1);
+}
 
-template <int LOGH, int LOGW, int IN_T>
+// slot value at ring position j (natural slot brev(j)); 0 past the packed grids.  TILE0:
+// every pack position reads tile 0 (prepared weights, replicated across the pack)
+template <class GR, bool TILE0 = false>
+EG_DEV uint32_t grid_gather(const uint32_t* S, int j, int pk) {
+  int pi, r, c;
+  GR::split(brev(j, kRnsLogN), pi, r, c);
+  return pi >= pk ? 0u : S[(TILE0 ? 0 : pi) * GR::TS + GR::fq(r, c)];
+}
+
+template <class GR, int IN_T>
 __global__ void __launch_bounds__(kRnsThreads, 2)
-    enc3_kernel(LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride, const void* __restrict__ in,
-                uint64_t* __restrict__ out) {
+    enc3_kernel(const __grid_constant__ LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride,
+                const void* __restrict__ in, uint64_t* __restrict__ out) {
   constexpr int LOGN = kRnsLogN, N = 1 << LOGN, NT = kRnsThreads, R = 3;
-  constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
-  constexpr int TS = tile_words<LOGH, LOGW>();
-  static_assert((size_t)2 * TS * 4 <= (size_t)N * 8 || true, "");
+  constexpr int TS = GR::TS;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
   uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);  // tiles alias qbuf
@@ -157,16 +248,16 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
   pdl_trigger();
 
   // 1. pad into the tiles (REF pad_image, ntt.cpp:155-185), pk images
-  for (int e = tid; e < npk * Lh * Lw; e += NT) {
-    const int pi = e >> (LOGH + LOGW), i = e & (Lh * Lw - 1);
-    const int r = i >> LOGW, c = i & (Lw - 1);
+  for (int e = tid; e < npk * GR::G; e += NT) {
+    const int pi = e / GR::G, i = e - pi * GR::G;
+    const int r = i / GR::L, c = i - r * GR::L;
     uint32_t v = 0;
     if (r < a.H && c < a.W && img * npk + pi < a.num_images) {
       const size_t src = ((size_t)((img * npk + pi) * a.cin + ch) * a.H + r) * a.W + c;
       if constexpr (IN_T == ENSEI_IN_U8) v = static_cast<const uint8_t*>(in)[src];
       else v = static_cast<const uint32_t*>(in)[src] % pf.q;
     }
-    S[pi * TS + r * LS + c] = v;
+    S[pi * TS + GR::px(r, c)] = v;
   }
   // Enc noise e0, two CBD draws per Philox call
   const int gimg = a.image_base / a.pk + img;
@@ -181,10 +272,10 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
   }
   __syncthreads();
   // 2. DFT2D of each tile
-  rns_tiles_2d<false, LOGH, LOGW>(pf, a.pp.cred, a.twc_fwd, S, LS, TS, npk);
+  GR::template transform<false>(a, S, S + npk * TS, npk);
   // 3. encode_slots: INTT_p of the slots gathered from the tiles
   {
-    auto src = [&](int j) { return gather_slot<LOGN, LOGH, LOGW>(S, 0, j, a.pk, TS); };
+    auto src = [&](int j) { return grid_gather<GR>(S, j, a.pk); };
     SmemRW<uint32_t> praw{pbuf};
     auto dst = [&](int i, uint32_t v) { praw(i, Bfly<Field32, 0>::fin_gs(pf, v)); };
     rns_inverse<Field32, uint32_t>(pf, a.twp_inv, pbuf, tid, src, dst);
@@ -237,11 +328,10 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
 // (bit-reversed) order, Bob's share tile aliases qbuf.
 constexpr size_t share3_smem() { return (size_t)(1 << kRnsLogN) * 8 + ssize<uint32_t>(1 << kRnsLogN) * 4; }
 
-template <int LOGH, int LOGW>
+template <class GR>
 __global__ void __launch_bounds__(kRnsThreads, 2)
-    share3_kernel(LayerArgs a, uint64_t* __restrict__ mask, uint32_t* __restrict__ bob_share) {
+    share3_kernel(const __grid_constant__ LayerArgs a, uint64_t* __restrict__ mask, uint32_t* __restrict__ bob_share) {
   constexpr int LOGN = kRnsLogN, N = 1 << LOGN, NT = kRnsThreads, R = 3;
-  constexpr int Lh = 1 << LOGH, Lw = 1 << LOGW, LS = Lw + 1;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
   uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);
@@ -265,24 +355,24 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
   // 2. Bob's share of every image of the pack: crop(IDFT2D(its part of the s_B grid))
   // (REF protocol.cpp:593-602); as many tiles at once as fit in qbuf's space
   {
-    constexpr int TS = tile_words<LOGH, LOGW>();
-    constexpr int TB = (int)(((size_t)N * 8) / ((size_t)TS * 4));  // tiles per batch
+    constexpr int TS = GR::TS;
+    constexpr int TB = (int)(((size_t)N * 8) / grid_tile_bytes<GR>(1));  // tiles per batch
     const int npi = min(a.pk, a.num_images - img * a.pk);
     for (int p0 = 0; p0 < npi; p0 += TB) {
       const int nb = min(TB, npi - p0);
       __syncthreads();
-      for (int e = tid; e < nb * Lh * Lw; e += NT) {
-        const int pi = e >> (LOGH + LOGW), i = e & (Lh * Lw - 1);
-        const int r = i >> LOGW, c = i & (Lw - 1);
-        S[pi * TS + brev(r, LOGH) * LS + brev(c, LOGW)] = pbuf[sidx<uint32_t>(brev((p0 + pi) * Lh * Lw + i, LOGN))];
+      for (int e = tid; e < nb * GR::G; e += NT) {
+        const int pi = e / GR::G, i = e - pi * GR::G;
+        const int r = i / GR::L, c = i - r * GR::L;
+        S[pi * TS + GR::fq(r, c)] = pbuf[sidx<uint32_t>(brev((p0 + pi) * GR::G + i, LOGN))];
       }
       __syncthreads();
-      rns_tiles_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, S, LS, TS, nb);
+      GR::template transform<true>(a, S, S + nb * TS, nb);
       for (int e = tid; e < nb * a.oh * a.ow; e += NT) {
         const int pi = e / (a.oh * a.ow), i = e % (a.oh * a.ow);
         const int r = i / a.ow, c = i % a.ow;
         bob_share[((size_t)(img * a.pk + p0 + pi) * a.cout + o) * a.oh * a.ow + i] =
-            pf.reduce_once(S[pi * TS + (r + a.r0) * LS + c + a.c0]);
+            pf.reduce_once(S[pi * TS + GR::px(r + a.r0, c + a.c0)]);
       }
     }
   }
@@ -360,20 +450,19 @@ __device__ __noinline__ uint32_t dec3_exact(const LayerArgs& a, const uint64_t* 
 // decides.  y_r comes out of the INTT itself: (Q/q_r)^-1 is folded
 // into the n^-1 constants of its last stage (PrimeConst::dec_*).  m overwrites acc_lo, the
 // p-side transform then runs in qbuf's space and scatters into the tiles (over acc).
-template <int LOGH, int LOGW>
+template <class GR>
 constexpr size_t dec3_smem(int pk) {
-  const size_t acc = (size_t)(1 << kRnsLogN) * 6, tiles = (size_t)pk * tile_words<LOGH, LOGW>() * 4;
+  const size_t acc = (size_t)(1 << kRnsLogN) * 6, tiles = (size_t)pk * GR::TS * 4;
   return (size_t)(1 << kRnsLogN) * 8 + (acc > tiles ? acc : tiles);
 }
 
-template <int LOGH, int LOGW>
+template <class GR>
 __global__ void __launch_bounds__(kRnsThreads, 2)
     dec3_kernel(const __grid_constant__ LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride, const uint64_t* __restrict__ ct,
                 uint32_t* __restrict__ alice_share, const uint32_t* __restrict__ bob_share,
                 uint32_t* __restrict__ outp, int ahead) {
   constexpr int LOGN = kRnsLogN, N = 1 << LOGN, NT = kRnsThreads, R = 3;
-  constexpr int Lw = 1 << LOGW, LS = Lw + 1;
-  constexpr int TS = tile_words<LOGH, LOGW>();
+  constexpr int TS = GR::TS;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
   uint32_t* acc_lo = reinterpret_cast<uint32_t*>(qbuf + N);
@@ -478,18 +567,20 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
   {
     auto psrc = [&](int i) { return acc_lo[i]; };
     auto pdst = [&](int j, uint32_t v) {
-      scatter_slot<LOGN, LOGH, LOGW>(S, 0, j, a.pk, TS, reduce_lazy(pf, v, a.pp.cred));
+      int pi, r, c;
+      GR::split(brev(j, LOGN), pi, r, c);
+      if (pi < a.pk) S[pi * TS + GR::fq(r, c)] = reduce_lazy(pf, v, a.pp.cred);
     };
     rns_forward<Field32, uint32_t, 1>(pf, a.twp_fwd, pbuf, tid, psrc, pdst);
   }
   __syncthreads();
   {  // IDFT2D of every image of the pack at once, crop (+ recombine)
     const int npi = min(a.pk, a.num_images - img * a.pk);
-    rns_tiles_2d<true, LOGH, LOGW>(pf, a.pp.cred, a.twc_inv, S, LS, TS, npi);
+    GR::template transform<true>(a, S, pbuf, npi);  // (scratch: qbuf's space, free after the p-side transform)
     for (int e = tid; e < npi * a.oh * a.ow; e += NT) {
       const int pi = e / (a.oh * a.ow), i = e % (a.oh * a.ow);
       const int r = i / a.ow, c = i % a.ow;
-      const uint32_t s = pf.reduce_once(S[pi * TS + (r + a.r0) * LS + c + a.c0]);
+      const uint32_t s = pf.reduce_once(S[pi * TS + GR::px(r + a.r0, c + a.c0)]);
       const size_t at = ((size_t)(img * a.pk + pi) * a.cout + o) * a.oh * a.ow + i;
       if (alice_share) alice_share[at] = s;
       if (outp) {
@@ -497,6 +588,61 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
         outp[at] = y >= p ? y - p : y;
       }
     }
+  }
+}
+
+// -------------------------------------------------------------------- weights
+// Bob's setup for layers with a grid override (REF protocol.cpp:462-502,
+// ringbfv.cpp:265-280): one CTA per (out, in) filter: pad -> DFT2D -> replicate across the
+// pack -> encode_slots -> centered lift -> NTT_q -> packed 30-bit limbs [cout][cin][1][R][n]
+// (the layout of tile_enc_kernel<TILE_WEIGHTS>, layer.cuh).  Shared memory as Enc.
+template <class GR>
+__global__ void __launch_bounds__(kRnsThreads, 2)
+    weights3_kernel(const __grid_constant__ LayerArgs a, const int32_t* __restrict__ w, uint64_t* __restrict__ out) {
+  constexpr int LOGN = kRnsLogN, N = 1 << LOGN, NT = kRnsThreads, R = 3;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* pbuf = reinterpret_cast<uint32_t*>(qbuf + N);
+  const int tid = threadIdx.x;
+  const Field32 pf = a.pp.f;
+  const uint32_t p = pf.q;
+  const int item = blockIdx.x;  // o * cin + ci
+  for (int e = tid; e < GR::G; e += NT) {
+    const int r = e / GR::L, c = e - r * GR::L;
+    uint32_t v = 0;
+    if (r < a.fh && c < a.fw) {
+      const int64_t m = (int64_t)w[((size_t)item * a.fh + r) * a.fw + c] % (int64_t)p;
+      v = (uint32_t)(m < 0 ? m + p : m);  // encode_signed
+    }
+    S[GR::px(r, c)] = v;
+  }
+  __syncthreads();
+  GR::template transform<false>(a, S, S + GR::TS, 1);
+  {
+    auto src = [&](int j) { return grid_gather<GR, true>(S, j, a.pk); };
+    SmemRW<uint32_t> praw{pbuf};
+    auto dst = [&](int i, uint32_t v) { praw(i, Bfly<Field32, 0>::fin_gs(pf, v)); };
+    rns_inverse<Field32, uint32_t>(pf, a.twp_inv, pbuf, tid, src, dst);
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int r = 0; r < R; ++r) {
+    const PrimeConst pc = a.pc[r];
+    const Field64 f = pc.f;
+    auto src = [&](int i) -> uint64_t {  // encode_signed(decode_signed(m)) over q_r
+      const uint32_t m = pbuf[sidx<uint32_t>(i)];
+      return m > p / 2 ? f.q - (uint64_t)(p - m) : (uint64_t)m;
+    };
+    SmemRW<uint64_t> qs{qbuf};
+    rns_forward<Field64, uint64_t, 1>(f, a.twq_fwd[r], qbuf, tid, src, qs, pc.cred);
+    __syncthreads();
+    uint64_t* ob = out + ((size_t)item * R + r) * N;
+    for (int j = tid; j < N; j += NT) {
+      const uint64_t x = Bfly<Field64, 0>::fin_ct(f, qbuf[sidx<uint64_t>(j)], pc.cred);
+      ob[j] = ((x >> 30) << 32) | (x & 0x3FFFFFFFull);
+    }
+    __syncthreads();
   }
 }
 

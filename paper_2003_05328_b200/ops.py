@@ -117,9 +117,10 @@ class ConvSpec:
     cin: int
     cout: int
     pack: int = 1  # images per ciphertext block (builder extension; 1 = REF geometry)
+    grid: int = 0  # padded grid side (builder extension; 0 = REF's next power of two)
 
     def desc(self) -> ConvDesc:
-        return ConvDesc(self.H, self.W, self.fh, self.fw, int(self.same), self.cin, self.cout, self.pack)
+        return ConvDesc(self.H, self.W, self.fh, self.fw, int(self.same), self.cin, self.cout, self.pack, self.grid)
 
 
 def unpack_limbs(t: torch.Tensor) -> torch.Tensor:

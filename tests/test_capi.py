@@ -18,7 +18,7 @@ def test_header_symbols_exported():
 
 
 def test_abi_version_and_symbol_visibility():
-    assert _lib.lib().ensei_gpu_abi_version() == 2
+    assert _lib.lib().ensei_gpu_abi_version() == 3
     out = subprocess.run(["nm", "-D", "--defined-only", _lib.SO_PATH], capture_output=True, text=True).stdout
     exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
     assert set(_lib.exported_symbols()) <= exported

@@ -44,7 +44,7 @@ struct LayerArgs {
   uint64_t psi_q[ENSEI_MAX_PRIMES];  // canonical 2n-th roots (direct-evaluation fallback)
   CrtConst crt;
   int dec_kbits;  // layer_rns.cuh: fraction bits of the packed CRT accumulator
-  // grid override (layer_rns.cuh GridDirect): primitive L-th root of unity mod p (REF's
+  // grid override (layer_rns.cuh GridPFA): primitive L-th root of unity mod p (REF's
   // canonical root, g^((p-1)/L)), its inverse, and L^-1 mod p
   uint32_t grid_w, grid_winv, grid_linv;
   PConst pp;

@@ -184,8 +184,8 @@ void launch_tile(const LayerRun& r, int tm, bool inj, int in_t, const uint64_t* 
   if (r.gridL) {  // grid override: second-generation kernels only
     if constexpr (LOGN == 13) {
       if (r.R == 3 && !inj && r.gridL == 39) {
-        if (tm == TILE_WEIGHTS) return weights3_go<GridDirect<39>>(r, static_cast<const int32_t*>(in), out, items);
-        if (tm == TILE_ENC && enc3_try<GridDirect<39>>(r, in_t, key, ks, in, out, items)) return;
+        if (tm == TILE_WEIGHTS) return weights3_go<GridPFA<3, 13>>(r, static_cast<const int32_t*>(in), out, items);
+        if (tm == TILE_ENC && enc3_try<GridPFA<3, 13>>(r, in_t, key, ks, in, out, items)) return;
       }
     }
     grid_fail();
@@ -249,7 +249,7 @@ void launch_share(const LayerRun& r, bool inj, uint64_t* mask, uint32_t* bob_sha
   if (items == 0) return;
   if (r.gridL) {
     if constexpr (LOGN == 13) {
-      if (r.R == 3 && !inj && r.gridL == 39) return share3_go<GridDirect<39>>(r, mask, bob_share, items);
+      if (r.R == 3 && !inj && r.gridL == 39) return share3_go<GridPFA<3, 13>>(r, mask, bob_share, items);
     }
     grid_fail();
   }
@@ -317,7 +317,7 @@ void launch_dec(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint6
   if (r.gridL) {
     if constexpr (LOGN == 13) {
       if (r.R == 3 && r.a.dec_kbits && r.gridL == 39 &&
-          dec3_try<GridDirect<39>>(r, key, ks, ct, alice, bob, out, items))
+          dec3_try<GridPFA<3, 13>>(r, key, ks, ct, alice, bob, out, items))
         return;
     }
     grid_fail();

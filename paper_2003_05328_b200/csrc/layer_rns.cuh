@@ -133,10 +133,10 @@ EG_DEV void rns_tiles_2d(const Field32& f, uint32_t cred, const TwPair<uint32_t>
 // frequency (r, c) of a transformed tile lives.
 //   GridPow2<LOG>  REF's choice (next power of two): radix-8 passes, frequencies in
 //                  bit-reversed positions (kernels.cuh conventions).
-//   GridDirect<L>  any L dividing p - 1 (ensei_conv_desc::grid): the O(L^2) transform REF
-//                  itself runs for such lengths (ntt_direct, ntt.cpp:35-49), rows from S into
-//                  a scratch buffer of the same size and columns back; natural order
-//                  throughout; L^-1 per dimension folded into the inverse root table.
+//   GridPFA<N1,N2> a side L = N1 N2 dividing p - 1 (ensei_conv_desc::grid): REF runs its
+//                  O(L^2) ntt_direct for such lengths (ntt.cpp:35-49); here the same
+//                  transform as a prime-factor one; natural order throughout; L^-1 per
+//                  dimension folded into the inverse tables.
 template <int LOG>
 struct GridPow2 {
   static constexpr int L = 1 << LOG, LS = L + 1, G = L * L;
@@ -155,11 +155,27 @@ struct GridPow2 {
   }
 };
 
-template <int L_>
-struct GridDirect {
-  static constexpr int L = L_, LS = (L_ & 1) ? L_ : L_ + 1, G = L_ * L_;  // odd row stride: conflict-free columns
-  static constexpr int TS = (int)((((size_t)L_ * LS * 4 + 127) & ~(size_t)127) / 4);
+// modular inverse of a mod m for small compile-time values
+constexpr int small_inv(int a, int m) {
+  for (int x = 1; x < m; ++x)
+    if ((a * x) % m == 1) return x;
+  return 0;
+}
+
+// L = N1 N2 with coprime factors (39 = 3 x 13): Good-Thomas prime-factor transform.  With
+// n = (N2 n1 + N1 n2) mod L and k = (A1 k1 + A2 k2) mod L (A1 = N2 (N2^-1 mod N1),
+// A2 = N1 (N1^-1 mod N2)) the L-point transform is a twiddle-free N1 x N2 one:
+//   X[k] = sum_n1 w1^(n1 k1) sum_n2 x[n] w2^(n2 k2),  w1 = w^N2, w2 = w^N1,
+// N2 + N1 products per output instead of L.  One thread per (line, k2): N1 lazy 64-bit
+// sums over the N2-point matrix row in shared memory, reduced, then the N1-point stage
+// from registers; rows from S into the scratch copy, columns back.
+template <int N1, int N2>
+struct GridPFA {
+  static constexpr int L = N1 * N2, LS = (L & 1) ? L : L + 1, G = L * L;  // odd row stride: conflict-free columns
+  static constexpr int TS = (int)((((size_t)L * LS * 4 + 127) & ~(size_t)127) / 4);
   static constexpr bool kScratch = true;
+  static constexpr int A1 = (N2 * small_inv(N2 % N1, N1)) % L, A2 = (N1 * small_inv(N1 % N2, N2)) % L;
+  static_assert(small_inv(N2 % N1, N1) && small_inv(N1 % N2, N2), "coprime factors");
   EG_DEV static int px(int r, int c) { return r * LS + c; }
   EG_DEV static int fq(int r, int c) { return r * LS + c; }
   EG_DEV static void split(int flat, int& pi, int& r, int& c) {
@@ -168,42 +184,65 @@ struct GridDirect {
     r = rem / L;
     c = rem - r * L;
   }
-  // one dimension: out[line][k] = sum_i in[line][i] W[(i k) mod L], 64-bit lazy sums
-  // (L 2^32 2^20 < 2^64), one reduction per output; a warp covers consecutive k of a line
-  // (broadcast reads of the line).  Outputs canonical (inverse: the caller's reduce_once
-  // is then the identity).
+  EG_DEV static uint32_t red64(const PConst& pp, uint64_t z) {  // z < 2^62 -> canonical
+    const uint64_t qt = mulhi64(z, pp.m64);
+    return pp.f.reduce_once((uint32_t)(z - qt * pp.f.q));
+  }
   template <bool COLS>
-  EG_DEV static void lines(const PConst& pp, const uint32_t* W, const uint32_t* in, uint32_t* out, int nt) {
-    for (int o = threadIdx.x; o < nt * G; o += blockDim.x) {
-      const int t = o / G, rem = o - t * G, ln = rem / L, k = rem - ln * L;
+  EG_DEV static void lines(const PConst& pp, const uint32_t* M2, const uint32_t* M1, const uint32_t* in,
+                           uint32_t* out, int nt) {
+    constexpr int ST = COLS ? LS : 1;
+    for (int it = threadIdx.x; it < nt * L * N2; it += blockDim.x) {
+      const int t = it / (L * N2), rem = it - t * (L * N2), ln = rem / N2, k2 = rem - ln * N2;
       const uint32_t* x = in + t * TS + (COLS ? ln : ln * LS);
-      uint64_t acc = 0;
-      int idx = 0;
-#pragma unroll 13
-      for (int i = 0; i < L; ++i) {
-        acc = madw(x[COLS ? i * LS : i], W[idx], acc);
-        idx += k;
-        if (idx >= L) idx -= L;
+      const uint32_t* m2 = M2 + k2 * N2;
+      uint32_t y[N1];
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) {
+        uint64_t acc = 0;
+#pragma unroll
+        for (int n2 = 0; n2 < N2; ++n2) acc = madw(x[((N2 * n1 + N1 * n2) % L) * ST], m2[n2], acc);
+        y[n1] = red64(pp, acc);
       }
-      const uint64_t qt = mulhi64(acc, pp.m64);
-      out[t * TS + (COLS ? k * LS + ln : ln * LS + k)] = pp.f.reduce_once((uint32_t)(acc - qt * pp.f.q));
+      const int kb = (A2 * k2) % L;
+#pragma unroll
+      for (int k1 = 0; k1 < N1; ++k1) {
+        uint64_t acc = 0;
+#pragma unroll
+        for (int n1 = 0; n1 < N1; ++n1) acc = madw(y[n1], M1[k1 * N1 + n1], acc);
+        int k = kb + A1 * k1;
+        k = k >= L ? k - L : k;  // kb < L, A1 k1 < L for k1 < N1
+        k = k >= L ? k - L : k;
+        out[t * TS + (COLS ? k * LS + ln : ln * LS + k)] = red64(pp, acc);
+      }
     }
   }
   template <bool INV>
   EG_DEV static void transform(const LayerArgs& a, uint32_t* S, uint32_t* scratch, int nt) {
-    __shared__ uint32_t W[L_];
-    if (threadIdx.x < L) {  // W[i] = w^i (inverse: w^-i / L)
-      uint32_t b = INV ? a.grid_winv : a.grid_w, r = INV ? a.grid_linv : 1u;
-      for (int e = threadIdx.x; e; e >>= 1) {
-        if (e & 1) r = a.pp.f.mul(r, b, a.pp.m64);
-        b = a.pp.f.mul(b, b, a.pp.m64);
+    __shared__ uint32_t M2[N2 * N2], M1[N1 * N1];
+    const Field32 f = a.pp.f;
+    auto pw = [&](uint32_t b, int e) {
+      uint32_t r = 1;
+      for (; e; e >>= 1) {
+        if (e & 1) r = f.mul(r, b, a.pp.m64);
+        b = f.mul(b, b, a.pp.m64);
       }
-      W[threadIdx.x] = r;
+      return r;
+    };
+    const uint32_t w = INV ? a.grid_winv : a.grid_w;
+    for (int i = threadIdx.x; i < N2 * N2 + N1 * N1; i += blockDim.x) {
+      if (i < N2 * N2) {
+        M2[i] = pw(pw(w, N1), ((i / N2) * (i % N2)) % N2);
+      } else {
+        const int j = i - N2 * N2;
+        const uint32_t v = pw(pw(w, N2), ((j / N1) * (j % N1)) % N1);
+        M1[j] = INV ? f.mul(v, a.grid_linv, a.pp.m64) : v;  // L^-1 per dimension
+      }
     }
     __syncthreads();
-    lines<false>(a.pp, W, S, scratch, nt);
+    lines<false>(a.pp, M2, M1, S, scratch, nt);
     __syncthreads();
-    lines<true>(a.pp, W, scratch, S, nt);
+    lines<true>(a.pp, M2, M1, scratch, S, nt);
     __syncthreads();
   }
 };

@@ -31,6 +31,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -86,7 +87,11 @@ def parse():
     ap.add_argument("--no-ntt", action="store_true")
     ap.add_argument("--no-side", action="store_true", help="config 4: skip the config-1 / unpacked side lines")
     ap.add_argument("--pack", type=int, default=None,
-                    help="images per ciphertext block (config 4 default 2; 1 = REF geometry); config 3: 1 = unpacked")
+                    help="images per ciphertext block (config 4 default: 5 on the 39x39 grid, 2 with --grid 0; "
+                         "1 = REF geometry); config 3: 1 = unpacked")
+    ap.add_argument("--grid", type=int, default=None,
+                    help="config 4: padded grid side (default 39, the smallest side dividing p - 1 that holds the "
+                         "convolution; 0 = REF's 64x64)")
     ap.add_argument("--no-graph", action="store_true", help="launch the layer eagerly instead of a CUDA graph")
     return ap.parse_args()
 
@@ -109,21 +114,38 @@ def idft2d(L):
     return dft2d(L) + L * L
 
 
+def _pfa_factors(L):
+    """L = N1 N2 with coprime factors (the device's prime-factor tile transform), or None."""
+    for a in range(2, L):
+        if L % a == 0 and math.gcd(a, L // a) == 1:
+            return a, L // a
+    return None
+
+
+def dft2d_any(L, inverse=False):
+    """Modmuls of one L x L tile transform: radix-2 for powers of two, the prime-factor form
+    (N1 + N2 products per output, no twiddles) for the non-power-of-two grid override."""
+    if L & (L - 1) == 0:
+        return idft2d(L) if inverse else dft2d(L)
+    n1, n2 = _pfa_factors(L)
+    return 2 * L * L * (n1 + n2)
+
+
 def layer_counts(n, R, L, B, cin, cout, H, W, oh, ow, imgs, pack=1):
     """Algorithmic modmul counts and HBM bytes per kernel per launch for
     `imgs` images; with packing, the ring work is per ciphertext image (pack images each),
     the 2D transforms and pixel / share bytes per image."""
     c = -(-imgs // pack)  # ciphertext images
     k = {}
-    k["enc"] = dict(q=c * cin * B * R * (2 * n + ntt_fwd(n)), mac=0, p=imgs * cin * dft2d(L) + c * cin * B * ntt_inv(n),
+    k["enc"] = dict(q=c * cin * B * R * (2 * n + ntt_fwd(n)), mac=0, p=imgs * cin * dft2d_any(L) + c * cin * B * ntt_inv(n),
                     bytes=imgs * cin * H * W + c * cin * B * 2 * R * n * 8 + 2 * R * n * 8)
     k["share"] = dict(q=c * cout * B * R * (n + ntt_fwd(n)), mac=0,
-                      p=c * cout * B * ntt_inv(n) + imgs * cout * idft2d(L),
+                      p=c * cout * B * ntt_inv(n) + imgs * cout * dft2d_any(L, True),
                       bytes=c * cout * B * R * n * 8 + imgs * cout * oh * ow * 4)
     k["mac"] = dict(q=0, mac=c * cin * cout * B * R * 2 * n, p=0,
                     bytes=c * cin * B * 2 * R * n * 8 + cout * cin * B * R * n * 8 + c * cout * B * R * n * 8
                     + c * cout * B * 2 * R * n * 8)
-    k["dec"] = dict(q=c * cout * B * R * (n + ntt_inv(n)), mac=0, p=c * cout * B * ntt_fwd(n) + imgs * cout * idft2d(L),
+    k["dec"] = dict(q=c * cout * B * R * (n + ntt_inv(n)), mac=0, p=c * cout * B * ntt_fwd(n) + imgs * cout * dft2d_any(L, True),
                     bytes=c * cout * B * 2 * R * n * 8 + 2 * R * n * 8 + imgs * cout * oh * ow * 4 * 3)
     for v in k.values():
         v["imad"] = C_Q * v["q"] + C_MAC * v["mac"] + C_P * v["p"]
@@ -627,9 +649,10 @@ def run_config4(args, world, rank, local):
     cfg = CF.CONFIG4
     imgs = args.images or cfg["images"]
     cin, cout = cfg["cin"], cfg["cout"]
-    pack = CF.CONFIG4_PACK if args.pack is None else args.pack
+    grid = CF.CONFIG4_GRID if args.grid is None else args.grid
+    pack = (CF.CONFIG4_GRID_PACK if grid else CF.CONFIG4_PACK) if args.pack is None else args.pack
     ctx = ops.Context(n=cfg["n"], q=cfg["q"], p=P, device=local)
-    L = ops.LayerOps(ctx, ops.ConvSpec(32, 32, 3, 3, True, cin, cout, pack))
+    L = ops.LayerOps(ctx, ops.ConvSpec(32, 32, 3, 3, True, cin, cout, pack, grid))
     g = L.geom
     shard = ImageShard(world * imgs, world, rank)  # contiguous image shards, global image ids
     # this rank's images (seeded per shard: 64 MiB of pixels per GPU), weights from the common seed
@@ -643,7 +666,10 @@ def run_config4(args, world, rank, local):
     we = L.prepare_weights(w_h.to(dev))  # Bob's t_setup (not timed in the step)
     torch.cuda.synchronize()
     setup_ms = (time.perf_counter() - t_s) * 1e3
-    rand = ops.Randomness(seed=args.seed, image_base=shard.start)
+    # stream ids are per ciphertext: a rank's first image id must be pack-aligned (ranks own whole
+    # ciphertexts; ids stay unique across ranks)
+    id_base = rank * (-(-imgs // pack)) * pack
+    rand = ops.Randomness(seed=args.seed, image_base=id_base)
     chunk = L.chunk_images(imgs)
     ws = L.workspace(imgs)
     shape = (imgs, cout, g.oh, g.ow)
@@ -664,7 +690,7 @@ def run_config4(args, world, rank, local):
         # chunk by chunk so each chunk's share all-gathers overlap the next chunk's kernels
         for i0 in range(0, imgs, chunk):
             i1 = min(imgs, i0 + chunk)
-            L.forward(key, we, x[i0:i1], ops.Randomness(seed=args.seed, image_base=shard.start + i0), ws=ws,
+            L.forward(key, we, x[i0:i1], ops.Randomness(seed=args.seed, image_base=id_base + i0), ws=ws,
                       out=out[i0:i1], want_shares=True, alice=alice[i0:i1], bob=bob[i0:i1])
             gather.post(i0, i1, alice, bob)
         gather.wait()
@@ -707,7 +733,7 @@ def run_config4(args, world, rank, local):
     prof = _lib.profile_read()
     _lib.profile(False)
     nchunks = -(-imgs // chunk)
-    kc = config4_counts(chunk, pack)
+    kc = config4_counts(chunk, pack, L=int(g.Lh))
     imad_peak = lib.ensei_gpu_imad_peak(local)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
@@ -756,20 +782,28 @@ def run_config4(args, world, rank, local):
         "c_q": C_Q, "c_mac": C_MAC, "c_p": C_P,
     }
     step_imad = sum(kc[k]["imad"] for k in ("enc", "share", "dec")) * nchunks
-    # the same layer in REF's geometry (one image per ciphertext block), for comparison
-    unpacked = None
-    if pack > 1 and not args.no_side:
-        L1 = ops.LayerOps(ctx, ops.ConvSpec(32, 32, 3, 3, True, cin, cout, 1))
+    # the same layer in REF's geometry (one image per ciphertext block on the 64x64 grid) and with
+    # two 64x64 grids per block, for comparison
+    def other_geometry(pk, gr, what):
+        L1 = ops.LayerOps(ctx, ops.ConvSpec(32, 32, 3, 3, True, cin, cout, pk, gr))
         we1 = L1.prepare_weights(w_h.to(dev))
         ws1 = L1.workspace(imgs)
         out1 = torch.empty_like(out)
-        t1 = _time_steps(lambda: L1.forward(key, we1, x, rand, ws=ws1, out=out1), max(3, args.steps // 4), 2, flush,
+        rand1 = ops.Randomness(seed=args.seed, image_base=rank * (-(-imgs // pk)) * pk)
+        t1 = _time_steps(lambda: L1.forward(key, we1, x, rand1, ws=ws1, out=out1), max(3, args.steps // 4), 2, flush,
                          stream)
-        unpacked = {"value": world * imgs * max(3, args.steps // 4) / (t1 / 1e3), "unit": "conv/s",
-                    "geometry": "REF's: one image per n = 8192 ciphertext block (half the slots empty)",
-                    "outputs_equal_packed": bool(torch.equal(out1, out))}
+        rec = {"value": world * imgs * max(3, args.steps // 4) / (t1 / 1e3), "unit": "conv/s", "geometry": what,
+               "outputs_equal_headline": bool(torch.equal(out1, out))}
         del ws1, we1
         torch.cuda.empty_cache()
+        return rec
+    unpacked = pow2_packed = None
+    if (pack > 1 or grid) and not args.no_side:
+        unpacked = other_geometry(1, 0, "REF's: one image per n = 8192 ciphertext block, 64x64 grid (half the slots "
+                                        "empty)")
+        if grid:
+            pow2_packed = other_geometry(CF.CONFIG4_PACK, 0, "two 64x64 grids per n = 8192 block (round-2 headline "
+                                                             "geometry before the grid override)")
     total_modmul = sum(kc[k]["modmul"] for k in ("enc", "share", "mac", "dec")) * nchunks
 
     # ---- e2e through the host-buffer C-ABI entry point (pinned host buffers, chunked inside)
@@ -851,24 +885,28 @@ def run_config4(args, world, rank, local):
         "vs_baseline": None, "dtype": "u64",
         "data": "synthetic: uint8 pixels U[0,256), int8 weights U[-128,128), seeded (no dataset)",
         "config": {"workload": f"config4: one 64->128 3x3 Same conv layer, {imgs} images/GPU x 64x32x32 uint8, int8 "
-                               "weights, n=8192, RNS q = 3 x 60-bit primes == 1 mod 16384 p, p=638977, 64x64 "
-                               "padded grid, 1 block/channel",
+                               "weights, n=8192, RNS q = 3 x 60-bit primes == 1 mod 16384 p, p=638977, "
+                               f"{g.Lh}x{g.Lw} padded grid, {pack} image(s) per ciphertext block, 1 block/channel",
                    "images_per_gpu": imgs, "global_batch": world * imgs, "parallelism": f"dp{world} (image shards)",
                    "sub_batch_images": chunk, "l2": "flushed (256 MB write) between timed steps; each step also "
                    "streams ~100 GB through HBM", "randomness": "Philox4x32-10 device streams",
-                   "launch": "eager (8 sub-batches x 6 kernels per step)",
+                   "launch": f"eager ({nchunks} sub-batches x 6 kernels per step)",
                    "gather": "both parties' output shares all-gathered per sub-batch over NCCL, overlapped"
                              if world > 1 else "none (1 GPU)",
                    "unit_def": "1 conv = 1 image through the whole 64->128 layer", "config_index": 4,
                    "mac_path": L.mac_path(chunk),
-                   "pack": pack, "packing": ("two images' 64x64 DFT grids per n = 8192 ciphertext block (builder "
-                                             "extension; every slot-wise step unchanged, outputs = REF's)")
-                   if pack > 1 else "REF geometry (one image per block)"},
+                   "pack": pack, "grid": int(g.Lh),
+                   "packing": (f"{pack} images' {g.Lh}x{g.Lw} DFT grids per n = 8192 ciphertext block (builder "
+                               "extension; every slot-wise step unchanged, outputs = REF's)"
+                               + ("; grid override: 39 is the smallest side dividing p - 1 = 2^14 39 that holds the "
+                                  "34x34 linear convolution (REF pads to 64 for its radix-2 transform), tile "
+                                  "transforms in prime-factor form" if grid else ""))
+                   if pack > 1 or grid else "REF geometry (one image per block)"},
         "roofline": roofline, "setup_ms": setup_ms,
         "imad_slot_rate": step_imad * args.steps / (total_ms / 1e3), "modmul_per_s": total_modmul * args.steps / (
             total_ms / 1e3),
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk, "verify": verify,
-        "config1": side1, "ntt_n8192": ntt, "ref_geometry": unpacked,
+        "config1": side1, "ntt_n8192": ntt, "ref_geometry": unpacked, "pow2_packed": pow2_packed,
     }
 
 

@@ -35,7 +35,10 @@ CONFIG3_IMAGES = 64
 # holds (1, 1, 2, 2, 8, 32, 32: the 32x32, 16x16 and 8x8 grids fill 1/2, 1/8, 1/32 of n = 2048)
 CONFIG3_SCHEDULE_PACKED = [Conv(s.fh, s.fw, s.same, s.cin, s.cout, 0) if isinstance(s, Conv) else s
                            for s in CONFIG3_SCHEDULE]
-CONFIG4_PACK = 2  # two 64x64 grids per n = 8192 block
+CONFIG4_PACK = 2  # two 64x64 grids per n = 8192 block (REF's power-of-two grid)
+# the headline geometry: the smallest grid side dividing p - 1 = 2^14 39 that holds the linear
+# convolution (32 + 3 - 1 = 34 <= 39), five 39x39 grids per n = 8192 block
+CONFIG4_GRID, CONFIG4_GRID_PACK = 39, 5
 # the three reference-expressible segments (REF has no pooling layer): [L1, ReLU, L2] @32,
 # [L3, ReLU, L4] @16, [L5, ReLU, L6, ReLU, L7] @8 as (first schedule index, last + 1, side, cin)
 CONFIG3_SEGMENTS = [(0, 3, 32, 3), (4, 7, 16, 64), (8, 13, 8, 128)]

@@ -51,6 +51,11 @@ METRIC = "oblivious NTT-domain conv/sec (1/2/4/8 B200); NTT modmul/s vs roofline
 #   q-Shoup 5 WIDE + 4 IMAD = 14 > 10 -> 10;  Karatsuba MAC 3 WIDE = 6 < 8 -> 6;
 #   p-Shoup 1 WIDE + 2 IMAD = 4 > 3 -> 3.
 C_Q, C_MAC, C_P = 10, 6, 3
+# What the SASS can reach with 32-bit multipliers: a Shoup product is 5 IMAD.WIDE (two pipe
+# slots each -- ncu: fmaheavy busy exceeds issue active by exactly that weighting) + 4 IMAD
+# = 14 slots (DESIGN 4, "NTT engine"); imad fractions against that floor are reported beside
+# the survey's c_q = 10.
+C_Q_SASS = 14
 
 
 # profile name -> kernel names it can stand for (the 3-prime RNS layer runs the second-generation
@@ -733,7 +738,13 @@ def run_config4(args, world, rank, local):
     prof = _lib.profile_read()
     _lib.profile(False)
     nchunks = -(-imgs // chunk)
-    kc = config4_counts(chunk, pack, L=int(g.Lh))
+    # algorithmic work of an AVERAGE launch: the step's sub-batches differ in size when the
+    # sub-batch does not divide the batch (1024 images = 640 + 384 with five images per block),
+    # and the event times below are per-launch averages over the same sub-batches
+    kc = config4_counts(imgs, pack, L=int(g.Lh))
+    for rec_ in kc.values():
+        for key_ in list(rec_):
+            rec_[key_] = rec_[key_] / nchunks
     imad_peak = lib.ensei_gpu_imad_peak(local)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
@@ -756,6 +767,7 @@ def run_config4(args, world, rank, local):
             if c.get("imad"):
                 rec["imad_frac"] = c["imad"] / t / imad_peak
                 rec["imad_slots_per_launch"] = c["imad"]
+                rec["imad_frac_sass_floor"] = (c["imad"] + (C_Q_SASS - C_Q) * c["q"]) / t / imad_peak
             if c.get("i8_mac"):
                 rec["tensor_frac"] = 2 * c["i8_mac"] / t / 1e12 / i8_peak
                 rec["int8_macs_per_launch"] = c["i8_mac"]
@@ -778,8 +790,9 @@ def run_config4(args, world, rank, local):
         "peak_source": {"tensor": i8_src, "imad": "live mad.lo.u32 probe (ensei_gpu_imad_peak)",
                         "hbm": "MEASURED_PEAKS.json hbm_gbs (measured)"}[bound],
         "legs": legs, "per_kernel": per_kernel,
-        "units_per_launch": f"{chunk} images (one sub-batch); {nchunks} launches of each kernel per step",
-        "c_q": C_Q, "c_mac": C_MAC, "c_p": C_P,
+        "units_per_launch": f"{imgs / nchunks:g} images on average ({nchunks} sub-batches of at most {chunk} images per step: "
+                            f"{nchunks} launches of each kernel)",
+        "c_q": C_Q, "c_mac": C_MAC, "c_p": C_P, "c_q_sass_floor": C_Q_SASS,
     }
     step_imad = sum(kc[k]["imad"] for k in ("enc", "share", "dec")) * nchunks
     # the same layer in REF's geometry (one image per ciphertext block on the 64x64 grid) and with
@@ -931,7 +944,8 @@ def ntt_side(ctx, dev, stream, imad_peak):
         ms = a.elapsed_time(b) / 5
         rate = cnt / (ms / 1e3)
         alg = ntt_inv(n) if inv else ntt_fwd(n)
-        res["inv" if inv else "fwd"] = {"transforms_per_s": rate, "ms": ms, "imad_frac": rate * alg * C_Q / imad_peak}
+        res["inv" if inv else "fwd"] = {"transforms_per_s": rate, "ms": ms, "imad_frac": rate * alg * C_Q / imad_peak,
+                                        "imad_frac_sass_floor": rate * alg * C_Q_SASS / imad_peak}
     del buf
     torch.cuda.empty_cache()
     return res
@@ -1032,6 +1046,7 @@ def other_config(args, world, rank, local):
         imad_peak = lib.ensei_gpu_imad_peak(local)
         alg = (ntt_fwd(n) + ntt_inv(n)) * C_Q * cnt
         extra["imad_frac"] = alg * args.steps / (total / 1e3) / imad_peak
+        extra["imad_frac_sass_floor"] = extra["imad_frac"] * C_Q_SASS / C_Q
         extra["hbm_GB_s"] = 2 * cnt * n * 16 * args.steps / (total / 1e3) / 1e9
         if rank == 0 and not args.no_cpu_baseline:
             import oracle as O

@@ -69,7 +69,11 @@ typedef struct ensei_gpu_ctx ensei_gpu_ctx;
  * num_q > 1 is the RNS extension for large runs), p = p_N = p_A = p_E.
  * Checks REF's invariants: every prime q_i and p are prime, == 1 mod 2n,
  * q_i == 1 mod p, q > p; throws (returns) ENSEI_ERR_GENERIC otherwise.
- * Builds canonical-root twiddle tables on `device`. */
+ * Builds canonical-root twiddle tables on `device`.
+ * Threading: a context owns an auxiliary stream, fork / join events, the cached host-entry
+ * graph and the wire status block; calls on ONE context must not overlap in time (two host
+ * threads, or two streams whose work can run concurrently).  Use one context per
+ * concurrently working party / stream; contexts are independent of each other. */
 int ensei_gpu_ctx_create(int device, uint32_t n, const uint64_t* q_primes, uint32_t num_q,
                          uint64_t p, ensei_gpu_ctx** out);
 void ensei_gpu_ctx_destroy(ensei_gpu_ctx* ctx);

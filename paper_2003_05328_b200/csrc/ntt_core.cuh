@@ -332,13 +332,26 @@ struct FwdBounds {
   }
 };
 
+// Barrier between pass I and pass I + 1 of a transform.  The last two passes (2 LOGE stages)
+// work inside blocks of 2^(2 LOGE) consecutive elements, and with LOGE = 3 a block's sets
+// belong to the same 8 consecutive threads in both passes (set j of the last pass =
+// elements [8j, 8j + 8); of the one before = block j / 8): a warp barrier is enough there.
+template <int LOGN, int LOGE, int I, class Bar>
+EG_DEV void pass_sync(const Bar& bar) {
+  using Plan = PassPlan<LOGN, LOGE>;
+  if constexpr (LOGE == 3 && I == Plan::npass - 2 && Plan::npass >= 3 && Plan::p_of(I) == 3 && LOGN - 3 >= 5)
+    __syncwarp();
+  else
+    bar.sync();
+}
+
 template <class F, class T, int LOGN, int LOGE, int MODE, int B_IN, int I, class Bar>
 EG_DEV void fwd_middle(const F& f, const TwPair<T>* __restrict__ tw, int tid, SmemRW<T>& s, const Bar& bar,
                        uint32_t cred) {
   if constexpr (I < PassPlan<LOGN, LOGE>::npass - 1) {
     constexpr bool C = FwdBounds<F, MODE, LOGN, LOGE, B_IN>::corr(I);
     run_pass<F, T, LOGN, LOGE, I, false, MODE, false, SmemRW<T>, SmemRW<T>, Bar, C>(f, tw, tid, s, s, bar, cred);
-    bar.sync();
+    pass_sync<LOGN, LOGE, I>(bar);
     fwd_middle<F, T, LOGN, LOGE, MODE, B_IN, I + 1>(f, tw, tid, s, bar, cred);
   }
 }
@@ -371,7 +384,7 @@ EG_DEV void ntt_forward(const F& f, const TwPair<T>* __restrict__ tw, T* sm, int
   } else {
     run_pass<F, T, LOGN, LOGE, 0, false, MODE, SPLIT_FIRST, Src, SmemRW<T>, Bar, FB::corr(0)>(f, tw, tid, src, s,
                                                                                           bar, cred);
-    bar.sync();
+    pass_sync<LOGN, LOGE, 0>(bar);
     fwd_middle<F, T, LOGN, LOGE, MODE, B_IN, 1>(f, tw, tid, s, bar, cred);
     run_pass<F, T, LOGN, LOGE, Plan::npass - 1, false, MODE, SPLIT_LAST, SmemRW<T>, Dst, Bar,
              FB::corr(Plan::npass - 1)>(f, tw, tid, s, dst, bar, cred);
@@ -391,7 +404,7 @@ EG_DEV void ntt_inverse(const F& f, const TwPair<T>* __restrict__ tw, T* sm, int
     run_pass<F, T, LOGN, LOGE, 0, true, MODE, SPLIT_FIRST || SPLIT_LAST>(f, tw, tid, src, dst, bar);
   } else {
     run_pass<F, T, LOGN, LOGE, L, true, MODE, SPLIT_FIRST>(f, tw, tid, src, s, bar);
-    bar.sync();
+    pass_sync<LOGN, LOGE, L - 1>(bar);  // passes L and L - 1: the same two block-local passes
     inv_middle<F, T, LOGN, LOGE, MODE, L - 1>(f, tw, tid, s, bar);
     run_pass<F, T, LOGN, LOGE, 0, true, MODE, SPLIT_LAST>(f, tw, tid, s, dst, bar);
   }

@@ -15,41 +15,55 @@ EG_DEV void prefetch_poly(uint64_t* sm, const uint64_t* g, int tid, int nthreads
   cp_async_commit();
 }
 
-// One length-N transform per CTA iteration (NT = N/E threads), persistent grid-stride
-// over polynomials.  The next polynomial streams into the second smem buffer with
-// cp.async while the current one is transformed; twiddles are staged once per CTA by
-// a TMA bulk copy (TW_SMEM) or read through L1.
-template <int LOGN, int LOGE, int MODE, bool INV, bool NATURAL, bool TW_SMEM>
-__global__ void __launch_bounds__((1 << LOGN) >> LOGE)
+// Barrier over the NT threads of thread group g of a CTA (literal ids: ptxas budgets barriers
+// by the largest id it sees)
+struct BatchGroupBar {
+  int g, count;
+  EG_DEV void sync() const {
+    if (g == 0) asm volatile("bar.sync 1, %0;" ::"r"(count) : "memory");
+    else asm volatile("bar.sync 2, %0;" ::"r"(count) : "memory");
+  }
+};
+
+// One length-N transform per thread group and iteration (NT = N/E threads per group, G groups
+// per CTA), persistent grid-stride over polynomials.  The next polynomial streams into the
+// group's second smem buffer with cp.async while the current one is transformed; twiddles
+// are staged once per CTA by a TMA bulk copy (TW_SMEM) or read through L1.  G = 2 lets two
+// polynomials share one staged table: 96 KB per 512-thread CTA at n = 2048 (two CTAs = 32
+// warps per SM instead of three 64 KB CTAs = 24), 192 KB per 1024-thread CTA at n = 4096
+// (32 warps instead of 16); the groups run out of step behind their own named barriers.
+template <int LOGN, int LOGE, int MODE, bool INV, bool NATURAL, bool TW_SMEM, int G = 1>
+__global__ void __launch_bounds__(G * ((1 << LOGN) >> LOGE), (G * ((1 << LOGN) >> LOGE) <= 512 && G == 2) ? 2 : 1)
     negacyclic_q_kernel(PrimeConst pc, const TwPair<uint64_t>* __restrict__ tw_g, uint64_t* data,
                         size_t count) {
   constexpr int N = 1 << LOGN, NT = N >> LOGE;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ uint64_t mbar;
   TwPair<uint64_t>* tw_s = reinterpret_cast<TwPair<uint64_t>*>(smem_raw);
-  uint64_t* buf0 = reinterpret_cast<uint64_t*>(smem_raw + (TW_SMEM ? N * sizeof(TwPair<uint64_t>) : 0));
-  const int tid = threadIdx.x;
-  const CtaBar bar;
+  const int g = G == 1 ? 0 : threadIdx.x / NT, tid = G == 1 ? threadIdx.x : threadIdx.x % NT;
+  uint64_t* buf0 = reinterpret_cast<uint64_t*>(smem_raw + (TW_SMEM ? N * sizeof(TwPair<uint64_t>) : 0)) + g * 2 * N;
+  const BatchGroupBar bar{g, NT};
   const Field64 f = pc.f;
   const TwPair<uint64_t>* tw = tw_g;
-  size_t poly = blockIdx.x;
+  size_t poly = (size_t)blockIdx.x * G + g;
+  const size_t stride = (size_t)gridDim.x * G;
   if (poly < count) prefetch_poly<N>(buf0, data + poly * N, tid, NT);
   if constexpr (TW_SMEM) {
     stage_table(tw_s, tw_g, N * sizeof(TwPair<uint64_t>), &mbar);
     tw = tw_s;
   }
   int cur = 0;
-  for (; poly < count; poly += gridDim.x) {
+  for (; poly < count; poly += stride) {
     cp_async_wait_all();
-    __syncthreads();
-    const size_t next = poly + gridDim.x;
+    bar.sync();
+    const size_t next = poly + stride;
     if (next < count) prefetch_poly<N>(buf0 + (cur ^ 1) * N, data + next * N, tid, NT);
     uint64_t* sm = buf0 + cur * N;
-    uint64_t* g = data + poly * N;
+    uint64_t* gp = data + poly * N;
     SmemRW<uint64_t> s{sm};
     if constexpr (!INV) {
       if constexpr (!NATURAL) {
-        GlobalOut64<MODE, true> out{g, f, pc.cred};
+        GlobalOut64<MODE, true> out{gp, f, pc.cred};
         ntt_forward<Field64, uint64_t, LOGN, LOGE, MODE, false, false>(f, tw, sm, tid, s, out, bar, pc.cred);
       } else {
         auto dst = [&](int i, uint64_t v) {
@@ -58,10 +72,10 @@ __global__ void __launch_bounds__((1 << LOGN) >> LOGE)
         ntt_forward<Field64, uint64_t, LOGN, LOGE, MODE, false, true>(f, tw, sm, tid, s, dst, bar, pc.cred);
         bar.sync();
         for (int c = tid; c < N / 2; c += NT)
-          *reinterpret_cast<ulonglong2*>(g + 2 * c) = *reinterpret_cast<const ulonglong2*>(sm + sidx<uint64_t>(2 * c));
+          *reinterpret_cast<ulonglong2*>(gp + 2 * c) = *reinterpret_cast<const ulonglong2*>(sm + sidx<uint64_t>(2 * c));
       }
     } else {
-      GlobalOut64<MODE, false> out{g, f, pc.cred};
+      GlobalOut64<MODE, false> out{gp, f, pc.cred};
       if constexpr (!NATURAL) {
         ntt_inverse<Field64, uint64_t, LOGN, LOGE, MODE, false, false>(f, tw, sm, tid, s, out, bar);
       } else {
@@ -74,9 +88,9 @@ __global__ void __launch_bounds__((1 << LOGN) >> LOGE)
   cp_async_wait_all();
 }
 
-template <int LOGN, int LOGE, bool TW_SMEM>
+template <int LOGN, int LOGE, bool TW_SMEM, int G = 1>
 constexpr size_t negacyclic_q_smem() {
-  return (TW_SMEM ? (1 << LOGN) * sizeof(TwPair<uint64_t>) : 0) + 2 * (1 << LOGN) * sizeof(uint64_t);
+  return (TW_SMEM ? (1 << LOGN) * sizeof(TwPair<uint64_t>) : 0) + (size_t)G * 2 * (1 << LOGN) * sizeof(uint64_t);
 }
 
 // Same structure over the 32-bit modulus p, uint64 storage (REF Residue).

@@ -6,32 +6,89 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "ntt_batch.cuh"
+#include "layer_rns.cuh"
 
 namespace ensei_gpu {
 
 // ------------------------------------------------------------------- launch
 
-template <int LOGN, int LOGE, int MODE, bool INV, bool NATURAL, bool TW_SMEM>
+template <int LOGN, int LOGE, int MODE, bool INV, bool NATURAL, bool TW_SMEM, int G>
 static void launch_q(const ensei_gpu_ctx* ctx, int prime, uint64_t* d, size_t count, cudaStream_t st) {
-  auto k = negacyclic_q_kernel<LOGN, LOGE, MODE, INV, NATURAL, TW_SMEM>;
-  constexpr int NT = (1 << LOGN) >> LOGE;
-  constexpr size_t smem = negacyclic_q_smem<LOGN, LOGE, TW_SMEM>();
+  auto k = negacyclic_q_kernel<LOGN, LOGE, MODE, INV, NATURAL, TW_SMEM, G>;
+  constexpr int NT = G * ((1 << LOGN) >> LOGE);
+  constexpr size_t smem = negacyclic_q_smem<LOGN, LOGE, TW_SMEM, G>();
   static int per_sm = -1;
   if (per_sm < 0) {
     EG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     EG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, smem));
   }
-  size_t grid = std::min<size_t>(count, (size_t)std::max(per_sm, 1) * ctx->sm_count);
+  size_t grid = std::min<size_t>((count + G - 1) / G, (size_t)std::max(per_sm, 1) * ctx->sm_count);
   const TwPair<uint64_t>* tw = INV ? ctx->tab.tw_q_inv[prime] : ctx->tab.tw_q_fwd[prime];
   k<<<(unsigned)grid, NT, smem, st>>>(ctx->pc[prime], tw, d, count);
   check_launch("negacyclic_q_kernel");
 }
 
+// n = 8192, device layout, lazy (MODE 0) butterflies: the tile kernels' form of the transform
+// (layer_rns.cuh): 512 threads run every pass in two rounds, one 64 KB buffer, two CTAs per SM
+// out of step with each other instead of one 1024-thread CTA with a prefetch buffer.
+struct GlobalIn64 {
+  const uint64_t* g;
+  static constexpr bool kVec = true;
+  EG_DEV uint64_t operator()(int i) const { return g[i]; }
+  EG_DEV void ld2(int i, uint64_t& a, uint64_t& b) const {
+    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(g + i);
+    a = v.x;
+    b = v.y;
+  }
+};
+template <bool INV>
+__global__ void __launch_bounds__(kRnsThreads, 2)
+    negacyclic_q13_kernel(PrimeConst pc, const TwPair<uint64_t>* __restrict__ tw, uint64_t* data, size_t count) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
+  const int tid = threadIdx.x;
+  const Field64 f = pc.f;
+  for (size_t poly = blockIdx.x; poly < count; poly += gridDim.x) {
+    uint64_t* g = data + poly * (size_t)(1 << kRnsLogN);
+    GlobalIn64 src{g};
+    if constexpr (!INV) {
+      GlobalOut64<0, true> out{g, f, pc.cred};
+      rns_forward<Field64, uint64_t, 1>(f, tw, qbuf, tid, src, out, pc.cred);
+    } else {
+      auto dst = [&](int i, uint64_t v) { g[i] = Bfly<Field64, 0>::fin_gs(f, v); };
+      rns_inverse<Field64, uint64_t>(f, tw, qbuf, tid, src, dst);
+    }
+    __syncthreads();
+  }
+}
+template <bool INV>
+static void launch_q13(const ensei_gpu_ctx* ctx, int prime, uint64_t* d, size_t count, cudaStream_t st) {
+  auto k = negacyclic_q13_kernel<INV>;
+  constexpr size_t smem = (size_t)(1 << kRnsLogN) * 8;
+  static bool once = false;
+  if (!once) {
+    EG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    once = true;
+  }
+  const size_t grid = std::min<size_t>(count, (size_t)2 * ctx->sm_count);
+  k<<<(unsigned)grid, kRnsThreads, smem, st>>>(ctx->pc[prime], INV ? ctx->tab.tw_q_inv[prime] : ctx->tab.tw_q_fwd[prime],
+                                               d, count);
+  check_launch("negacyclic_q13_kernel");
+}
+
 template <int LOGN, bool INV, bool NATURAL>
 static void launch_q_dispatch(const ensei_gpu_ctx* ctx, int prime, uint64_t* d, size_t count, cudaStream_t st) {
   constexpr bool TWS = LOGN <= 12;  // tools/tune_ntt.cu sweep: TMA-staged twiddles win up to n = 4096
-  if (ctx->approx_ok) launch_q<LOGN, 3, 0, INV, NATURAL, TWS>(ctx, prime, d, count, st);
-  else launch_q<LOGN, 3, 1, INV, NATURAL, TWS>(ctx, prime, d, count, st);
+  // G = 2 (two polynomials per CTA sharing the staged table: 32 resident warps instead of 24 at
+  // n = 2048, 16 at n = 4096) measured slower: 57.8 vs 65.5 M forward transforms/s at n = 2048,
+  // 26.7 vs 29.3 M at n = 4096 (the 64-register cap and the per-group barriers cost more than
+  // the extra warps bring)
+  constexpr int G = 1;
+  if constexpr (LOGN == 13 && !NATURAL) {
+    if (ctx->approx_ok) return launch_q13<INV>(ctx, prime, d, count, st);
+  }
+  if (ctx->approx_ok) launch_q<LOGN, 3, 0, INV, NATURAL, TWS, G>(ctx, prime, d, count, st);
+  else launch_q<LOGN, 3, 1, INV, NATURAL, TWS, G>(ctx, prime, d, count, st);
 }
 
 template <int LOGN, bool INV, bool NATURAL>

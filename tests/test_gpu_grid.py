@@ -91,3 +91,50 @@ def test_grid_override_refusals():
     w = torch.zeros((1, 1, 3, 3), dtype=torch.int32, device=dev())
     with pytest.raises(EnseiError, match="Unsupported"):
         L.prepare_weights(w)
+
+
+def test_config4_grid_full_shape():
+    """Config 4's real layer (64 -> 128, tcgen05 ElementMult) on the 39x39 grid with five
+    images per block: 163 images = 33 ciphertext images, the last one ragged (3 images).
+    Sampled outputs against the plaintext convolution; ciphertexts of both wire directions
+    and both shares of one full and of the ragged ciphertext image against the oracle."""
+    from paper_2003_05328_b200 import configs as CF
+    from paper_2003_05328_b200 import ops
+    n, H, cin, cout = 8192, 32, 64, 128
+    pack, grid, imgs = CF.CONFIG4_GRID_PACK, CF.CONFIG4_GRID, 163
+    ctx = ops.Context(n=n, q=RNS)
+    g = torch.Generator().manual_seed(4039)
+    x = torch.randint(0, 256, (imgs, cin, H, H), dtype=torch.uint8, generator=g)
+    w = torch.randint(-128, 128, (cout, cin, 3, 3), dtype=torch.int32, generator=g)
+    L = ops.LayerOps(ctx, ops.ConvSpec(H, H, 3, 3, True, cin, cout, pack, grid))
+    assert L.mac_path(imgs) == "tcgen05"
+    _, key = ops.secret_sample(ctx, 43)
+    R = ops.Randomness(seed=43, image_base=10 * pack)
+    we = L.prepare_weights(w.to(dev()))
+    xd = x.to(dev())
+    ct = L.alice_encrypt(key, xd, R)
+    ct_out, bob = L.bob_eval(ct.clone(), we, R, images=imgs)
+    alice = L.alice_decrypt(key, ct_out, images=imgs)
+    out, fa, fb = L.forward(key, we, xd, R, want_shares=True)
+    torch.cuda.synchronize()
+    assert torch.equal(fa, alice) and torch.equal(fb, bob)
+    for i in list(range(0, imgs, 13)) + [imgs - 1]:
+        assert (to_np(out[i]).astype(np.uint64).reshape(-1) == _direct(x[i].numpy(), w.numpy(), H, cin, cout)).all(), i
+    Ls = OP.rns_layers(list(RNS), P, n, H, H, 3, 3, 1, cin, cout, pack, grid)
+    wr = [OP.prepare_weights(Lr, w.numpy(), W) for Lr in Ls]
+    ctx.permute(ct)
+    ctx.permute(ct_out)
+    for c in (7, L.cts(imgs) - 1):
+        pr = OP.PhiloxRandomnessRNS(43, 10 + c, n, list(RNS), P)
+        te = [OP.secret_eval(Lr, pr.secret()) for Lr in Ls]
+        e, a = pr.enc_rns(0, cin, 1)
+        xin = np.zeros((pack, cin, H, H), np.uint64)
+        k = min(pack, imgs - c * pack)
+        xin[:k] = x[c * pack:c * pack + k].numpy()
+        r_ = OP.run_layer_rns(Ls, te, xin, wr, e, a, pr.share(0, cout, 1), W)
+        assert (to_np(ct[c]) == r_["ct_in"]).all(), c
+        assert (to_np(ct_out[c]) == r_["ct_out"]).all(), c
+        al, bo = np.asarray(r_["alice"]).reshape(pack, -1), np.asarray(r_["bob"]).reshape(pack, -1)
+        for pi in range(k):
+            assert (to_np(alice[c * pack + pi]).astype(np.uint64).reshape(-1) == al[pi]).all(), (c, pi)
+            assert (to_np(bob[c * pack + pi]).astype(np.uint64).reshape(-1) == bo[pi]).all(), (c, pi)

@@ -1058,7 +1058,8 @@ def other_config(args, world, rank, local):
         from paper_2003_05328_b200 import configs as CF
         imgs = args.images or CF.CONFIG3_IMAGES
         ctx = ops.Context(n=2048, device=local)
-        sched = CF.CONFIG3_SCHEDULE if args.pack == 1 else CF.CONFIG3_SCHEDULE_PACKED
+        sched = (CF.CONFIG3_SCHEDULE if args.pack == 1 else
+                 CF.CONFIG3_SCHEDULE_PACKED if args.grid == 0 else CF.CONFIG3_SCHEDULE_GRID)
         ws = [torch.randint(-128, 128, s_, dtype=torch.int32, generator=gen) for s_ in CF.CONFIG3_WEIGHTS]
         sess = GP.Session(ctx, sched, 32, 32, ws)
         shard = ImageShard(world * imgs, world, rank)  # contiguous image shards, global image ids
@@ -1066,7 +1067,9 @@ def other_config(args, world, rank, local):
                             generator=torch.Generator().manual_seed(args.seed * 7919 + shard.start))
         x = x_h.to(dev)
         _, key = ops.secret_sample(ctx, args.seed)
-        rands = [ops.Randomness(seed=args.seed, layer=li, image_base=shard.start) for li in range(len(sched))]
+        # ids aligned to every layer's pack (3, 12 and 32 images per block: multiples of 96)
+        id_base = rank * (-(-imgs // 96)) * 96
+        rands = [ops.Randomness(seed=args.seed, layer=li, image_base=id_base) for li in range(len(sched))]
         out3 = {}
         gathered = torch.empty((world * imgs, 16, 8, 8), dtype=torch.int32, device=dev) if world > 1 else None
 
@@ -1081,6 +1084,7 @@ def other_config(args, world, rank, local):
                     "128->128 @16; 128->128 3x3, 128->128 1x1, 128->16 1x1 @8), ReLU, 2x2 max-pool after L2/L4")
         extra["mac_paths"] = [lo.mac_path(imgs) for lo in sess.layers if lo is not None]
         extra["packs"] = [lo.pack for lo in sess.layers if lo is not None]
+        extra["grids"] = [int(lo.geom.Lh) for lo in sess.layers if lo is not None]
         if rank == 0:  # sampled outputs of the last timed step vs the plaintext chain (oracle as checker)
             try:
                 from oracle import protocol as OP

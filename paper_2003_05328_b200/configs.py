@@ -35,6 +35,18 @@ CONFIG3_IMAGES = 64
 # holds (1, 1, 2, 2, 8, 32, 32: the 32x32, 16x16 and 8x8 grids fill 1/2, 1/8, 1/32 of n = 2048)
 CONFIG3_SCHEDULE_PACKED = [Conv(s.fh, s.fw, s.same, s.cin, s.cout, 0) if isinstance(s, Conv) else s
                            for s in CONFIG3_SCHEDULE]
+# the same stack on the smallest grids dividing p - 1 = 2^14 39 that hold each layer's linear
+# convolution (grid override): 39x39 for the 32x32 layers (one block per channel instead of
+# two), 24x24 x 3 images for the 16x16 layers, 12x12 x 12 images for the 8x8 3x3 layer; the
+# 1x1 layers keep REF's 8x8 grid x 32 images
+CONFIG3_GRIDS = [(39, 1), (39, 1), (24, 3), (24, 3), (12, 12), (0, 0), (0, 0)]
+CONFIG3_SCHEDULE_GRID = []
+for _s in CONFIG3_SCHEDULE:
+    if isinstance(_s, Conv):
+        _g, _pk = CONFIG3_GRIDS[sum(isinstance(t, Conv) for t in CONFIG3_SCHEDULE_GRID)]
+        CONFIG3_SCHEDULE_GRID.append(Conv(_s.fh, _s.fw, _s.same, _s.cin, _s.cout, _pk, _g))
+    else:
+        CONFIG3_SCHEDULE_GRID.append(_s)
 CONFIG4_PACK = 2  # two 64x64 grids per n = 8192 block (REF's power-of-two grid)
 # the headline geometry: the smallest grid side dividing p - 1 = 2^14 39 that holds the linear
 # convolution (32 + 3 - 1 = 34 <= 39), five 39x39 grids per n = 8192 block

@@ -123,78 +123,95 @@ static void enc_dispatch_r(const LayerRun& r, int tm, bool inj, int in_t, const 
   fail(ENSEI_ERR_UNSUPPORTED, "padded grid side must be a power of two <= 64 on this path");
 }
 
-// ---- second-generation RNS tile kernels (layer_rns.cuh): n = 8192, 3 primes; 32x32 / 64x64
-// grids (REF's geometry) or a grid override (ensei_conv_desc::grid, direct transform) ----
-template <class GR, int IN_T>
+// ---- second-generation tile kernels (layer_rns.cuh): the 3-prime RNS layer at n = 8192 on
+// 32x32 / 64x64 grids (REF's geometry) or the 39x39 override, and single-prime layers at
+// n = 2048 on an overridden grid (39, 24 or 12: ensei_conv_desc::grid) ----
+template <int LOGN, int R, class GR, int IN_T, bool HOMREC>
 static void enc3_go(const LayerRun& r, const uint64_t* key, uint32_t ks, const void* in, uint64_t* out, int items) {
-  auto k = enc3_kernel<GR, IN_T>;
-  constexpr size_t smem = enc3_smem();
+  auto k = enc3_kernel<LOGN, R, GR, IN_T, HOMREC>;
+  constexpr size_t smem = enc3_smem<LOGN>();
   set_smem_shared_sm(k, smem);
-  k<<<items, kRnsThreads, smem, r.st>>>(r.a, key, ks, in, out);
+  k<<<items, Ring<LOGN>::NT, smem, r.st>>>(r.a, key, ks, in, out);
   check_launch("enc3_kernel");
 }
-template <class GR>
-static bool enc3_try(const LayerRun& r, int in_t, const uint64_t* key, uint32_t ks, const void* in, uint64_t* out,
-                     int items) {
-  if (grid_tile_bytes<GR>(r.a.pk) > (size_t)(1 << kRnsLogN) * 8) return false;  // tiles alias qbuf
-  if (in_t == ENSEI_IN_U8) enc3_go<GR, ENSEI_IN_U8>(r, key, ks, in, out, items);
-  else enc3_go<GR, ENSEI_IN_U32>(r, key, ks, in, out, items);
+template <int LOGN, int R, class GR>
+static bool enc3_try(const LayerRun& r, int tm, int in_t, const uint64_t* key, uint32_t ks, const void* in,
+                     uint64_t* out, int items) {
+  if (grid_tile_bytes<GR>(r.a.pk) > (size_t)(1 << LOGN) * 8) return false;  // tiles alias qbuf
+  if (tm == TILE_HOMREC) enc3_go<LOGN, R, GR, ENSEI_IN_U32, true>(r, key, ks, in, out, items);
+  else if (in_t == ENSEI_IN_U8) enc3_go<LOGN, R, GR, ENSEI_IN_U8, false>(r, key, ks, in, out, items);
+  else enc3_go<LOGN, R, GR, ENSEI_IN_U32, false>(r, key, ks, in, out, items);
   return true;
 }
-template <class GR>
+template <int LOGN, int R, class GR>
 static void share3_go(const LayerRun& r, uint64_t* mask, uint32_t* bob_share, int items) {
-  auto k = share3_kernel<GR>;
-  constexpr size_t smem = share3_smem();
+  auto k = share3_kernel<LOGN, R, GR>;
+  constexpr size_t smem = share3_smem<LOGN>();
   set_smem_shared_sm(k, smem);
-  k<<<items, kRnsThreads, smem, r.st>>>(r.a, mask, bob_share);
+  k<<<items, Ring<LOGN>::NT, smem, r.st>>>(r.a, mask, bob_share);
   check_launch("share3_kernel");
 }
-template <class GR>
+template <int LOGN, int R, class GR>
 static bool dec3_try(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint64_t* ct, uint32_t* alice,
                      const uint32_t* bob, uint32_t* out, int items) {
-  const size_t smem = dec3_smem<GR>(r.a.pk);
-  if (smem > 113 * 1024 || grid_tile_bytes<GR>(r.a.pk) / (GR::kScratch ? 2 : 1) > (size_t)(1 << kRnsLogN) * 8)
+  const size_t smem = dec3_smem<LOGN, GR>(r.a.pk);
+  if (smem > 113 * 1024 || grid_tile_bytes<GR>(r.a.pk) / (GR::kScratch ? 2 : 1) > (size_t)(1 << LOGN) * 8 ||
+      (size_t)r.a.pk * GR::TS * 4 > (size_t)(1 << LOGN) * 6)
     return false;
-  auto k = dec3_kernel<GR>;
+  auto k = dec3_kernel<LOGN, R, GR>;
   set_smem_shared_sm(k, smem);
-  k<<<items, kRnsThreads, smem, r.st>>>(r.a, key, ks, ct, alice, bob, out, 2 * r.ctx->sm_count);
+  k<<<items, Ring<LOGN>::NT, smem, r.st>>>(r.a, key, ks, ct, alice, bob, out, Ring<LOGN>::MINB * r.ctx->sm_count);
   check_launch("dec3_kernel");
   return true;
 }
-template <class GR>
-static void weights3_go(const LayerRun& r, const int32_t* w, uint64_t* out, int items) {
-  auto k = weights3_kernel<GR>;
-  constexpr size_t smem = enc3_smem();
+template <int LOGN, int R, class GR>
+static bool weights3_try(const LayerRun& r, const int32_t* w, uint64_t* out, int items) {
+  if (grid_tile_bytes<GR>(1) > (size_t)(1 << LOGN) * 8) return false;
+  auto k = weights3_kernel<LOGN, R, GR>;
+  constexpr size_t smem = enc3_smem<LOGN>();
   set_smem_shared_sm(k, smem);
-  k<<<items, kRnsThreads, smem, r.st>>>(r.a, w, out);
+  k<<<items, Ring<LOGN>::NT, smem, r.st>>>(r.a, w, out);
   check_launch("weights3_kernel");
+  return true;
 }
-// grid override: the side lengths compiled in (p - 1 = 2^14 39 for the default p: 39 holds a
-// 32x32 image with a filter up to 8x8)
-inline bool grid_supported(int L) { return L == 39; }
 [[noreturn]] inline void grid_fail() {
   fail(ENSEI_ERR_UNSUPPORTED,
-       "grid override: 3-prime RNS layers at n = 8192 with grid = 39, Philox randomness, no HomRec, pack 39^2 <= n");
+       "grid override: 3-prime RNS layers at n = 8192 with grid 39, single-prime layers at n = 2048 with grid 39, 24 "
+       "or 12; Philox randomness; pack x grid^2 <= n and the pack's tiles within the kernels' shared memory");
 }
+// the grid sides compiled in, as (LOGN, R, factors): p - 1 = 2^14 x 3 x 13 for the default p
+#define EG_GRID_CASES(X)  \
+  X(13, 3, 39, 3, 13)     \
+  X(11, 1, 39, 3, 13)     \
+  X(11, 1, 24, 3, 8)      \
+  X(11, 1, 12, 3, 4)
 
 template <int LOGN>
 void launch_tile(const LayerRun& r, int tm, bool inj, int in_t, const uint64_t* key, uint32_t ks, const void* in,
                  uint64_t* out, int items) {
   if (items == 0) return;
   if (r.gridL) {  // grid override: second-generation kernels only
-    if constexpr (LOGN == 13) {
-      if (r.R == 3 && !inj && r.gridL == 39) {
-        if (tm == TILE_WEIGHTS) return weights3_go<GridPFA<3, 13>>(r, static_cast<const int32_t*>(in), out, items);
-        if (tm == TILE_ENC && enc3_try<GridPFA<3, 13>>(r, in_t, key, ks, in, out, items)) return;
-      }
+    if (!inj) {
+#define EG_X(LN, RR, LL, N1, N2)                                                                              \
+  if constexpr (LOGN == LN) {                                                                                 \
+    if (r.R == RR && r.gridL == LL) {                                                                         \
+      if (tm == TILE_WEIGHTS) {                                                                               \
+        if (weights3_try<LN, RR, GridPFA<N1, N2>>(r, static_cast<const int32_t*>(in), out, items)) return;    \
+      } else if (enc3_try<LN, RR, GridPFA<N1, N2>>(r, tm, in_t, key, ks, in, out, items)) {                   \
+        return;                                                                                               \
+      }                                                                                                       \
+    }                                                                                                         \
+  }
+      EG_GRID_CASES(EG_X)
+#undef EG_X
     }
     grid_fail();
   }
   if (r.R == 1) return enc_dispatch_r<LOGN, 1>(r, tm, inj, in_t, key, ks, in, out, items);
   if constexpr (LOGN == 13) {
     if (r.R == 3 && r.tile_gen && tm == TILE_ENC && !inj) {
-      if (r.logL == 6 && enc3_try<GridPow2<6>>(r, in_t, key, ks, in, out, items)) return;
-      if (r.logL == 5 && enc3_try<GridPow2<5>>(r, in_t, key, ks, in, out, items)) return;
+      if (r.logL == 6 && enc3_try<13, 3, GridPow2<6>>(r, tm, in_t, key, ks, in, out, items)) return;
+      if (r.logL == 5 && enc3_try<13, 3, GridPow2<5>>(r, tm, in_t, key, ks, in, out, items)) return;
     }
     if (r.R == 3) return enc_dispatch_r<LOGN, 3>(r, tm, inj, in_t, key, ks, in, out, items);
   }
@@ -248,8 +265,13 @@ template <int LOGN>
 void launch_share(const LayerRun& r, bool inj, uint64_t* mask, uint32_t* bob_share, int items) {
   if (items == 0) return;
   if (r.gridL) {
-    if constexpr (LOGN == 13) {
-      if (r.R == 3 && !inj && r.gridL == 39) return share3_go<GridPFA<3, 13>>(r, mask, bob_share, items);
+    if (!inj) {
+#define EG_X(LN, RR, LL, N1, N2)                                                             \
+  if constexpr (LOGN == LN) {                                                                \
+    if (r.R == RR && r.gridL == LL) return share3_go<LN, RR, GridPFA<N1, N2>>(r, mask, bob_share, items); \
+  }
+      EG_GRID_CASES(EG_X)
+#undef EG_X
     }
     grid_fail();
   }
@@ -259,8 +281,8 @@ void launch_share(const LayerRun& r, bool inj, uint64_t* mask, uint32_t* bob_sha
   }
   if constexpr (LOGN == 13) {
     if (r.R == 3 && !inj && r.tile_gen) {
-      if (r.logL == 6) return share3_go<GridPow2<6>>(r, mask, bob_share, items);
-      if (r.logL == 5) return share3_go<GridPow2<5>>(r, mask, bob_share, items);
+      if (r.logL == 6) return share3_go<13, 3, GridPow2<6>>(r, mask, bob_share, items);
+      if (r.logL == 5) return share3_go<13, 3, GridPow2<5>>(r, mask, bob_share, items);
     }
     if (r.R == 3 && !inj) return share_dispatch<LOGN, 3, false>(r, mask, bob_share, items);
   }
@@ -315,18 +337,21 @@ void launch_dec(const LayerRun& r, const uint64_t* key, uint32_t ks, const uint6
                 const uint32_t* bob, uint32_t* out, int items) {
   if (items == 0) return;
   if (r.gridL) {
-    if constexpr (LOGN == 13) {
-      if (r.R == 3 && r.a.dec_kbits && r.gridL == 39 &&
-          dec3_try<GridPFA<3, 13>>(r, key, ks, ct, alice, bob, out, items))
-        return;
-    }
+#define EG_X(LN, RR, LL, N1, N2)                                                                         \
+  if constexpr (LOGN == LN) {                                                                            \
+    if (r.R == RR && r.gridL == LL && (RR == 1 || r.a.dec_kbits) &&                                      \
+        dec3_try<LN, RR, GridPFA<N1, N2>>(r, key, ks, ct, alice, bob, out, items))                       \
+      return;                                                                                            \
+  }
+    EG_GRID_CASES(EG_X)
+#undef EG_X
     grid_fail();
   }
   if (r.R != 1) {
     if constexpr (LOGN == 13) {
       if (r.R == 3 && r.tile_gen && r.a.dec_kbits) {
-        if (r.logL == 6 && dec3_try<GridPow2<6>>(r, key, ks, ct, alice, bob, out, items)) return;
-        if (r.logL == 5 && dec3_try<GridPow2<5>>(r, key, ks, ct, alice, bob, out, items)) return;
+        if (r.logL == 6 && dec3_try<13, 3, GridPow2<6>>(r, key, ks, ct, alice, bob, out, items)) return;
+        if (r.logL == 5 && dec3_try<13, 3, GridPow2<5>>(r, key, ks, ct, alice, bob, out, items)) return;
       }
       if (r.R == 3) {
         switch (r.logL) {

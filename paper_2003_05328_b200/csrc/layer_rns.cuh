@@ -22,64 +22,83 @@
 
 namespace ensei_gpu {
 
-constexpr int kRnsLogN = 13;
-constexpr int kRnsThreads = 512;
-constexpr int kRnsRounds = 2;  // virtual threads (n / 8) per real thread
+// Thread geometry of a second-generation tile kernel for ring degree 2^LOGN: n / 8 virtual
+// threads (8 coefficients each, radix-8 passes) run by at most 512 real threads in rounds.
+template <int LOGN>
+struct Ring {
+  static constexpr int N = 1 << LOGN, NV = N >> 3;
+  static constexpr int NT = NV < 512 ? NV : 512;  // threads per CTA
+  static constexpr int RD = NV / NT;              // rounds per pass
+  static constexpr int MINB = 1024 / NT;          // CTAs per SM the 64-register budget allows
+};
+constexpr int kRnsLogN = 13;  // the 3-prime RNS layer's ring degree
+constexpr int kRnsThreads = Ring<kRnsLogN>::NT;
 
-// One pass of a transform run by 512 threads as two rounds of virtual threads; in place
-// or between disjoint buffers (no SPLIT: a virtual thread stores exactly where it loaded,
-// or where nobody loads).
-template <class F, class T, int I, bool INV, class Src, class Dst, bool CORR = false>
+// One pass of a transform run as RD rounds of virtual threads; in place or between disjoint
+// buffers (no SPLIT: a virtual thread stores exactly where it loaded, or where nobody loads).
+template <int LOGN, class F, class T, int I, bool INV, class Src, class Dst, bool CORR = false>
 EG_DEV void rns_pass(const F& f, const TwPair<T>* __restrict__ tw, int tid, Src& src, Dst& dst, uint32_t cred = 0) {
   const CtaBar bar;
 #pragma unroll 1
-  for (int rd = 0; rd < kRnsRounds; ++rd)
-    run_pass<F, T, kRnsLogN, 3, I, INV, 0, false, Src, Dst, CtaBar, CORR>(f, tw, tid + rd * kRnsThreads, src, dst, bar,
-                                                                         cred);
+  for (int rd = 0; rd < Ring<LOGN>::RD; ++rd)
+    run_pass<F, T, LOGN, 3, I, INV, 0, false, Src, Dst, CtaBar, CORR>(f, tw, tid + rd * Ring<LOGN>::NT, src, dst, bar,
+                                                                     cred);
 }
 
-// forward: passes 0 (src -> sm), 1..3 (sm), 4 (sm -> dst); no barrier before the first
-// pass or after the last.  B_IN bounds the inputs in units of q.
-template <class F, class T, int B_IN, class Src, class Dst>
+// forward: pass 0 (src -> sm), the middle passes (sm), the last (sm -> dst); no barrier before
+// the first pass or after the last; a warp barrier between the two block-local last passes
+// (ntt_core.cuh pass_sync: rounds keep a block's sets on the same 8 lanes).  B_IN bounds the
+// inputs in units of q.
+template <int LOGN, class F, class T, int B_IN, int I, class Src, class Dst>
+EG_DEV void rns_forward_from(const F& f, const TwPair<T>* __restrict__ tw, T* sm, int tid, Src& src, Dst& dst,
+                             uint32_t cred) {
+  using FB = FwdBounds<F, 0, LOGN, 3, B_IN>;
+  constexpr int L = PassPlan<LOGN, 3>::npass - 1;
+  SmemRW<T> s{sm};
+  if constexpr (I == L) {
+    rns_pass<LOGN, F, T, L, false, SmemRW<T>, Dst, FB::corr(L)>(f, tw, tid, s, dst, cred);
+  } else {
+    if constexpr (I == 0) rns_pass<LOGN, F, T, 0, false, Src, SmemRW<T>, FB::corr(0)>(f, tw, tid, src, s, cred);
+    else rns_pass<LOGN, F, T, I, false, SmemRW<T>, SmemRW<T>, FB::corr(I)>(f, tw, tid, s, s, cred);
+    pass_sync<LOGN, 3, I>(CtaBar{});
+    rns_forward_from<LOGN, F, T, B_IN, I + 1, Src, Dst>(f, tw, sm, tid, src, dst, cred);
+  }
+}
+template <int LOGN, class F, class T, int B_IN, class Src, class Dst>
 EG_DEV void rns_forward(const F& f, const TwPair<T>* __restrict__ tw, T* sm, int tid, Src src, Dst dst,
                         uint32_t cred = 0) {
-  using FB = FwdBounds<F, 0, kRnsLogN, 3, B_IN>;
-  SmemRW<T> s{sm};
-  rns_pass<F, T, 0, false, Src, SmemRW<T>, FB::corr(0)>(f, tw, tid, src, s, cred);
-  __syncthreads();
-  rns_pass<F, T, 1, false, SmemRW<T>, SmemRW<T>, FB::corr(1)>(f, tw, tid, s, s, cred);
-  __syncthreads();
-  rns_pass<F, T, 2, false, SmemRW<T>, SmemRW<T>, FB::corr(2)>(f, tw, tid, s, s, cred);
-  __syncthreads();
-  rns_pass<F, T, 3, false, SmemRW<T>, SmemRW<T>, FB::corr(3)>(f, tw, tid, s, s, cred);
-  // passes 3 and 4 (stages 7..12) work inside 64-element blocks owned by the same 8 lanes
-  // of a warp in both passes and both rounds: a warp barrier is enough
-  __syncwarp();
-  rns_pass<F, T, 4, false, SmemRW<T>, Dst, FB::corr(4)>(f, tw, tid, s, dst, cred);
+  static_assert(PassPlan<LOGN, 3>::npass >= 2, "at least two passes");
+  rns_forward_from<LOGN, F, T, B_IN, 0, Src, Dst>(f, tw, sm, tid, src, dst, cred);
 }
 
-// inverse passes 4 (src -> sm), 3..1 (sm); the caller runs pass 0 (or rns_inverse_last)
-template <class F, class T, class Src>
+// inverse passes L (src -> sm) down to 1 (sm), a barrier after each; the caller runs pass 0
+template <int LOGN, class F, class T, int I, class Src>
+EG_DEV void rns_inverse_from(const F& f, const TwPair<T>* __restrict__ tw, T* sm, int tid, Src& src) {
+  constexpr int L = PassPlan<LOGN, 3>::npass - 1;
+  SmemRW<T> s{sm};
+  if constexpr (I == L) {
+    rns_pass<LOGN, F, T, L, true, Src, SmemRW<T>>(f, tw, tid, src, s);
+    pass_sync<LOGN, 3, L - 1>(CtaBar{});  // passes L and L - 1: the two block-local passes
+  } else {
+    rns_pass<LOGN, F, T, I, true, SmemRW<T>, SmemRW<T>>(f, tw, tid, s, s);
+    __syncthreads();
+  }
+  if constexpr (I > 1) rns_inverse_from<LOGN, F, T, I - 1, Src>(f, tw, sm, tid, src);
+}
+template <int LOGN, class F, class T, class Src>
 EG_DEV void rns_inverse_head(const F& f, const TwPair<T>* __restrict__ tw, T* sm, int tid, Src src) {
-  SmemRW<T> s{sm};
-  rns_pass<F, T, 4, true, Src, SmemRW<T>>(f, tw, tid, src, s);
-  __syncwarp();  // passes 4 and 3 share their 64-element blocks within a warp (see rns_forward)
-  rns_pass<F, T, 3, true, SmemRW<T>, SmemRW<T>>(f, tw, tid, s, s);
-  __syncthreads();
-  rns_pass<F, T, 2, true, SmemRW<T>, SmemRW<T>>(f, tw, tid, s, s);
-  __syncthreads();
-  rns_pass<F, T, 1, true, SmemRW<T>, SmemRW<T>>(f, tw, tid, s, s);
-  __syncthreads();
+  static_assert(PassPlan<LOGN, 3>::npass >= 2, "at least two passes");
+  rns_inverse_from<LOGN, F, T, PassPlan<LOGN, 3>::npass - 1, Src>(f, tw, sm, tid, src);
 }
-template <class F, class T, class Src, class Dst>
+template <int LOGN, class F, class T, class Src, class Dst>
 EG_DEV void rns_inverse(const F& f, const TwPair<T>* __restrict__ tw, T* sm, int tid, Src src, Dst dst) {
-  rns_inverse_head<F, T, Src>(f, tw, sm, tid, src);
+  rns_inverse_head<LOGN, F, T, Src>(f, tw, sm, tid, src);
   SmemRW<T> s{sm};
-  rns_pass<F, T, 0, true, SmemRW<T>, Dst>(f, tw, tid, s, dst);
+  rns_pass<LOGN, F, T, 0, true, SmemRW<T>, Dst>(f, tw, tid, s, dst);
 }
 
-// x * q-ish helper: floor(x C / 2^64) from three wide products (the low x low product and
-// the middle carries are dropped): at most 2 below the exact floor.
+// floor(x C / 2^64) from three wide products (the low x low product and the middle carries
+// are dropped): at most 2 below the exact floor.
 EG_DEV uint64_t mulhi64_approx(uint64_t x, uint64_t c) {
   const uint32_t x0 = lo32(x), x1 = hi32(x), c0 = lo32(c), c1 = hi32(c);
   return mulw(x1, c1) + hi32(mulw(x0, c1)) + hi32(mulw(x1, c0));
@@ -250,8 +269,9 @@ struct GridPFA {
 // -------------------------------------------------------------------- Enc
 // shared: [ qbuf n u64 | pbuf n u32 (padded) | noise n int8 ]; the pk DFT2D tiles alias
 // qbuf (dead once encode_slots' first pass has gathered them).
+template <int LOGN>
 constexpr size_t enc3_smem() {
-  return (size_t)(1 << kRnsLogN) * 8 + ssize<uint32_t>(1 << kRnsLogN) * 4 + (1 << kRnsLogN);
+  return (size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4 + (1 << LOGN);
 }
 // tiles (and the direct transform's scratch copy) that must fit in qbuf's space
 template <class GR>
@@ -261,18 +281,18 @@ constexpr size_t grid_tile_bytes(int nt) {
 
 // slot value at ring position j (natural slot brev(j)); 0 past the packed grids.  TILE0:
 // every pack position reads tile 0 (prepared weights, replicated across the pack)
-template <class GR, bool TILE0 = false>
+template <int LOGN, class GR, bool TILE0 = false>
 EG_DEV uint32_t grid_gather(const uint32_t* S, int j, int pk) {
   int pi, r, c;
-  GR::split(brev(j, kRnsLogN), pi, r, c);
+  GR::split(brev(j, LOGN), pi, r, c);
   return pi >= pk ? 0u : S[(TILE0 ? 0 : pi) * GR::TS + GR::fq(r, c)];
 }
 
-template <class GR, int IN_T>
-__global__ void __launch_bounds__(kRnsThreads, 2)
+template <int LOGN, int R, class GR, int IN_T, bool HOMREC = false>
+__global__ void __launch_bounds__(Ring<LOGN>::NT, Ring<LOGN>::MINB)
     enc3_kernel(const __grid_constant__ LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride,
                 const void* __restrict__ in, uint64_t* __restrict__ out) {
-  constexpr int LOGN = kRnsLogN, N = 1 << LOGN, NT = kRnsThreads, R = 3;
+  constexpr int N = 1 << LOGN, NT = Ring<LOGN>::NT;
   constexpr int TS = GR::TS;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
@@ -300,7 +320,7 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
   }
   // Enc noise e0, two CBD draws per Philox call
   const int gimg = a.image_base / a.pk + img;
-  {
+  if constexpr (!HOMREC) {
     const uint32_t mask = a.cbd_k >= 32 ? 0xFFFFFFFFu : ((1u << a.cbd_k) - 1u);
     const uint64_t sid = stream_id(PURPOSE_NOISE, a.layer, gimg, ch, 0);
     for (int i2 = tid; i2 < N / 2; i2 += NT) {
@@ -314,10 +334,10 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
   GR::template transform<false>(a, S, S + npk * TS, npk);
   // 3. encode_slots: INTT_p of the slots gathered from the tiles
   {
-    auto src = [&](int j) { return grid_gather<GR>(S, j, a.pk); };
+    auto src = [&](int j) { return grid_gather<LOGN, GR>(S, j, a.pk); };
     SmemRW<uint32_t> praw{pbuf};
     auto dst = [&](int i, uint32_t v) { praw(i, Bfly<Field32, 0>::fin_gs(pf, v)); };
-    rns_inverse<Field32, uint32_t>(pf, a.twp_inv, pbuf, tid, src, dst);
+    rns_inverse<LOGN, Field32, uint32_t>(pf, a.twp_inv, pbuf, tid, src, dst);
   }
   __syncthreads();
   const uint64_t* kimg = key + (size_t)img * key_stride;
@@ -330,10 +350,11 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
     auto src = [&](int i) -> uint64_t {
       uint64_t x = mul_shoup_small(f, pbuf[sidx<uint32_t>(i)], pc.delta, pc.delta_shoup);  // < 4q
       if (x >= f.q2) x -= f.q2;
-      return x + signed_mod(ebuf[i], f.q);
+      if constexpr (HOMREC) return x;
+      else return x + signed_mod(ebuf[i], f.q);
     };
     SmemRW<uint64_t> qs{qbuf};
-    rns_forward<Field64, uint64_t, 3>(f, a.twq_fwd[r], qbuf, tid, src, qs, pc.cred);
+    rns_forward<LOGN, Field64, uint64_t, 3>(f, a.twq_fwd[r], qbuf, tid, src, qs, pc.cred);
     __syncthreads();
     // 5. c0 = -a^, c1 = a^ t^ + NTT(Delta m + e); two slots per step, 16-byte accesses
     uint64_t* c0 = ob + (size_t)r * N;
@@ -344,6 +365,13 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
     for (int j2 = tid; j2 < N / 2; j2 += NT) {
       const int j = 2 * j2;
       const ulonglong2 xv = *reinterpret_cast<const ulonglong2*>(qbuf + sidx<uint64_t>(j));
+      if constexpr (HOMREC) {  // HomRec (REF hss.cpp:51-62): c1 += NTT_q(Delta INTT_p(DFT2D(Bob's share)))
+        const ulonglong2 cv = *reinterpret_cast<const ulonglong2*>(c1 + j);
+        const uint64_t y0 = cv.x + Bfly<Field64, 0>::fin_ct(f, xv.x, pc.cred);
+        const uint64_t y1 = cv.y + Bfly<Field64, 0>::fin_ct(f, xv.y, pc.cred);
+        *reinterpret_cast<ulonglong2*>(c1 + j) = make_ulonglong2(y0 >= f.q ? y0 - f.q : y0, y1 >= f.q ? y1 - f.q : y1);
+        continue;
+      }
       const ulonglong2 tv = __ldg(reinterpret_cast<const ulonglong2*>(tk + j));
       const ulonglong2 tpv = __ldg(reinterpret_cast<const ulonglong2*>(tkp + j));
       const int k = brev(j, LOGN);  // natural slot index keys the a^ stream; slot j + 1 -> k + n/2
@@ -365,12 +393,15 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
 // ------------------------------------------------------- HomShare + Bob share
 // shared: [ qbuf n u64 | pbuf n u32 (padded) ]; pbuf first holds s_B in evaluation
 // (bit-reversed) order, Bob's share tile aliases qbuf.
-constexpr size_t share3_smem() { return (size_t)(1 << kRnsLogN) * 8 + ssize<uint32_t>(1 << kRnsLogN) * 4; }
+template <int LOGN>
+constexpr size_t share3_smem() {
+  return (size_t)(1 << LOGN) * 8 + ssize<uint32_t>(1 << LOGN) * 4;
+}
 
-template <class GR>
-__global__ void __launch_bounds__(kRnsThreads, 2)
+template <int LOGN, int R, class GR>
+__global__ void __launch_bounds__(Ring<LOGN>::NT, Ring<LOGN>::MINB)
     share3_kernel(const __grid_constant__ LayerArgs a, uint64_t* __restrict__ mask, uint32_t* __restrict__ bob_share) {
-  constexpr int LOGN = kRnsLogN, N = 1 << LOGN, NT = kRnsThreads, R = 3;
+  constexpr int N = 1 << LOGN, NT = Ring<LOGN>::NT;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
   uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);
@@ -424,16 +455,8 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
       return s == 0 ? 0u : p - s;
     };
     auto dst = [&](int i, uint32_t v) { praw(i, Bfly<Field32, 0>::fin_gs(pf, v)); };
-    // the first pass negates on load: same positions loaded and stored per virtual thread
-    rns_pass<Field32, uint32_t, 4, true>(pf, a.twp_inv, tid, src, praw);
-    __syncwarp();
-    rns_pass<Field32, uint32_t, 3, true>(pf, a.twp_inv, tid, praw, praw);
-    __syncthreads();
-    rns_pass<Field32, uint32_t, 2, true>(pf, a.twp_inv, tid, praw, praw);
-    __syncthreads();
-    rns_pass<Field32, uint32_t, 1, true>(pf, a.twp_inv, tid, praw, praw);
-    __syncthreads();
-    rns_pass<Field32, uint32_t, 0, true>(pf, a.twp_inv, tid, praw, dst);
+    // in place: the first pass negates on load, every virtual thread stores where it loaded
+    rns_inverse<LOGN, Field32, uint32_t>(pf, a.twp_inv, pbuf, tid, src, dst);
   }
   __syncthreads();
   // 4. masks NTT_q(Delta m) land where c1 of the output ciphertext lives
@@ -447,7 +470,7 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
     };
     uint64_t* mo = mask + (size_t)item * ct_words<R>(N) + (size_t)(R + r) * N;
     GlobalOut64Fwd outw{mo, f, pc.cred};
-    rns_forward<Field64, uint64_t, 2>(f, a.twq_fwd[r], qbuf, tid, qsrc, outw, pc.cred);
+    rns_forward<LOGN, Field64, uint64_t, 2>(f, a.twq_fwd[r], qbuf, tid, qsrc, outw, pc.cred);
     __syncthreads();
   }
 }
@@ -489,18 +512,18 @@ __device__ __noinline__ uint32_t dec3_exact(const LayerArgs& a, const uint64_t* 
 // decides.  y_r comes out of the INTT itself: (Q/q_r)^-1 is folded
 // into the n^-1 constants of its last stage (PrimeConst::dec_*).  m overwrites acc_lo, the
 // p-side transform then runs in qbuf's space and scatters into the tiles (over acc).
-template <class GR>
+template <int LOGN, class GR>
 constexpr size_t dec3_smem(int pk) {
-  const size_t acc = (size_t)(1 << kRnsLogN) * 6, tiles = (size_t)pk * GR::TS * 4;
-  return (size_t)(1 << kRnsLogN) * 8 + (acc > tiles ? acc : tiles);
+  const size_t acc = (size_t)(1 << LOGN) * 6, tiles = (size_t)pk * GR::TS * 4;
+  return (size_t)(1 << LOGN) * 8 + (acc > tiles ? acc : tiles);
 }
 
-template <class GR>
-__global__ void __launch_bounds__(kRnsThreads, 2)
+template <int LOGN, int R, class GR>
+__global__ void __launch_bounds__(Ring<LOGN>::NT, Ring<LOGN>::MINB)
     dec3_kernel(const __grid_constant__ LayerArgs a, const uint64_t* __restrict__ key, uint32_t key_stride, const uint64_t* __restrict__ ct,
                 uint32_t* __restrict__ alice_share, const uint32_t* __restrict__ bob_share,
                 uint32_t* __restrict__ outp, int ahead) {
-  constexpr int LOGN = kRnsLogN, N = 1 << LOGN, NT = kRnsThreads, R = 3;
+  constexpr int N = 1 << LOGN, NT = Ring<LOGN>::NT;
   constexpr int TS = GR::TS;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
@@ -535,8 +558,9 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // qbuf: generic reads/writes -> TMA writes
       mbar_expect_tx(&c1_bar, N * 8);
       const uint8_t* c1g = reinterpret_cast<const uint8_t*>(cb + (size_t)(R + r) * N);
-      for (uint32_t off = 0; off < N * 8; off += 32768u)
-        tma_bulk_g2s(reinterpret_cast<uint8_t*>(qbuf) + off, c1g + off, 32768u, &c1_bar);
+      constexpr uint32_t kCopy = N * 8 < 32768 ? N * 8 : 32768;
+      for (uint32_t off = 0; off < N * 8; off += kCopy)
+        tma_bulk_g2s(reinterpret_cast<uint8_t*>(qbuf) + off, c1g + off, kCopy, &c1_bar);
       // the next prime's words (or the first prime's of the tile this SM slot runs next)
       // into L2 while this prime's passes run
       const uint64_t* nb = r + 1 < R ? cb : cb + (size_t)ahead * ct_words<R>(N);
@@ -572,7 +596,25 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
     }
     __syncthreads();
     SmemRW<uint64_t> src{qbuf};
-    rns_inverse_head<Field64, uint64_t>(f, a.twq_inv[r], qbuf, tid, src);
+    rns_inverse_head<LOGN, Field64, uint64_t>(f, a.twq_inv[r], qbuf, tid, src);
+    if constexpr (R == 1) {
+      // one prime: the last pass rounds exactly, floor((p phi + floor(q/2)) / q) mod p (REF
+      // ringbfv.cpp:224-229; the estimate floor(phi cp / 2^64) is at most 2 below, so the
+      // remainder is < 3q and exact in 64 bits), m in natural order into acc_lo
+      const uint64_t cp = pc.cp, h = f.q >> 1;
+      auto dst = [&](int i, uint64_t v) {
+        const uint64_t phi = Bfly<Field64, 0>::fin_gs(f, v);
+        const uint64_t Qe = mulhi64(phi, cp);
+        const uint64_t rem = (uint64_t)p * phi + h - Qe * f.q;
+        const uint32_t Qs = (uint32_t)Qe + (rem >= f.q) + (rem >= f.q2);
+        acc_lo[i] = Qs >= p ? Qs - p : Qs;
+      };
+      SmemRW<uint64_t> qs{qbuf};
+      rns_pass<LOGN, Field64, uint64_t, 0, true>(f, a.twq_inv[0], tid, qs, dst);
+      __syncthreads();
+      continue;
+    }
+    static_assert(R == 1 || LOGN == 13, "the CRT last stage below is written for the 1 + 3 + 3 + 3 + 3 pass plan");
     // last stage (coefficients i, i + n/2) with the CRT constants folded in, then the
     // accumulator
     const TwPair<uint64_t> t1{pc.dec_t1, pc.dec_t1_shoup}, ni{pc.dec_ni, pc.dec_ni_shoup};
@@ -610,7 +652,7 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
       GR::split(brev(j, LOGN), pi, r, c);
       if (pi < a.pk) S[pi * TS + GR::fq(r, c)] = reduce_lazy(pf, v, a.pp.cred);
     };
-    rns_forward<Field32, uint32_t, 1>(pf, a.twp_fwd, pbuf, tid, psrc, pdst);
+    rns_forward<LOGN, Field32, uint32_t, 1>(pf, a.twp_fwd, pbuf, tid, psrc, pdst);
   }
   __syncthreads();
   {  // IDFT2D of every image of the pack at once, crop (+ recombine)
@@ -635,10 +677,10 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
 // ringbfv.cpp:265-280): one CTA per (out, in) filter: pad -> DFT2D -> replicate across the
 // pack -> encode_slots -> centered lift -> NTT_q -> packed 30-bit limbs [cout][cin][1][R][n]
 // (the layout of tile_enc_kernel<TILE_WEIGHTS>, layer.cuh).  Shared memory as Enc.
-template <class GR>
-__global__ void __launch_bounds__(kRnsThreads, 2)
+template <int LOGN, int R, class GR>
+__global__ void __launch_bounds__(Ring<LOGN>::NT, Ring<LOGN>::MINB)
     weights3_kernel(const __grid_constant__ LayerArgs a, const int32_t* __restrict__ w, uint64_t* __restrict__ out) {
-  constexpr int LOGN = kRnsLogN, N = 1 << LOGN, NT = kRnsThreads, R = 3;
+  constexpr int N = 1 << LOGN, NT = Ring<LOGN>::NT;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint64_t* qbuf = reinterpret_cast<uint64_t*>(smem_raw);
   uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);
@@ -659,10 +701,10 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
   __syncthreads();
   GR::template transform<false>(a, S, S + GR::TS, 1);
   {
-    auto src = [&](int j) { return grid_gather<GR, true>(S, j, a.pk); };
+    auto src = [&](int j) { return grid_gather<LOGN, GR, true>(S, j, a.pk); };
     SmemRW<uint32_t> praw{pbuf};
     auto dst = [&](int i, uint32_t v) { praw(i, Bfly<Field32, 0>::fin_gs(pf, v)); };
-    rns_inverse<Field32, uint32_t>(pf, a.twp_inv, pbuf, tid, src, dst);
+    rns_inverse<LOGN, Field32, uint32_t>(pf, a.twp_inv, pbuf, tid, src, dst);
   }
   __syncthreads();
 #pragma unroll 1
@@ -674,7 +716,7 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
       return m > p / 2 ? f.q - (uint64_t)(p - m) : (uint64_t)m;
     };
     SmemRW<uint64_t> qs{qbuf};
-    rns_forward<Field64, uint64_t, 1>(f, a.twq_fwd[r], qbuf, tid, src, qs, pc.cred);
+    rns_forward<LOGN, Field64, uint64_t, 1>(f, a.twq_fwd[r], qbuf, tid, src, qs, pc.cred);
     __syncthreads();
     uint64_t* ob = out + ((size_t)item * R + r) * N;
     for (int j = tid; j < N; j += NT) {

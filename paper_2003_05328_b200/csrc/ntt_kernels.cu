@@ -53,10 +53,10 @@ __global__ void __launch_bounds__(kRnsThreads, 2)
     GlobalIn64 src{g};
     if constexpr (!INV) {
       GlobalOut64<0, true> out{g, f, pc.cred};
-      rns_forward<Field64, uint64_t, 1>(f, tw, qbuf, tid, src, out, pc.cred);
+      rns_forward<kRnsLogN, Field64, uint64_t, 1>(f, tw, qbuf, tid, src, out, pc.cred);
     } else {
       auto dst = [&](int i, uint64_t v) { g[i] = Bfly<Field64, 0>::fin_gs(f, v); };
-      rns_inverse<Field64, uint64_t>(f, tw, qbuf, tid, src, dst);
+      rns_inverse<kRnsLogN, Field64, uint64_t>(f, tw, qbuf, tid, src, dst);
     }
     __syncthreads();
   }

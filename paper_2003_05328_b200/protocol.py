@@ -32,6 +32,7 @@ class Conv:
     cin: int
     cout: int
     pack: int = 1  # images per ciphertext block (builder extension; 0 = the most the ring holds)
+    grid: int = 0  # padded grid side (builder extension, ensei_conv_desc::grid; 0 = REF's power of two)
 
 
 @dataclass
@@ -66,10 +67,10 @@ class Session:
             if isinstance(s, Conv):
                 pk = s.pack
                 if pk == 0:  # the most images one ciphertext block holds (1 when the grid spans blocks)
-                    probe = ops.LayerOps(ctx, ops.ConvSpec(h, w, s.fh, s.fw, s.same, s.cin, s.cout))
+                    probe = ops.LayerOps(ctx, ops.ConvSpec(h, w, s.fh, s.fw, s.same, s.cin, s.cout, 1, s.grid))
                     grid = probe.geom.Lh * probe.geom.Lw
                     pk = max(1, ctx.n // grid) if probe.B == 1 else 1
-                lo = ops.LayerOps(ctx, ops.ConvSpec(h, w, s.fh, s.fw, s.same, s.cin, s.cout, pk))
+                lo = ops.LayerOps(ctx, ops.ConvSpec(h, w, s.fh, s.fw, s.same, s.cin, s.cout, pk, s.grid))
                 wt = weights[ci].to(device=ctx.device, dtype=torch.int32).contiguous()
                 self.layers.append(lo)
                 self.w_eval.append(lo.prepare_weights(wt))

@@ -96,13 +96,16 @@ size_t w_planes_bytes(const ensei_gpu_ctx* c, const LayerArgs& a) {
   return tc_planes_bytes(a.B * (int)c->R * (int)c->n, (a.cout + kTcColsB - 1) / kTcColsB, kTcColsB, a.cin);
 }
 
-// The tcgen05 ElementMult (mac_tc.cuh): chosen automatically for GEMM-sized slots (>= one
-// 32-channel chunk, >= one 64-image / 128-row tile, >= one 16-column tile) within the
-// exact-sum bound K (q_i - 1)^2 < 2^128 (ctx->i8_kmax); forced by variant 5.
+// The tcgen05 ElementMult (mac_tc.cuh): chosen automatically for >= one 32-channel chunk and
+// >= one 16-column tile within the exact-sum bound K (q_i - 1)^2 < 2^128 (ctx->i8_kmax);
+// forced by variant 5.  A mostly empty 128-row tile still beats the IMAD kernels at these
+// channel counts (config 3 on its packed grids: 44, 12 and 4 rows per layer -- 10.2k ->
+// 12.4k images/s with the tensor-core path on every cin >= 32 layer), so there is no row
+// threshold beyond a ciphertext pair.
 bool use_tc(const ensei_gpu_ctx* c, const LayerArgs& a) {
   const int var = mac_variant(), rows = 2 * a.num_images;
   if (!has_w_planes(c, a.cin)) return false;
-  return var == 5 || (var == -1 && rows >= 64 && a.cout >= kTcColsB);
+  return var == 5 || (var == -1 && rows >= 4 && a.cout >= kTcColsB);
 }
 
 // Tile choice (measured on B200, configs 1/3/4; cout <= 2 and cin <= 4 use mac_direct_kernel): 8-slot x 32-row x 16-col tiles with 36-channel

@@ -584,8 +584,30 @@ def run_config1(args, world, rank, local, side=False):
             cpu = {"value": None, "unit": "conv/s", "cores": host_cores(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    # ---- the same layer on the 39x39 grid (grid override: one ciphertext block per channel
+    # instead of two), device timing, CUDA graph replay
+    grid39 = None
+    try:
+        Lg = ops.LayerOps(ctx, ops.ConvSpec(32, 32, 3, 3, True, 16, 16, 1, 39))
+        weg = Lg.prepare_weights(wts)
+        wsg = Lg.workspace(imgs)
+        outg = torch.empty_like(out)
+        for _ in range(2):
+            Lg.forward(key, weg, x, rand, ws=wsg, out=outg)
+        torch.cuda.synchronize()
+        gg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gg):
+            Lg.forward(key, weg, x, rand, ws=wsg, out=outg)
+        tg = _time_steps(gg.replay, args.steps, max(3, args.warmup), flush, stream)
+        grid39 = {"value": world * imgs * args.steps / (tg / 1e3), "unit": "conv/s", "ms_per_step": tg / args.steps,
+                  "outputs_equal": bool(torch.equal(outg, L.forward(key, w_eval, x, rand, ws=ws))),
+                  "geometry": "39x39 padded grid (ensei_conv_desc::grid), 1 block per channel"}
+    except Exception as e:  # noqa: BLE001
+        grid39 = {"value": None, "error": str(e)}
+
     if side:
         return {"value": value, "unit": "conv/s", "ms_per_step": ms_step, "e2e": e2e, "kernel_ms": times,
+                "grid39": grid39,
                 "workload": "config1: 8 images/GPU x 16x32x32, 16->16 3x3 Same, n=2048, single 60-bit q, CUDA graph"}
     if rank == 0:
         line = {
@@ -602,7 +624,7 @@ def run_config1(args, world, rank, local, side=False):
             "roofline": roofline,
             "modmul_per_s": total_modmul * world * args.steps / (total_ms / 1e3),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk, "ntt_config2": ntt,
-            "wire": wire,
+            "wire": wire, "grid39": grid39,
         }
         return line
     return None

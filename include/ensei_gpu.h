@@ -135,8 +135,9 @@ typedef struct {
    * transform on the device too and lets more images share a block (32x32 images, 3x3
    * filter, p - 1 = 2^14 39: L = 39, five images per n = 8192 block instead of two).
    * Outputs are REF's; ciphertexts are the oracle's restatement with the same grid.
-   * Supported for the 3-prime RNS layer at n = 8192 (one layer: no HomRec), any pack with
-   * pack L^2 <= n. */
+   * Supported: the 3-prime RNS layer at n = 8192 with L = 39, and single-prime layers at
+   * n = 2048 with L = 39, 24 or 12 (HomRec included); Philox randomness; any pack with
+   * pack L^2 <= n whose tiles fit the kernels' shared memory (12 images of a 12x12 grid). */
   uint32_t grid;
 } ensei_conv_desc;
 

@@ -209,7 +209,7 @@ void launch_tile(const LayerRun& r, int tm, bool inj, int in_t, const uint64_t* 
   }
   if (r.R == 1) return enc_dispatch_r<LOGN, 1>(r, tm, inj, in_t, key, ks, in, out, items);
   if constexpr (LOGN == 13) {
-    if (r.R == 3 && r.tile_gen && tm == TILE_ENC && !inj) {
+    if (r.R == 3 && r.tile_gen && (tm == TILE_ENC || tm == TILE_HOMREC) && !inj) {
       if (r.logL == 6 && enc3_try<13, 3, GridPow2<6>>(r, tm, in_t, key, ks, in, out, items)) return;
       if (r.logL == 5 && enc3_try<13, 3, GridPow2<5>>(r, tm, in_t, key, ks, in, out, items)) return;
     }

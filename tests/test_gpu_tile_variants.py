@@ -61,6 +61,35 @@ def test_generations_agree(tile_variant, H, pack, imgs, cin, cout):
         assert (to_np(got[1][4][i]).astype(np.uint64).reshape(-1) == _direct(x[i].numpy(), w.numpy(), H, cin, cout)).all(), i
 
 
+@pytest.mark.parametrize("pack,grid", [(1, 0), (2, 0), (5, 39)])
+def test_homrec_rns_generations(tile_variant, pack, grid):
+    """A second RNS layer (HomRec: Bob adds his previous share into the ciphertexts): the
+    second-generation HomRec kernel against the first generation (REF's grids) and the
+    plaintext convolution of the recombined input (every geometry)."""
+    from paper_2003_05328_b200 import ops
+    H, imgs, cin, cout = 32, 7, 3, 2
+    ctx = ops.Context(n=8192, q=RNS)
+    g = torch.Generator().manual_seed(77 + pack)
+    x = torch.randint(0, P, (imgs, cin, H, H), dtype=torch.int32, generator=g)
+    prev = torch.randint(0, P, (imgs, cin, H, H), dtype=torch.int32, generator=g)
+    w = torch.randint(-128, 128, (cout, cin, 3, 3), dtype=torch.int32, generator=g)
+    L = ops.LayerOps(ctx, ops.ConvSpec(H, H, 3, 3, True, cin, cout, pack, grid))
+    _, key = ops.secret_sample(ctx, 19)
+    we = L.prepare_weights(w.to(dev()))
+    R = ops.Randomness(seed=19, image_base=4 * pack)
+    got = {}
+    for v in ((1,) if grid else (0, 1)):
+        tile_variant(v)
+        got[v] = L.forward(key, we, x.to(dev()), R, bob_prev=prev.to(dev()), want_shares=True)
+        torch.cuda.synchronize()
+    if not grid:
+        for a, b in zip(got[0], got[1]):
+            assert torch.equal(a, b)
+    for i in range(imgs):
+        xin = (x[i].numpy().astype(np.int64) + prev[i].numpy()) % P
+        assert (to_np(got[1][0][i]).astype(np.uint64).reshape(-1) == _direct(xin, w.numpy(), H, cin, cout)).all(), i
+
+
 @pytest.mark.parametrize("variant", [0, 1])
 def test_fallback_both_generations(tile_variant, variant):
     """The in-kernel exact-rounding fallback of either generation (crafted ciphertext, 96

@@ -24,8 +24,10 @@ def test_negacyclic_vs_reference(q, n):
         assert (O.negacyclic(x, q, inverse=bool(inv)) == y).all()
 
 
-@pytest.mark.parametrize("L", [2, 4, 8, 16, 32, 64])
+@pytest.mark.parametrize("L", [2, 4, 8, 16, 32, 64, 3, 12, 13, 24, 39])
 def test_ntt2d_vs_reference(L):
+    # the non-powers-of-two take REF's O(L^2) ntt_direct (ntt.cpp:35-49): the lengths of the
+    # device's grid override (12, 24, 39) and their prime-factor pieces
     rng = np.random.default_rng(L)
     x = rng.integers(0, P, size=(3, L, L), dtype=np.uint64)
     for inv in (0, 1):
@@ -86,3 +88,35 @@ def test_reference_rng_restatement():
         r = O.MTRng(seed, salt)
         O.ref_check(O.ref().ref_rng_draw(seed, salt, 1, 1, Q, 0.0, 500, out))
         assert [r.uniform_below(Q) for _ in range(500)] == list(out.astype(np.uint64))
+
+
+@pytest.mark.parametrize("H,grid,pack", [(32, 39, 1), (16, 24, 3), (8, 12, 12)])
+def test_oracle_grid_override_layer_recombines_to_ref_conv(H, grid, pack):
+    """The oracle's layer restatement on an overridden grid (oracle.protocol.set_grid, the
+    checker of the device's ensei_conv_desc::grid) still reconstructs REF's conv_oracle
+    output: the padded side only has to hold the linear convolution and divide p - 1."""
+    from oracle import protocol as OP
+    cin, cout, n = 2, 2, 2048
+    rng = np.random.default_rng(grid)
+    x = rng.integers(0, 256, size=(pack, cin, H, H)).astype(np.uint64)
+    w = rng.integers(-128, 128, size=(cout, cin, 3, 3)).astype(np.int64)
+    L = OP.set_grid(O.layer(Q, P, n, H, H, 3, 3, 1, cin, cout), grid)
+    L.pack = pack
+    assert (L.Lh, L.Lw, L.blocks) == (grid, grid, 1)
+    pr = OP.PhiloxRandomness(9, 0, n, Q, P)
+    te = OP.secret_eval(L, pr.secret())
+    e, a = pr.enc(0, cin, 1)
+    r = OP.run_layer(L, te, x if pack > 1 else x[0], None, OP.prepare_weights(L, w), e, a, pr.share(0, cout, 1))
+    al = np.asarray(r["alice"]).reshape(pack, -1)
+    bo = np.asarray(r["bob"]).reshape(pack, -1)
+    for i in range(pack):
+        want = np.zeros(cout * H * H, np.int64)
+        for o in range(cout):
+            acc = np.zeros(H * H, np.int64)
+            for c in range(cin):
+                y = np.zeros(H * H, np.uint64)
+                O.ref_check(O.ref().ref_conv_oracle(P, x[i, c].astype(np.int64).reshape(-1), H, H,
+                                                    w[o, c].reshape(-1), 3, 3, 1, y))
+                acc = (acc + y.astype(np.int64)) % P
+            want[o * H * H:(o + 1) * H * H] = acc
+        assert (((al[i] + bo[i]) % np.uint64(P)).astype(np.int64) == want).all(), i

@@ -17,7 +17,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-side --no-ntt > $O/ncu_launch.log 2>&1; echo "ncu launches rc=$?" >> $O/status
 # full captures: one launch of each config-4 layer kernel (after warm-up)
 timeout 1200 ncu --set full --import-source on --clock-control none \
-  -k regex:"enc3_kernel|share3_kernel|planes_tc_kernel|mac_tc_kernel|mac_out_kernel|dec3_kernel" --launch-skip 24 -c 6 \
+  -k regex:"enc3_kernel|share3_kernel|planes_tc_kernel|mac_tc_kernel|mac_out_kernel|dec3_kernel" --launch-skip 25 -c 6 \
   -o /tmp/full_c4 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-side --no-ntt > $O/ncu_full_c4.log 2>&1; echo "ncu full c4 rc=$?" >> $O/status
 if [ -f /tmp/full_c4.ncu-rep ]; then
   ncu -i /tmp/full_c4.ncu-rep --page raw --csv > $O/full_c4_raw.csv 2>/dev/null

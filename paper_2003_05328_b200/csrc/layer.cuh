@@ -47,6 +47,8 @@ struct LayerArgs {
   // grid override (layer_rns.cuh GridPFA): primitive L-th root of unity mod p (REF's
   // canonical root, g^((p-1)/L)), its inverse, and L^-1 mod p
   uint32_t grid_w, grid_winv, grid_linv;
+  // Barrett reduction of the tile transforms' lazy sums (< 2^zb): shifts and floor(2^zb / p)
+  uint32_t grid_mu, grid_s1, grid_s2;
   PConst pp;
   const TwPair<uint64_t>* twq_fwd[ENSEI_MAX_PRIMES];
   const TwPair<uint64_t>* twq_inv[ENSEI_MAX_PRIMES];

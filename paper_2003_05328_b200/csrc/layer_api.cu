@@ -162,6 +162,14 @@ LayerRun make_run(const ensei_gpu_ctx* c, const ensei_conv_desc* d, const Geo& g
     a.grid_w = (uint32_t)w;
     a.grid_winv = (uint32_t)host::invmod(w, c->p);
     a.grid_linv = (uint32_t)host::invmod(g.gridL % c->p, c->p);
+    // lazy sums of at most 16 products of residues: z < 16 p^2 < 2^zb
+    uint32_t bp = 0;
+    while ((c->p >> bp) != 0) ++bp;
+    const uint32_t zb = 2 * bp + 4;
+    require(zb <= 62 && zb - bp + 1 < 32 + bp, ENSEI_ERR_UNSUPPORTED, "grid override: p too large for the tile transform");
+    a.grid_s1 = bp - 1;
+    a.grid_s2 = zb - bp + 1;
+    a.grid_mu = (uint32_t)((((unsigned __int128)1) << zb) / c->p);
   }
   a.pp = c->pp;
   a.twp_fwd = c->tab.tw_p_fwd;

@@ -195,6 +195,7 @@ struct GridPFA {
   static constexpr bool kScratch = true;
   static constexpr int A1 = (N2 * small_inv(N2 % N1, N1)) % L, A2 = (N1 * small_inv(N1 % N2, N2)) % L;
   static_assert(small_inv(N2 % N1, N1) && small_inv(N1 % N2, N2), "coprime factors");
+  static_assert(N1 <= 16 && N2 <= 16, "lazy sums of at most 16 products (red64)");
   EG_DEV static int px(int r, int c) { return r * LS + c; }
   EG_DEV static int fq(int r, int c) { return r * LS + c; }
   EG_DEV static void split(int flat, int& pi, int& r, int& c) {
@@ -203,12 +204,17 @@ struct GridPFA {
     r = rem / L;
     c = rem - r * L;
   }
-  EG_DEV static uint32_t red64(const PConst& pp, uint64_t z) {  // z < 2^62 -> canonical
-    const uint64_t qt = mulhi64(z, pp.m64);
-    return pp.f.reduce_once((uint32_t)(z - qt * pp.f.q));
+  // z < 2^zb (zb = grid_zbits: N2 p^2 fits) -> canonical.  Barrett with one wide product:
+  // q^ = ((z >> (bp - 1)) mu) >> (zb - bp + 1), mu = floor(2^zb / p), bp = bits(p): at most 2
+  // below the quotient, so z - q^ p < 3p (the generic 64-bit reduction took four wide products)
+  EG_DEV static uint32_t red64(const LayerArgs& a, uint64_t z) {
+    const uint32_t qh = (uint32_t)((mulw((uint32_t)(z >> a.grid_s1), a.grid_mu)) >> a.grid_s2);
+    uint32_t r = (uint32_t)z - qh * a.pp.f.q;
+    if (r >= a.pp.f.q2) r -= a.pp.f.q2;
+    return a.pp.f.reduce_once(r);
   }
   template <bool COLS>
-  EG_DEV static void lines(const PConst& pp, const uint32_t* M2, const uint32_t* M1, const uint32_t* in,
+  EG_DEV static void lines(const LayerArgs& a, const uint32_t* M2, const uint32_t* M1, const uint32_t* in,
                            uint32_t* out, int nt) {
     constexpr int ST = COLS ? LS : 1;
     for (int it = threadIdx.x; it < nt * L * N2; it += blockDim.x) {
@@ -221,7 +227,7 @@ struct GridPFA {
         uint64_t acc = 0;
 #pragma unroll
         for (int n2 = 0; n2 < N2; ++n2) acc = madw(x[((N2 * n1 + N1 * n2) % L) * ST], m2[n2], acc);
-        y[n1] = red64(pp, acc);
+        y[n1] = red64(a, acc);
       }
       const int kb = (A2 * k2) % L;
 #pragma unroll
@@ -232,7 +238,7 @@ struct GridPFA {
         int k = kb + A1 * k1;
         k = k >= L ? k - L : k;  // kb < L, A1 k1 < L for k1 < N1
         k = k >= L ? k - L : k;
-        out[t * TS + (COLS ? k * LS + ln : ln * LS + k)] = red64(pp, acc);
+        out[t * TS + (COLS ? k * LS + ln : ln * LS + k)] = red64(a, acc);
       }
     }
   }
@@ -259,9 +265,9 @@ struct GridPFA {
       }
     }
     __syncthreads();
-    lines<false>(a.pp, M2, M1, S, scratch, nt);
+    lines<false>(a, M2, M1, S, scratch, nt);
     __syncthreads();
-    lines<true>(a.pp, M2, M1, scratch, S, nt);
+    lines<true>(a, M2, M1, scratch, S, nt);
     __syncthreads();
   }
 };

@@ -809,6 +809,8 @@ def run_config4(args, world, rank, local):
     roofline = {
         "bound": "tensor" if bound == "tensor" else ("hbm" if bound == "hbm" else "imad"), "kernel": dom,
         "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak, "traffic": ncu_traffic("config4", dom),
+        "traffic_note": f"ncu dram__bytes of one launch at the full sub-batch ({chunk} images); achieved / peak are per "
+                        f"average launch ({imgs / nchunks:g} images)",
         "peak_source": {"tensor": i8_src, "imad": "live mad.lo.u32 probe (ensei_gpu_imad_peak)",
                         "hbm": "MEASURED_PEAKS.json hbm_gbs (measured)"}[bound],
         "legs": legs, "per_kernel": per_kernel,

@@ -235,3 +235,32 @@ def test_config3_grid_stack():
     for i in (0, 11, imgs - 1):
         want = OP.plain_protocol(osched, x[i].numpy().astype(np.int64), wnp, RNS[0], P, 2048, W)
         assert (to_np(outs["grid"][i]).astype(np.uint64) == want).all(), i
+
+
+@pytest.mark.parametrize("H,fh,same,grid,pack", [(32, 5, True, 39, 1), (32, 7, True, 39, 1), (32, 3, False, 39, 1),
+                                                 (16, 5, True, 24, 3), (16, 9, False, 24, 2), (8, 5, True, 12, 12),
+                                                 (8, 3, False, 12, 7), (8, 1, True, 12, 3), (20, 3, True, 24, 2)])
+def test_grid_override_filter_shapes(H, fh, same, grid, pack):
+    """Overridden grids with other filter sizes and Valid convolutions (crop origin, output
+    size) at n = 2048: every output equals the plaintext convolution and the run in REF's
+    geometry."""
+    from paper_2003_05328_b200 import ops
+    cin, cout, imgs = 3, 4, 2 * pack + 1
+    ctx = ops.Context(n=2048)
+    g = torch.Generator().manual_seed(H * 100 + fh * 10 + pack)
+    x = torch.randint(0, 256, (imgs, cin, H, H), dtype=torch.uint8, generator=g)
+    w = torch.randint(-128, 128, (cout, cin, fh, fh), dtype=torch.int32, generator=g)
+    _, key = ops.secret_sample(ctx, 5)
+    outs = []
+    for gr, pk in ((grid, pack), (0, 1)):
+        L = ops.LayerOps(ctx, ops.ConvSpec(H, H, fh, fh, same, cin, cout, pk, gr))
+        out = L.forward(key, L.prepare_weights(w.to(dev())), x.to(dev()), ops.Randomness(seed=5, image_base=pk * 3))
+        torch.cuda.synchronize()
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
+    Lo = O.layer(RNS[0], P, 2048, H, H, fh, fh, int(same), cin, cout)
+    for i in range(imgs):
+        want = np.zeros(cout * Lo.oh * Lo.ow, np.uint64)
+        O.lib().eo_conv_direct(C.byref(Lo), x[i].numpy().astype(np.uint64).reshape(-1),
+                               w.numpy().astype(np.int64).reshape(-1), want)
+        assert (to_np(outs[0][i]).astype(np.uint64).reshape(-1) == want).all(), i

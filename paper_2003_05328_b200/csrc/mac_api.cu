@@ -91,9 +91,20 @@ bool use_i8(const ensei_gpu_ctx* c, const LayerArgs& a) {
 // layer can take the tcgen05 ElementMult: 32 <= cin <= ctx->i8_kmax.
 bool has_w_planes(const ensei_gpu_ctx* c, int cin) { return cin >= 32 && cin <= (int)c->i8_kmax; }
 size_t w_words(const ensei_gpu_ctx* c, const LayerArgs& a) { return (size_t)a.cout * a.cin * a.B * c->R * c->n; }
+// Which operand fills the MMA's 128-row side.  The tensor-core kernel multiplies a 128-row
+// tile by 16-row tiles; padding goes to the 128-row side.  With the ciphertext rows there,
+// a batch pays for whole blocks of 64 ciphertexts (config 4's 1024 images = 410 rows cost 512;
+// config 3's packed layers 44, 12 and 4 rows cost 128 each); when the out channels fill
+// 128-row blocks (almost) exactly they take that side instead and the ciphertext rows only
+// pad to 16.  Decided from cout alone (the weight planes are laid out at prepare time).
+bool tc_swap(const LayerArgs& a) {
+  const int padded = (a.cout + kTcRowsA - 1) / kTcRowsA * kTcRowsA;
+  return (padded - a.cout) * 8 <= a.cout;
+}
 size_t w_planes_bytes(const ensei_gpu_ctx* c, const LayerArgs& a) {
   if (!has_w_planes(c, a.cin)) return 0;
-  return tc_planes_bytes(a.B * (int)c->R * (int)c->n, (a.cout + kTcColsB - 1) / kTcColsB, kTcColsB, a.cin);
+  const int T = tc_swap(a) ? kTcRowsA : kTcColsB;
+  return tc_planes_bytes(a.B * (int)c->R * (int)c->n, (a.cout + T - 1) / T, T, a.cin);
 }
 
 // The tcgen05 ElementMult (mac_tc.cuh): chosen automatically for >= one 32-channel chunk and
@@ -139,12 +150,14 @@ void mac_i8_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_
 
 // Byte-plane scratch of the int8 tensor-core MAC (bytes; 0 when the IMAD kernels run).
 // tcgen05 scratch: the ciphertext byte planes, then the slot-major product Y
-size_t tc_a_bytes(const ensei_gpu_ctx* c, const LayerArgs& a) {
-  return tc_planes_bytes(a.B * (int)c->R * (int)c->n, (2 * a.num_images + kTcRowsA - 1) / kTcRowsA, kTcRowsA, a.cin);
+size_t tc_a_bytes(const ensei_gpu_ctx* c, const LayerArgs& a) {  // the ciphertext planes
+  const int T = tc_swap(a) ? kTcColsB : kTcRowsA;
+  return tc_planes_bytes(a.B * (int)c->R * (int)c->n, (2 * a.num_images + T - 1) / T, T, a.cin);
 }
 size_t tc_y_bytes(const ensei_gpu_ctx* c, const LayerArgs& a) {
-  return (size_t)a.B * c->R * c->n * ((2 * a.num_images + kTcRowsA - 1) / kTcRowsA) * kTcRowsA *
-         ((a.cout + kTcColsB - 1) / kTcColsB) * kTcColsB * sizeof(uint64_t);
+  const int big = tc_swap(a) ? a.cout : 2 * a.num_images, small = tc_swap(a) ? 2 * a.num_images : a.cout;
+  return (size_t)a.B * c->R * c->n * ((big + kTcRowsA - 1) / kTcRowsA) * kTcRowsA *
+         ((small + kTcColsB - 1) / kTcColsB) * kTcColsB * sizeof(uint64_t);
 }
 
 size_t mac_scratch_bytes(const ensei_gpu_ctx* c, const LayerArgs& a) {
@@ -199,7 +212,7 @@ bool mac_i8p_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64
 // context scratch), then one mac_tc_kernel pass per 32*NK-channel chunk.  The weight
 // planes follow the packed words of the prepared weights (ensei_gpu_prepare_weights).
 template <int R, int NK>
-void mac_tc_launch(const LayerRun& r, const uint8_t* Ap, const uint8_t* Bp, uint64_t* Y) {
+void mac_tc_launch(const LayerRun& r, const uint8_t* Ap, const uint8_t* Bp, uint64_t* Y, int rows, int cols) {
   auto k = mac_tc_kernel<NK, R>;
   constexpr size_t smem = tc_smem_bytes<NK>();
   set_smem(k, smem);
@@ -207,7 +220,7 @@ void mac_tc_launch(const LayerRun& r, const uint8_t* Ap, const uint8_t* Bp, uint
   for (int kc = 0; kc < nkc; ++kc) {
     ProfScope ps("mac_tc", r.st);
     launch_pdl(k, (unsigned)(r.ctx->sm_count & ~1), kTcThreads, smem, r.st, r.a, (int)r.ctx->logn, Ap, Bp, kc,
-               Y);  // CTA pairs: an even grid
+               Y, rows, cols);  // CTA pairs: an even grid
     check_launch("mac_tc_kernel");
   }
 }
@@ -218,19 +231,32 @@ bool mac_tc_go(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_
   uint8_t* Ap = static_cast<uint8_t*>(scratch ? scratch : ctx_scratch(r, need));
   if (!Ap) return false;
   uint64_t* Y = reinterpret_cast<uint64_t*>(Ap + tc_a_bytes(r.ctx, r.a));
-  const uint8_t* Bp = reinterpret_cast<const uint8_t*>(w + w_words(r.ctx, r.a));
+  const uint8_t* Wp = reinterpret_cast<const uint8_t*>(w + w_words(r.ctx, r.a));
+  const bool swap = tc_swap(r.a);
+  const int rows = 2 * r.a.num_images, cols = r.a.cout;
   {
     ProfScope ps("planes_tc", r.st);
-    launch_pdl(planes_tc_kernel<kTcRowsA, false>, (unsigned)r.ctx->sm_count * 8, 256, 0, r.st, r.a, (int)r.ctx->logn,
-               R, ct, Ap, 2 * r.a.num_images);
+    if (swap)
+      launch_pdl(planes_tc_kernel<kTcColsB, false>, (unsigned)r.ctx->sm_count * 8, 256, 0, r.st, r.a,
+                 (int)r.ctx->logn, R, ct, Ap, rows);
+    else
+      launch_pdl(planes_tc_kernel<kTcRowsA, false>, (unsigned)r.ctx->sm_count * 8, 256, 0, r.st, r.a,
+                 (int)r.ctx->logn, R, ct, Ap, rows);
     check_launch("planes_tc_kernel");
   }
-  if (tc_nk(r.a.cin) == 2) mac_tc_launch<R, 2>(r, Ap, Bp, Y);
-  else mac_tc_launch<R, 1>(r, Ap, Bp, Y);
+  // the 128-row operand first: the weights when swapped (out channels x ciphertext rows)
+  const uint8_t* A = swap ? Wp : Ap;
+  const uint8_t* B = swap ? Ap : Wp;
+  if (tc_nk(r.a.cin) == 2) mac_tc_launch<R, 2>(r, A, B, Y, swap ? cols : rows, swap ? rows : cols);
+  else mac_tc_launch<R, 1>(r, A, B, Y, swap ? cols : rows, swap ? rows : cols);
   {
     ProfScope ps("mac_out", r.st);
-    launch_pdl(mac_out_kernel<R>, (unsigned)r.ctx->sm_count * 8, 256, 0, r.st, r.a, (int)r.ctx->logn,
-               (const uint64_t*)Y, 1, out);
+    if (swap)
+      launch_pdl(mac_out_kernel<R, true>, (unsigned)r.ctx->sm_count * 8, 256, 0, r.st, r.a, (int)r.ctx->logn,
+                 (const uint64_t*)Y, 1, out);
+    else
+      launch_pdl(mac_out_kernel<R, false>, (unsigned)r.ctx->sm_count * 8, 256, 0, r.st, r.a, (int)r.ctx->logn,
+                 (const uint64_t*)Y, 1, out);
     check_launch("mac_out_kernel");
   }
   return true;
@@ -286,8 +312,13 @@ void mac(const LayerRun& r, const uint64_t* ct, const uint64_t* w, uint64_t* out
 void build_w_planes(const LayerRun& r, uint64_t* w_eval) {
   if (!has_w_planes(r.ctx, r.a.cin)) return;
   ProfScope ps("planes_w_tc", r.st);
-  planes_tc_kernel<kTcColsB, true><<<(unsigned)r.ctx->sm_count * 8, 256, 0, r.st>>>(
-      r.a, (int)r.ctx->logn, (int)r.ctx->R, w_eval, reinterpret_cast<uint8_t*>(w_eval + w_words(r.ctx, r.a)), r.a.cout);
+  uint8_t* wp = reinterpret_cast<uint8_t*>(w_eval + w_words(r.ctx, r.a));
+  if (tc_swap(r.a))
+    planes_tc_kernel<kTcRowsA, true><<<(unsigned)r.ctx->sm_count * 8, 256, 0, r.st>>>(
+        r.a, (int)r.ctx->logn, (int)r.ctx->R, w_eval, wp, r.a.cout);
+  else
+    planes_tc_kernel<kTcColsB, true><<<(unsigned)r.ctx->sm_count * 8, 256, 0, r.st>>>(
+        r.a, (int)r.ctx->logn, (int)r.ctx->R, w_eval, wp, r.a.cout);
   check_launch("planes_tc_kernel");
 }
 size_t prepared_weights_bytes(const ensei_gpu_ctx* c, const LayerArgs& a) {

@@ -229,7 +229,7 @@ EG_DEV uint64_t tc_reduce(const Field64& f, const PrimeConst& pc, uint64_t P0, u
 template <int NK, int R>
 __global__ void __launch_bounds__(kTcThreads, 1)
     mac_tc_kernel(LayerArgs a, int logn, const uint8_t* __restrict__ Ap, const uint8_t* __restrict__ Bp, int kc,
-                  uint64_t* __restrict__ Y) {
+                  uint64_t* __restrict__ Y, int rows, int cols) {
   extern __shared__ __align__(1024) uint8_t tc_smem[];
   TcShared& sh = *reinterpret_cast<TcShared*>(tc_smem);
   constexpr size_t A_BYTES = tc_tile_bytes(kTcRowsA, NK), B_BYTES = tc_tile_bytes(kTcColsB, NK);
@@ -245,7 +245,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint8_t* b_buf = a_buf + 2 * A_BYTES;
   const int n = 1 << logn;
   const long S = (long)a.B * R * n, SQ = S / 4;
-  const int rows = 2 * a.num_images, cols = a.cout;
+  // rows = the A operand's side (128-row tiles), cols = the B operand's (16-row tiles): the
+  // ciphertext rows and the out channels, or the other way round (mac_api.cu tc_swap)
   const int nrb = (rows + kTcRowsA - 1) / kTcRowsA, nct = (cols + kTcColsB - 1) / kTcColsB;
   // CTA pairs (2k, 2k+1) walk the same range of (row block, slot quad) units, CTA 2k the
   // quad's first slot pair, 2k+1 its second: the two halves of every 32-byte output sector
@@ -407,61 +408,71 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
 // Y (slot-major MAC product) -> the ciphertext layout out[img][cout][B][2][R][n], + the
 // HomShare mask already in out's c1 words (has_mask).  CTA tile = 64 consecutive slots
-// (same block and prime) x 4 rows x 16 out channels through shared memory: reads are
-// 128-byte rows of Y, writes (and mask reads) 512-byte slot runs per (row, channel).
-constexpr int kTrSlots = 64, kTrRows = 4, kTrCols = 16;
-template <int R>
-__global__ void __launch_bounds__(256) mac_out_kernel(LayerArgs a, int logn, const uint64_t* __restrict__ Y,
+// (same block and prime) x 4 rows x 16 out channels through shared memory (SWAP: 16 rows x 4
+// channels -- Y then is [slot][128-channel block][channel][row], the ElementMult having run
+// with the weights as its 128-row operand): reads are contiguous runs of Y, writes (and mask
+// reads) 512-byte slot runs per (row, channel).
+constexpr int kTrSlots = 64;
+template <int R, bool SWAP>
+__global__ void __launch_bounds__(256, 4) mac_out_kernel(LayerArgs a, int logn, const uint64_t* __restrict__ Y,
                                                       int has_mask, uint64_t* __restrict__ out) {
-  __shared__ uint64_t t[kTrRows * kTrCols][kTrSlots + 1];
+  constexpr int TR = SWAP ? 16 : 4, TC = SWAP ? 4 : 16;  // tile rows / out channels
+  __shared__ uint64_t t[TR * TC][kTrSlots + 1];
   pdl_wait();
   pdl_trigger();
   const int n = 1 << logn;
   const long S = (long)a.B * R * n;
   const int rows = 2 * a.num_images, cols = a.cout;
-  const int nrb = (rows + kTcRowsA - 1) / kTcRowsA, nct = (cols + kTcColsB - 1) / kTcColsB;
-  const int ycols = nct * kTcColsB;
-  const int nrg = (rows + kTrRows - 1) / kTrRows, ncg = (cols + kTrCols - 1) / kTrCols;
+  // Y's row blocks (of its 128-row operand) and row length (its 16-row operand, padded)
+  const int nab = ((SWAP ? cols : rows) + kTcRowsA - 1) / kTcRowsA;
+  const int ylen = (((SWAP ? rows : cols) + kTcColsB - 1) / kTcColsB) * kTcColsB;
+  const int nrg = (rows + TR - 1) / TR, ncg = (cols + TC - 1) / TC;
   const long tiles = (S / kTrSlots) * nrg * ncg;
   const size_t ctw = (size_t)2 * R * n, chan_stride = (size_t)a.B * ctw;
   for (long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int cg = (int)(tile % ncg), rg = (int)((tile / ncg) % nrg);
     const long s0 = tile / ((long)ncg * nrg) * kTrSlots;
-    // gather: thread -> (slot, row, 16-byte column pair); every load of the tile is issued
-    // before the first shared store (8 x 16 B in flight per thread)
-    constexpr int GATHER = kTrSlots * kTrRows * (kTrCols / 2) / 256;
+    // gather: thread -> (slot, index along Y's rows, 16-byte pair along Y's row length); every
+    // load of the tile is issued before the first shared store (8 x 16 B in flight per thread)
+    constexpr int GATHER = kTrSlots * 4 * 8 / 256;
     ulonglong2 v[GATHER];
 #pragma unroll
     for (int u = 0; u < GATHER; ++u) {
       const int e = threadIdx.x + u * 256;
-      const int cp = e % (kTrCols / 2), rr = (e / (kTrCols / 2)) % kTrRows, sl = e / (kTrCols / 2 * kTrRows);
-      const int row = rg * kTrRows + rr, col = cg * kTrCols + 2 * cp;
+      const int cp = e % 8, oth = (e / 8) % 4, sl = e / 32;  // pair along the 16-side, index along the 4-side
+      const int row = rg * TR + (SWAP ? 2 * cp : oth), col = cg * TC + (SWAP ? oth : 2 * cp);
+      const int ya = SWAP ? col : row, yb = SWAP ? row : col;  // Y[(slot, block of ya)][ya % 128][yb]
       v[u] = make_ulonglong2(0, 0);
-      if (row < rows && col < ycols)
+      if (row < rows && col < cols && yb < ylen)
         v[u] = __ldg(reinterpret_cast<const ulonglong2*>(
-            Y + (((size_t)(s0 + sl) * nrb + row / kTcRowsA) * kTcRowsA + row % kTcRowsA) * ycols + col));
+            Y + (((size_t)(s0 + sl) * nab + ya / kTcRowsA) * kTcRowsA + ya % kTcRowsA) * ylen + yb));
     }
 #pragma unroll
     for (int u = 0; u < GATHER; ++u) {
       const int e = threadIdx.x + u * 256;
-      const int cp = e % (kTrCols / 2), rr = (e / (kTrCols / 2)) % kTrRows, sl = e / (kTrCols / 2 * kTrRows);
-      t[rr * kTrCols + 2 * cp][sl] = v[u].x;
-      t[rr * kTrCols + 2 * cp + 1][sl] = v[u].y;
+      const int cp = e % 8, oth = (e / 8) % 4, sl = e / 32;
+      if (SWAP) {  // the pair = rows 2 cp, 2 cp + 1 of channel oth
+        t[(2 * cp) * TC + oth][sl] = v[u].x;
+        t[(2 * cp + 1) * TC + oth][sl] = v[u].y;
+      } else {  // the pair = channels 2 cp, 2 cp + 1 of row oth
+        t[oth * TC + 2 * cp][sl] = v[u].x;
+        t[oth * TC + 2 * cp + 1][sl] = v[u].y;
+      }
     }
     __syncthreads();
     const int bp = (int)(s0 >> logn), b = bp / R, r = bp % R, j0 = (int)(s0 & (n - 1));
     const PrimeConst pc = a.pc[r];
     // scatter: a warp per (row, column) run of 64 slots, 2 slots per lane (16 bytes); the
     // mask loads of the thread's c1 runs are issued first
-    constexpr int SCATTER = kTrRows * kTrCols * (kTrSlots / 2) / 256;
+    constexpr int SCATTER = TR * TC * (kTrSlots / 2) / 256;
     ulonglong2 mk[SCATTER];
     uint64_t* dst[SCATTER];
 #pragma unroll
     for (int u = 0; u < SCATTER; ++u) {
       const int e = threadIdx.x + u * 256;
       const int sp = e % (kTrSlots / 2), rc = e / (kTrSlots / 2);
-      const int rr = rc / kTrCols, cc = rc % kTrCols;
-      const int row = rg * kTrRows + rr, col = cg * kTrCols + cc;
+      const int rr = rc / TC, cc = rc % TC;
+      const int row = rg * TR + rr, col = cg * TC + cc;
       const int img = row >> 1, comp = row & 1;
       dst[u] = (row < rows && col < cols)
                    ? out + ((size_t)img * a.cout + col) * chan_stride + (size_t)b * ctw + (size_t)(comp * R + r) * n +

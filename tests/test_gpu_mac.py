@@ -109,6 +109,11 @@ TC_CASES = [
     (2048, 40, 33, 20, 1),        # partial row tile (80 rows), K = 33 (padded to 64), partial col tile
     (2048, 32, 255, 16, 1),       # the int8 K limit
     (4096, 48, 48, 40, 1),        # K = 48 in one 64-channel chunk, n = 4096
+    # operand swap (out channels on the MMA's 128-row side, ciphertext rows in 16-row tiles):
+    (8192, 13, 64, 128, 3),       # 26 rows: one full 16-row tile + a partial one, three primes
+    (2048, 5, 40, 120, 1),        # cout = 120 (8 padded channels), 10 rows, K = 40
+    (2048, 23, 130, 256, 1),      # two 128-channel blocks, three K passes, 46 rows
+    (2048, 1, 32, 128, 1),        # a single ciphertext (2 rows)
 ]
 
 

@@ -1,22 +1,28 @@
-// layer_rns.cuh -- tile kernels of the 3-prime RNS layer at n = 8192 (config 4), second
-// generation: 512-thread CTAs, two resident per SM.
+// layer_rns.cuh -- second-generation tile kernels (Enc / HomRec, HomShare, Dec, weight
+// preparation), templates over the ring degree, the prime count and the padded-grid policy.
+// Instantiated for the 3-prime RNS layer at n = 8192 (config 4: 512-thread CTAs, two per SM)
+// and for single-prime layers at n = 2048 on overridden grids (configs 3 / 1: 256-thread
+// CTAs, four per SM).
 //
-// The first-generation kernels (layer.cuh) give every (ciphertext image, channel) tile a
-// 1024-thread CTA that fills an SM's register file: all 32 warps are in the same fused
-// stage at the same time, so the load-bound stages (Dec's first INTT pass straight from
+// The first-generation kernels (layer.cuh) give every (ciphertext image, channel) tile at
+// n = 8192 a 1024-thread CTA that fills an SM's register file: all 32 warps are in the same
+// fused stage at the same time, so the load-bound stages (Dec's first INTT pass straight from
 // HBM, Enc's a^ draw, the global stores) never overlap the FMA-bound butterfly passes
-// (ncu, profiles/r02_ncu_summary.md: issue active 42-56 %, one CTA per SM).  Here a tile is
-// owned by 512 threads that run every radix-8 pass in two rounds of 1024 virtual threads
-// (same registers per thread, same shared-memory traffic), and the working set is cut to
-// <= 113 KB by aliasing buffers whose lifetimes do not overlap, so two CTAs in different
-// stages share an SM (an Enc and a HomShare CTA co-reside too).
+// (ncu, profiles/r02a_ncu_summary_first_generation.md: issue active 42-56 %, one CTA per SM).
+// Here a tile is owned by at most 512 threads that run every radix-8 pass in rounds of n / 8
+// virtual threads (same registers per thread, same shared-memory traffic), and the working
+// set is cut to <= 113 KB at n = 8192 by aliasing buffers whose lifetimes do not overlap, so
+// two CTAs in different stages share an SM (an Enc and a HomShare CTA co-reside too).
 //
-// At n = 8192 every supported grid (<= 64 x 64) fits one block per channel: B = 1.
+// One block per channel (B = 1): at n = 8192 every supported grid (<= 64 x 64) fits; at
+// n = 2048 the overridden grids do (39^2, 3 x 24^2, 12 x 12^2 <= 2048).
 //
-//   enc3_kernel    Alice Enc, REF protocol.cpp:310-329 + ringbfv.cpp:180-201 per prime
-//   share3_kernel  Bob HomShare masks + his share, REF hss.cpp:22-49, protocol.cpp:587-603
-//   dec3_kernel    Alice Dec (exact CRT rounding over Q = q0 q1 q2, REF ringbfv.cpp:203-231
-//                  semantics) -> merge -> IDFT2D -> crop (+ recombine), REF protocol.cpp:332-355
+//   enc3_kernel     Alice Enc, REF protocol.cpp:310-329 + ringbfv.cpp:180-201 per prime;
+//                   HOMREC: Bob's HomRec, REF protocol.cpp:543-557, hss.cpp:51-62
+//   share3_kernel   Bob HomShare masks + his share, REF hss.cpp:22-49, protocol.cpp:587-603
+//   dec3_kernel     Alice Dec (REF ringbfv.cpp:203-231; three primes: exact CRT rounding over
+//                   Q = q0 q1 q2) -> merge -> IDFT2D -> crop (+ recombine), REF protocol.cpp:332-355
+//   weights3_kernel Bob's prepare_plain on an overridden grid, REF protocol.cpp:462-502
 #pragma once
 #include "layer.cuh"
 
